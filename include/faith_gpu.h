@@ -1,0 +1,205 @@
+/*
+ * faith_gpu.h -- C ABI of the B200-native bound-propagation library
+ * (paper_2209_12708_b200/_lib/libfaith_gpu.so).
+ *
+ * Drop-in boundary for the hot path of the Faith verifier reproduction
+ * (/root/reference/proj): the free functions of faith::relax / faith::
+ * bounds ops that graph::evaluate calls node by node, the fused bound pass
+ * that replaces graph::evaluate, and the certify / max-epsilon drivers that
+ * replace cli::cmd_verify / cli::cmd_maxeps.  Plain pointers and sizes only.
+ *
+ * Two levels:
+ *   (1) operator level -- host f64 buffers in the reference layout
+ *       (faith::LinearBounds: lw/uw [n, d] row-major, lb/ub [n];
+ *       proj/include/faith/bounds.hpp:34-45).  Each call uploads, runs the same
+ *       CUDA kernels the fused pass uses, and downloads (value semantics, like
+ *       the reference's const&-in / fresh-value-out functions).
+ *   (2) model level -- weights uploaded once (fg_model_create); fg_bound_pass /
+ *       fg_certify / fg_maxeps run whole verification passes for a batch of
+ *       independent sentences with Λ resident in HBM.
+ *
+ * Errors: every entry returns an fg_status.  Numeric failures inside a pass are
+ * reported per sentence with the same taxonomy as the reference's exceptions:
+ *   FG_EINVAL  <- std::invalid_argument (shape mismatch; concretized lo > hi,
+ *                 bounds.cpp:69-78)
+ *   FG_EDOMAIN <- std::domain_error (relax_exp overflow relax.cpp:389-391,
+ *                 relax_recip lo<=0 relax.cpp:406-409, non-finite result
+ *                 graph.cpp:663-671)
+ *   FG_ERANGE  <- std::out_of_range (check_robust true_class, bounds.cpp:144)
+ * fg_last_error() returns a message for the last failing call on a context.
+ * There is no CPU fallback: without a usable sm_100 device fg_ctx_create
+ * fails with FG_ECUDA.
+ */
+#ifndef FAITH_GPU_H
+#define FAITH_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int fg_status;
+#define FG_OK 0
+#define FG_EINVAL 1
+#define FG_EDOMAIN 2
+#define FG_ERANGE 3
+#define FG_ERUNTIME 4 /* std::runtime_error, e.g. "misclassified input" in maxeps */
+#define FG_ECUDA 5
+#define FG_ENOMEM 6
+
+/* faith::Norm (bounds.hpp:12): perturbation norm p; concretization uses dual(p) */
+#define FG_NORM_L1 0
+#define FG_NORM_L2 1
+#define FG_NORM_LINF 2
+
+/* elementwise relaxations (relax.hpp:62-66) */
+#define FG_RELAX_RELU 0
+#define FG_RELAX_TANH 1
+#define FG_RELAX_SILU 2
+#define FG_RELAX_EXP 3
+#define FG_RELAX_RECIP 4
+
+/* faith::relax::DotLayout (relax.hpp:79) */
+#define FG_DOT_SIMILARITY 0
+#define FG_DOT_WEIGHTED_VALUES 1
+
+typedef struct fg_ctx fg_ctx;
+typedef struct fg_model fg_model;
+
+/* ---- context ----------------------------------------------------------- */
+/* One context per (host thread, device).  Fails with FG_ECUDA when the device
+ * is absent or is not compute capability 10.x. */
+fg_status fg_ctx_create(int device, fg_ctx** out);
+void fg_ctx_destroy(fg_ctx* ctx);
+const char* fg_last_error(const fg_ctx* ctx);
+/* Number of kernels this context has launched so far (evidence counter). */
+uint64_t fg_kernel_launches(const fg_ctx* ctx);
+const char* fg_version(void);
+
+/* ---- operator level (host buffers, reference layout) -------------------- */
+/* concretize (bounds.cpp:122-140): lo = lb - eps*||lw||_q, hi = ub + eps*||uw||_q */
+fg_status fg_concretize(fg_ctx* ctx, size_t n, size_t d, const double* lw, const double* lb,
+                        const double* uw, const double* ub, int norm, double eps, double* lo,
+                        double* hi);
+/* check_robust (bounds.cpp:142-157); host-side, no device work */
+fg_status fg_check_robust(size_t n, const double* lo, const double* hi, size_t true_class,
+                          double margin, int* verified);
+/* propagate_affine (relax.cpp:237-307): x is rows x c neurons, w [c, o] row-major,
+ * bias [o] or NULL -> y rows x o neurons */
+fg_status fg_affine(fg_ctx* ctx, size_t rows, size_t c, size_t o, size_t d, const double* xlw,
+                    const double* xlb, const double* xuw, const double* xub, const double* w,
+                    const double* bias, double* ylw, double* ylb, double* yuw, double* yub);
+/* relax_{relu,tanh,silu,exp,recip} (relax.cpp:313-468) */
+fg_status fg_relax(fg_ctx* ctx, int kind, size_t n, const double* lo, const double* hi,
+                   double* a_low, double* b_low, double* a_up, double* b_up);
+/* compose_elementwise (relax.cpp:470-497) */
+fg_status fg_compose(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const double* xlb,
+                     const double* xuw, const double* xub, const double* a_low,
+                     const double* b_low, const double* a_up, const double* b_up, double* ylw,
+                     double* ylb, double* yuw, double* yub);
+/* concretize -> relax_<kind> -> compose as one fused kernel (graph.cpp:484-501) */
+fg_status fg_elementwise_verify(fg_ctx* ctx, int kind, size_t n, size_t d, const double* xlw,
+                                const double* xlb, const double* xuw, const double* xub,
+                                int norm, double eps, double* ylw, double* ylb, double* yuw,
+                                double* yub);
+/* propagate_dot_product (relax.cpp:573-654), batch 1:
+ *   SIMILARITY:      a, b [len, embed]          -> y [heads, len, len]
+ *   WEIGHTED_VALUES: a [heads, len, len], b [len, embed] -> y [len, embed] */
+fg_status fg_dot(fg_ctx* ctx, int layout, size_t len, size_t embed, size_t heads, size_t d,
+                 const double* alw, const double* alb, const double* auw, const double* aub,
+                 const double* blw, const double* blb, const double* buw, const double* bub,
+                 int norm, double eps, double* ylw, double* ylb, double* yuw, double* yub);
+/* propagate_softmax along the last axis of [rows, n] (relax.cpp:777-790), evaluated as
+ * the fused graph does (exp -> sum -> recip -> McCormick multiply, graph.cpp:237-240) */
+fg_status fg_softmax(fg_ctx* ctx, size_t rows, size_t n, size_t d, const double* xlw,
+                     const double* xlb, const double* xuw, const double* xub, int norm,
+                     double eps, double* ylw, double* ylb, double* yuw, double* yub);
+/* propagate_add (relax.cpp:656-674) and propagate_scale (relax.cpp:676-703) */
+fg_status fg_add(fg_ctx* ctx, size_t n, size_t d, const double* alw, const double* alb,
+                 const double* auw, const double* aub, const double* blw, const double* blb,
+                 const double* buw, const double* bub, double* ylw, double* ylb, double* yuw,
+                 double* yub);
+fg_status fg_scale(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const double* xlb,
+                   const double* xuw, const double* xub, double s, double* ylw, double* ylb,
+                   double* yuw, double* yub);
+
+/* ---- model level --------------------------------------------------------- */
+typedef struct {
+  int layers, heads, embed, ffn, length, classes, activation; /* activation: FG_RELAX_* of
+                                                                  relu/tanh/silu */
+} fg_config;
+
+/* params: gen_synthetic order (model.cpp:99-131) -- per layer wq[E,E] bq wk bk wv bv wo bo
+ * w1[E,F] b1 w2[F,E] b2, then wc[E,C] bc; row-major [in, out], f64 values (the reference
+ * stores f32-rounded weights as f64, model.cpp:92). */
+fg_status fg_model_create(fg_ctx* ctx, const fg_config* cfg, const double* params,
+                          fg_model** out);
+void fg_model_destroy(fg_model* model);
+/* Exact f64 forward pass (model::forward, model.cpp:566-571) -> logits[classes]; host. */
+fg_status fg_forward(fg_model* model, const double* x, double* logits);
+
+/* One word-level verification pass (graph::evaluate over fuse_all(build_graph), graph.cpp:
+ * 505-673) for S independent sentences.  x [S, L, E] host f64; positions [S, words];
+ * D = words*E perturbation columns.  eps[S] per sentence.  Outputs per
+ * sentence: logits_lo/hi [S, classes] and status[S] (FG_OK / FG_EINVAL / FG_EDOMAIN). */
+fg_status fg_bound_pass(fg_model* model, int S, const double* x, const int* positions, int words,
+                        int norm, const double* eps, double* logits_lo, double* logits_hi,
+                        int* status);
+/* Debug/parity variant for ONE sentence: also writes the concretized lo/hi of the nodes
+ * the fused pass materialises, in fo_bound_pass node order (oracle/faith_oracle.h);
+ * entries for nodes that stay on chip are NaN.  node_lo/hi sized fg_node_dump_size(). */
+size_t fg_node_dump_size(const fg_config* cfg);
+fg_status fg_bound_pass_dump(fg_model* model, const double* x, const int* positions, int words,
+                             int norm, double eps, double* logits_lo, double* logits_hi,
+                             double* node_lo, double* node_hi, int* status);
+
+/* certify(sentence, p, eps) -- cmd_verify (cli.cpp:64-133) for S sentences:
+ * predicted = argmax(forward); verified = check_robust(concretize(pass), predicted, margin).
+ * bounded[s] = 0 when the pass raised a domain error (cli.cpp:92-94). */
+fg_status fg_certify(fg_model* model, int S, const double* x, const int* positions, int words,
+                     int norm, const double* eps, double margin, int* verified, int* bounded,
+                     int* predicted, double* logits_lo, double* logits_hi, int* status);
+
+/* cmd_maxeps (cli.cpp:135-193) for S sentences: per sentence the same bisection path
+ * (verified_at(0) must hold, then eps_max, then midpoints while hi-lo > tol), all sentences
+ * advancing together on the GPU (continuous batching over `slots` resident sentences;
+ * slots <= 0 picks a default from free HBM).  status[s] = FG_ERUNTIME for a
+ * misclassified input (cli.cpp:159-161). */
+fg_status fg_maxeps(fg_model* model, int S, const double* x, const int* positions, int words,
+                    int norm, double eps_max, double tol, int slots, double* eps_out,
+                    int* calls_out, int* predicted_out, int* status);
+
+/* Synthetic model / inputs with the reference's seeded recipe (model.cpp:87-141):
+ * gen_synthetic weights U(+-0.5/sqrt(fan_in)) rounded to f32, gen_synthetic_input
+ * U(-0.5, 0.5); word positions = `words` distinct Rng(seed).uniform_index(length) draws,
+ * sorted.  fg_param_count() doubles are written to params. */
+size_t fg_param_count(const fg_config* cfg);
+fg_status fg_gen_synthetic(const fg_config* cfg, uint64_t seed, double* params);
+fg_status fg_gen_input(const fg_config* cfg, uint64_t seed, double* x);
+fg_status fg_gen_positions(uint64_t seed, int length, int words, int* positions);
+
+/* Profiling: one eager pass over the sentences resident from the last fg_maxeps /
+ * fg_bound_pass call, with CUDA events around every launch site.  Writes up to
+ * max_sites site names (32 chars each), device ms and kernel counts. */
+fg_status fg_profile_pass(fg_model* model, int norm, double eps, int max_sites, char* names,
+                          double* ms, int* kernels, int* nsites);
+
+/* Timing of the last fg_maxeps / fg_bound_pass call, measured with CUDA events on the
+ * library's stream (device time), and pass counts. */
+typedef struct {
+  double device_ms;      /* total device time of the last call */
+  double pass_ms;        /* mean device time of one batched bound pass */
+  int passes;            /* batched passes run */
+  int slots;             /* sentences resident per pass */
+  uint64_t launches;     /* kernels launched by the last call */
+  double sentence_passes;/* sentence-passes executed (sum over passes of active slots) */
+} fg_run_stats;
+fg_status fg_last_run_stats(const fg_model* model, fg_run_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -858,12 +858,14 @@ typedef struct {
   size_t off;
   int p;
   double eps;
+  int count, max_nodes; /* max_nodes > 0: stop the pass after that many nodes */
 } dumper;
 
-static void dump(dumper* dp, const bnd* b) {
-  if (!dp->lo) return;
-  concretize(b, dp->p, dp->eps, dp->lo + dp->off, dp->hi + dp->off);
+/* returns 1 when the node budget of a prefix pass is exhausted */
+static int dump(dumper* dp, const bnd* b) {
+  if (dp->lo) concretize(b, dp->p, dp->eps, dp->lo + dp->off, dp->hi + dp->off);
   dp->off += b->n;
+  return dp->max_nodes > 0 && ++dp->count >= dp->max_nodes;
 }
 
 static int all_finite(const bnd* b) {
@@ -881,14 +883,14 @@ static int all_finite(const bnd* b) {
     }                          \
   } while (0)
 
-int fo_bound_pass(const fo_config* c, const double* params, const double* x,
-                  const int* positions, int words, int norm, double eps, double* logits_lo,
-                  double* logits_hi, double* node_lo, double* node_hi) {
+static int bound_pass(const fo_config* c, const double* params, const double* x,
+                      const int* positions, int words, int norm, double eps, double* logits_lo,
+                      double* logits_hi, double* node_lo, double* node_hi, int max_nodes) {
   if (!(eps >= 0.0) || !isfinite(eps)) return FO_EINVAL;
   size_t L = (size_t)c->length, E = (size_t)c->embed, H = (size_t)c->heads,
          F = (size_t)c->ffn, C = (size_t)c->classes, D = (size_t)words * E;
   if (words < 1 || H == 0 || E % H != 0) return FO_EINVAL;
-  dumper dp = {node_lo, node_hi, 0, norm, eps};
+  dumper dp = {node_lo, node_hi, 0, norm, eps, 0, max_nodes};
   int st = FO_OK;
   bnd cur = {0}, q = {0}, k = {0}, v = {0}, sc = {0}, scl = {0}, e = {0}, s = {0}, r = {0},
       pr = {0}, ctx = {0}, attn = {0}, res1 = {0}, f1 = {0}, act = {0}, f2 = {0}, sum = {0},
@@ -910,37 +912,37 @@ int fo_bound_pass(const fo_config* c, const double* params, const double* x,
   for (int l = 0; l < c->layers; ++l) {
     layer_w w;
     tail = layer_view(c, params, l, &w);
-    TRY(bnd_alloc(&q, L * E, D)); affine(&cur, L, E, E, w.wq, w.bq, &q); dump(&dp, &q);
-    TRY(bnd_alloc(&k, L * E, D)); affine(&cur, L, E, E, w.wk, w.bk, &k); dump(&dp, &k);
-    TRY(bnd_alloc(&v, L * E, D)); affine(&cur, L, E, E, w.wv, w.bv, &v); dump(&dp, &v);
+    TRY(bnd_alloc(&q, L * E, D)); affine(&cur, L, E, E, w.wq, w.bq, &q); if (dump(&dp, &q)) { st = FO_STOPPED; goto done; }
+    TRY(bnd_alloc(&k, L * E, D)); affine(&cur, L, E, E, w.wk, w.bk, &k); if (dump(&dp, &k)) { st = FO_STOPPED; goto done; }
+    TRY(bnd_alloc(&v, L * E, D)); affine(&cur, L, E, E, w.wv, w.bv, &v); if (dump(&dp, &v)) { st = FO_STOPPED; goto done; }
     TRY(bnd_alloc(&sc, H * L * L, D));
     TRY(dot(FO_DOT_SIMILARITY, L, E, H, &q, &k, norm, eps, &sc));
-    dump(&dp, &sc);
+    if (dump(&dp, &sc)) { st = FO_STOPPED; goto done; }
     bnd_free(&q); bnd_free(&k);
-    TRY(bnd_alloc(&scl, H * L * L, D)); scale(&sc, inv_sqrt_hd, &scl); dump(&dp, &scl);
+    TRY(bnd_alloc(&scl, H * L * L, D)); scale(&sc, inv_sqrt_hd, &scl); if (dump(&dp, &scl)) { st = FO_STOPPED; goto done; }
     bnd_free(&sc);
     TRY(softmax_chain(&scl, H * L, L, norm, eps, &e, &s, &r, &pr));
-    dump(&dp, &e); dump(&dp, &s); dump(&dp, &r); dump(&dp, &pr);
+    if (dump(&dp, &e)) { st = FO_STOPPED; goto done; } if (dump(&dp, &s)) { st = FO_STOPPED; goto done; } if (dump(&dp, &r)) { st = FO_STOPPED; goto done; } if (dump(&dp, &pr)) { st = FO_STOPPED; goto done; }
     bnd_free(&scl); bnd_free(&e); bnd_free(&s); bnd_free(&r);
     TRY(bnd_alloc(&ctx, L * E, D));
     TRY(dot(FO_DOT_WEIGHTED_VALUES, L, E, H, &pr, &v, norm, eps, &ctx));
-    dump(&dp, &ctx);
+    if (dump(&dp, &ctx)) { st = FO_STOPPED; goto done; }
     bnd_free(&pr); bnd_free(&v);
-    TRY(bnd_alloc(&attn, L * E, D)); affine(&ctx, L, E, E, w.wo, w.bo, &attn); dump(&dp, &attn);
+    TRY(bnd_alloc(&attn, L * E, D)); affine(&ctx, L, E, E, w.wo, w.bo, &attn); if (dump(&dp, &attn)) { st = FO_STOPPED; goto done; }
     bnd_free(&ctx);
-    TRY(bnd_alloc(&res1, L * E, D)); add(&cur, &attn, &res1); dump(&dp, &res1);
+    TRY(bnd_alloc(&res1, L * E, D)); add(&cur, &attn, &res1); if (dump(&dp, &res1)) { st = FO_STOPPED; goto done; }
     bnd_free(&cur); bnd_free(&attn);
-    TRY(bnd_alloc(&f1, L * F, D)); affine(&res1, L, E, F, w.w1, w.b1, &f1); dump(&dp, &f1);
+    TRY(bnd_alloc(&f1, L * F, D)); affine(&res1, L, E, F, w.w1, w.b1, &f1); if (dump(&dp, &f1)) { st = FO_STOPPED; goto done; }
     int kind = c->activation == FO_ACT_TANH   ? FO_RELAX_TANH
                : c->activation == FO_ACT_SILU ? FO_RELAX_SILU
                                               : FO_RELAX_RELU;
     TRY(bnd_alloc(&act, L * F, D));
     TRY(elementwise_verify(kind, &f1, norm, eps, &act));
-    dump(&dp, &act);
+    if (dump(&dp, &act)) { st = FO_STOPPED; goto done; }
     bnd_free(&f1);
-    TRY(bnd_alloc(&f2, L * E, D)); affine(&act, L, F, E, w.w2, w.b2, &f2); dump(&dp, &f2);
+    TRY(bnd_alloc(&f2, L * E, D)); affine(&act, L, F, E, w.w2, w.b2, &f2); if (dump(&dp, &f2)) { st = FO_STOPPED; goto done; }
     bnd_free(&act);
-    TRY(bnd_alloc(&cur, L * E, D)); add(&res1, &f2, &cur); dump(&dp, &cur);
+    TRY(bnd_alloc(&cur, L * E, D)); add(&res1, &f2, &cur); if (dump(&dp, &cur)) { st = FO_STOPPED; goto done; }
     bnd_free(&res1); bnd_free(&f2);
   }
   /* MeanPool (graph.cpp:628-634) then the classifier head. */
@@ -948,14 +950,14 @@ int fo_bound_pass(const fo_config* c, const double* params, const double* x,
   sum_axis(&cur, 1, L, E, &sum);
   TRY(bnd_alloc(&pooled, E, D));
   scale(&sum, 1.0 / (double)L, &pooled);
-  dump(&dp, &pooled);
+  if (dump(&dp, &pooled)) { st = FO_STOPPED; goto done; }
   {
     const double* wc = tail;
     const double* bc = wc + E * C;
     TRY(bnd_alloc(&logits, C, D));
     affine(&pooled, 1, E, C, wc, bc, &logits);
   }
-  dump(&dp, &logits);
+  if (dump(&dp, &logits)) { st = FO_STOPPED; goto done; }
   if (!all_finite(&logits)) { /* graph.cpp:663-671 */
     st = FO_EDOMAIN;
     goto done;
@@ -967,6 +969,20 @@ done:
   bnd_free(&res1); bnd_free(&f1); bnd_free(&act); bnd_free(&f2); bnd_free(&sum);
   bnd_free(&pooled); bnd_free(&logits);
   return st;
+}
+
+int fo_bound_pass(const fo_config* c, const double* params, const double* x,
+                  const int* positions, int words, int norm, double eps, double* logits_lo,
+                  double* logits_hi, double* node_lo, double* node_hi) {
+  return bound_pass(c, params, x, positions, words, norm, eps, logits_lo, logits_hi, node_lo,
+                    node_hi, 0);
+}
+
+int fo_bound_pass_prefix(const fo_config* c, const double* params, const double* x,
+                         const int* positions, int words, int norm, double eps, int max_nodes) {
+  double lo[64], hi[64];
+  if (c->classes > 64) return FO_EINVAL;
+  return bound_pass(c, params, x, positions, words, norm, eps, lo, hi, NULL, NULL, max_nodes);
 }
 
 /* cmd_maxeps (cli.cpp:135-193) on the word-level pass. */

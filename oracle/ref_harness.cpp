@@ -112,14 +112,19 @@ md::TransformerSpec spec_from(const fo_config* c, const double* p) {
 
 // Node walk of graph::evaluate over fuse_all(build_graph(spec)), reference
 // operators only.  `x0` is the already-bound input (word-level or identity).
+struct StopWalk {};  // prefix budget reached (fo_bound_pass_prefix)
+
 struct Walk {
   const md::TransformerSpec& s;
   PerturbationSpec ps;
   double* node_lo;
   double* node_hi;
+  int max_nodes = 0;
+  int count = 0;
   std::size_t off = 0;
 
   void dump(const LinearBounds& b) {
+    if (max_nodes > 0 && ++count >= max_nodes) throw StopWalk{};
     if (!node_lo) return;
     ConcreteBounds c = concretize(b, ps);
     std::memcpy(node_lo + off, c.lo.data(), c.lo.numel() * sizeof(double));
@@ -420,6 +425,22 @@ int fo_bound_pass(const fo_config* c, const double* params, const double* x,
     std::memcpy(logits_lo, cb.lo.data(), cb.lo.numel() * sizeof(double));
     std::memcpy(logits_hi, cb.hi.data(), cb.hi.numel() * sizeof(double));
   });
+}
+
+int fo_bound_pass_prefix(const fo_config* c, const double* params, const double* x,
+                         const int* positions, int words, int norm, double eps, int max_nodes) {
+  bool stopped = false;
+  int st = guarded([&] {
+    md::TransformerSpec s = spec_from(c, params);
+    std::size_t D = static_cast<std::size_t>(words) * c->embed;
+    Walk walk{s, PerturbationSpec(to_norm(norm), eps, D), nullptr, nullptr, max_nodes};
+    try {
+      walk.run(word_input(s, x, positions, words));
+    } catch (const StopWalk&) {
+      stopped = true;
+    }
+  });
+  return stopped ? FO_STOPPED : st;
 }
 
 int fo_maxeps(const fo_config* c, const double* params, const double* x, const int* positions,

@@ -1,0 +1,1370 @@
+// fg_host.cu -- C++ host side of libfaith_gpu.so: the C ABI of include/faith_gpu.h.
+//
+//   * operator level: host f64 buffers in the reference layout, uploaded into the
+//     device's center/radius f32 Λ planes, run through the same kernels as the
+//     fused pass, downloaded back (value semantics of proj/src/relax.cpp).
+//   * model level: weights uploaded once; one bound pass = the node sequence of
+//     graph::evaluate over fuse_all(build_graph(spec)) (graph.cpp:531-661,
+//     model.cpp:406-445) as ~11 fused kernels per layer, batched over S
+//     independent sentences, captured once into a CUDA graph and replayed;
+//   * drivers: certify (cli::cmd_verify, cli.cpp:64-133) and the epsilon
+//     bisection (cli::cmd_maxeps, cli.cpp:135-193) with continuous batching.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <future>
+#include <limits>
+#include <memory>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/faith_gpu.h"
+#include "fg_internal.cuh"
+
+using namespace fg;
+
+struct fg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+};
+
+namespace {
+
+const char* kVersion = "faith-b200 0.1 (sm_100a)";
+
+fg_status fail(fg_ctx* ctx, fg_status code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(ctx, FG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));  \
+  } while (0)
+
+// Optional per-launch-site profiler (fg_profile_pass): events around each LAUNCH.
+struct Profiler {
+  struct Site {
+    std::string tag;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    int kernels = 0;
+  };
+  std::vector<Site> sites;
+  cudaStream_t st = nullptr;
+  Site& site(const char* tag) {
+    for (auto& x : sites)
+      if (x.tag == tag) return x;
+    sites.push_back(Site{tag, {}, 0});
+    return sites.back();
+  }
+};
+thread_local Profiler* g_prof = nullptr;
+thread_local const char* g_tag = "other";
+
+struct ProfScope {
+  Profiler::Site* site = nullptr;
+  cudaEvent_t b = nullptr, e = nullptr;
+  ProfScope() {
+    if (!g_prof) return;
+    site = &g_prof->site(g_tag);
+    cudaEventCreate(&b);
+    cudaEventCreate(&e);
+    cudaEventRecord(b, g_prof->st);
+  }
+  void done(int kernels) {
+    if (!site) return;
+    cudaEventRecord(e, g_prof->st);
+    site->ev.emplace_back(b, e);
+    site->kernels += kernels;
+  }
+};
+
+#define LAUNCH(expr)                                                     \
+  do {                                                                   \
+    ProfScope ps_;                                                       \
+    int n_ = (expr);                                                     \
+    ps_.done(n_);                                                        \
+    if (n_ < 0) return fail(ctx, FG_EINVAL, "unsupported shape: " #expr); \
+    ctx->launches += (uint64_t)n_;                                       \
+    cudaError_t e_ = cudaGetLastError();                                 \
+    if (e_ != cudaSuccess)                                               \
+      return fail(ctx, FG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// RAII device allocation
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t alloc(size_t b) {
+    reset();
+    bytes = b ? b : 16;
+    return cudaMalloc(&p, bytes);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+inline int round4(size_t d) { return (int)((d + 3) / 4 * 4); }
+
+fg_status decode_status(int v) {
+  if (v == kStatusClear) return FG_OK;
+  int code = v & 15;
+  return code == kCodeInval ? FG_EINVAL : FG_EDOMAIN;
+}
+
+// Device-resident bound tensor for the operator-level API: n neurons, padded D.
+struct OpBounds {
+  DBuf lam, lb, ub;
+  long long n = 0;
+  int d = 0, Dp = 0;
+  long long cr() const { return n * (long long)Dp; }
+  float* c() const { return lam.as<float>(); }
+};
+
+fg_status op_alloc(fg_ctx* ctx, OpBounds& b, long long n, int d) {
+  b.n = n;
+  b.d = d;
+  b.Dp = round4(d > 0 ? d : 1);
+  CK(b.lam.alloc(sizeof(float) * 2 * (size_t)n * b.Dp));
+  CK(b.lb.alloc(sizeof(double) * (size_t)n));
+  CK(b.ub.alloc(sizeof(double) * (size_t)n));
+  return FG_OK;
+}
+
+fg_status op_upload(fg_ctx* ctx, OpBounds& b, long long n, int d, const double* lw, const double* lb,
+                    const double* uw, const double* ub) {
+  fg_status s = op_alloc(ctx, b, n, d);
+  if (s) return s;
+  DBuf tl, tu;
+  size_t nd = (size_t)n * d;
+  CK(tl.alloc(sizeof(double) * nd));
+  CK(tu.alloc(sizeof(double) * nd));
+  if (nd) {
+    CK(cudaMemcpyAsync(tl.p, lw, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(tu.p, uw, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CK(cudaMemcpyAsync(b.lb.p, lb, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(b.ub.p, ub, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  LAUNCH(launch_ul_to_cr(tl.as<double>(), tu.as<double>(), b.c(), b.cr(), n, d, b.Dp, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return FG_OK;
+}
+
+fg_status op_download(fg_ctx* ctx, const OpBounds& b, double* lw, double* lb, double* uw, double* ub) {
+  DBuf tl, tu;
+  size_t nd = (size_t)b.n * b.d;
+  CK(tl.alloc(sizeof(double) * nd));
+  CK(tu.alloc(sizeof(double) * nd));
+  LAUNCH(launch_cr_to_ul(b.c(), b.cr(), tl.as<double>(), tu.as<double>(), b.n, b.d, b.Dp, ctx->stream));
+  if (nd) {
+    CK(cudaMemcpyAsync(lw, tl.p, sizeof(double) * nd, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(uw, tu.p, sizeof(double) * nd, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaMemcpyAsync(lb, b.lb.p, sizeof(double) * b.n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ub, b.ub.p, sizeof(double) * b.n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return FG_OK;
+}
+
+struct DevScalar {  // eps + status for operator-level calls (one "sentence")
+  DBuf eps, status;
+};
+
+fg_status op_scalar(fg_ctx* ctx, DevScalar& s, double eps) {
+  CK(s.eps.alloc(sizeof(double)));
+  CK(s.status.alloc(sizeof(int)));
+  CK(cudaMemcpyAsync(s.eps.p, &eps, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  LAUNCH(launch_fill_int(s.status.as<int>(), kStatusClear, 1, ctx->stream));
+  return FG_OK;
+}
+
+fg_status op_status(fg_ctx* ctx, DevScalar& s) {
+  int v = 0;
+  CK(cudaMemcpyAsync(&v, s.status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  fg_status st = decode_status(v);
+  if (st == FG_EINVAL) return fail(ctx, st, "invalid_argument: concretized lo > hi");
+  if (st == FG_EDOMAIN) return fail(ctx, st, "domain_error: relaxation domain / overflow");
+  return FG_OK;
+}
+
+bool eps_ok(double eps) { return eps >= 0.0 && std::isfinite(eps); }  // bounds.cpp:38-44
+
+// Weights of one affine layer on the device: W and |W| as f32 [C][O] (M-major
+// GEMM A operand: A[m=j, k=i] = W[i*O + j]), W as f64 for the bias path, bias f64.
+struct DevAffine {
+  DBuf w32, w64, b64;
+  int C = 0, O = 0;
+};
+
+fg_status upload_affine(fg_ctx* ctx, DevAffine& a, int C, int O, const std::vector<double>& w,
+                        const double* bias) {
+  a.C = C;
+  a.O = O;
+  std::vector<float> w32(2 * (size_t)C * O);
+  for (size_t i = 0; i < (size_t)C * O; ++i) {
+    w32[i] = (float)w[i];
+    w32[(size_t)C * O + i] = std::fabs((float)w[i]);
+  }
+  CK(a.w32.alloc(sizeof(float) * w32.size()));
+  CK(a.w64.alloc(sizeof(double) * w.size()));
+  CK(a.b64.alloc(sizeof(double) * O));
+  CK(cudaMemcpy(a.w32.p, w32.data(), sizeof(float) * w32.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(a.w64.p, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+  if (bias) {
+    CK(cudaMemcpy(a.b64.p, bias, sizeof(double) * O, cudaMemcpyHostToDevice));
+  } else {
+    CK(cudaMemset(a.b64.p, 0, sizeof(double) * O));
+  }
+  return FG_OK;
+}
+
+// Λ GEMM of propagate_affine for `rows` token rows per sentence:
+//   out_c = W^T in_c (+res_c),  out_r = |W|^T in_r (+res_r)   (see fg_internal.cuh)
+GemmArgs affine_gemm(const DevAffine& a, const float* in, long long in_cr, float* out,
+                     long long out_cr, const float* res, long long res_cr, long long nrows, int D) {
+  GemmArgs g{};
+  g.M = a.O; g.N = D; g.K = a.C; g.K0 = a.C;
+  g.A = a.w32.as<float>(); g.lda = a.O;
+  g.B = in; g.ldb = D; g.b_off1 = 0;
+  g.C = out; g.ldc = D;
+  g.R = res; g.ldr = D;
+  g.alpha = 1.0f; g.accumulate = 0;
+  g.nb[0] = (int)nrows; g.nb[1] = 2; g.nb[2] = 1; g.nb[3] = 1;
+  g.sA[1] = (long long)a.C * a.O;
+  g.sB[0] = (long long)a.C * D; g.sB[1] = in_cr;
+  g.sC[0] = (long long)a.O * D; g.sC[1] = out_cr;
+  g.sR[0] = (long long)a.O * D; g.sR[1] = res_cr;
+  return g;
+}
+
+}  // namespace
+
+// ============================================================================
+// context
+// ============================================================================
+extern "C" {
+
+const char* fg_version(void) { return kVersion; }
+
+fg_status fg_ctx_create(int device, fg_ctx** out) {
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0)
+    return FG_ECUDA;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) return FG_ECUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return FG_ECUDA;
+  fg_ctx* ctx = new fg_ctx();
+  ctx->device = device;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return FG_ECUDA;
+  }
+  *out = ctx;
+  return FG_OK;
+}
+
+void fg_ctx_destroy(fg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* fg_last_error(const fg_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+uint64_t fg_kernel_launches(const fg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ============================================================================
+// operator level
+// ============================================================================
+fg_status fg_check_robust(size_t n, const double* lo, const double* hi, size_t t, double margin,
+                          int* verified) {
+  if (t >= n) return FG_ERANGE;      // bounds.cpp:144-147
+  if (margin < 0.0) return FG_EINVAL;  // bounds.cpp:148-150
+  *verified = 1;
+  for (size_t j = 0; j < n; ++j) {
+    if (j == t) continue;
+    if (!(lo[t] > hi[j] + margin)) {
+      *verified = 0;
+      break;
+    }
+  }
+  return FG_OK;
+}
+
+fg_status fg_concretize(fg_ctx* ctx, size_t n, size_t d, const double* lw, const double* lb,
+                        const double* uw, const double* ub, int norm, double eps, double* lo,
+                        double* hi) {
+  if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  cudaSetDevice(ctx->device);
+  OpBounds x;
+  fg_status s = op_upload(ctx, x, (long long)n, (int)d, lw, lb, uw, ub);
+  if (s) return s;
+  DevScalar sc;
+  if ((s = op_scalar(ctx, sc, eps))) return s;
+  DBuf dlo, dhi;
+  CK(dlo.alloc(sizeof(double) * n));
+  CK(dhi.alloc(sizeof(double) * n));
+  LAUNCH(launch_concretize(x.c(), x.cr(), x.lb.as<double>(), x.ub.as<double>(), (long long)n,
+                           (long long)n, x.Dp, norm, sc.eps.as<double>(), dlo.as<double>(),
+                           dhi.as<double>(), ctx->stream));
+  CK(cudaMemcpyAsync(lo, dlo.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(hi, dhi.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return FG_OK;
+}
+
+fg_status fg_affine(fg_ctx* ctx, size_t rows, size_t c, size_t o, size_t d, const double* xlw,
+                    const double* xlb, const double* xuw, const double* xub, const double* w,
+                    const double* bias, double* ylw, double* ylb, double* yuw, double* yub) {
+  cudaSetDevice(ctx->device);
+  if (rows == 0 || c == 0 || o == 0) return fail(ctx, FG_EINVAL, "propagate_affine: empty shape");
+  OpBounds x, y;
+  fg_status s = op_upload(ctx, x, (long long)(rows * c), (int)d, xlw, xlb, xuw, xub);
+  if (s) return s;
+  if ((s = op_alloc(ctx, y, (long long)(rows * o), (int)d))) return s;
+  DevAffine a;
+  std::vector<double> wv(w, w + c * o);
+  if ((s = upload_affine(ctx, a, (int)c, (int)o, wv, bias))) return s;
+  LAUNCH(launch_gemm(affine_gemm(a, x.c(), x.cr(), y.c(), y.cr(), nullptr, 0, (long long)rows, x.Dp),
+                     ctx->stream));
+  LAUNCH(launch_affine_bias(x.lb.as<double>(), x.ub.as<double>(), a.w64.as<double>(),
+                            bias ? a.b64.as<double>() : nullptr, nullptr, nullptr, y.lb.as<double>(),
+                            y.ub.as<double>(), 1, (int)rows, (int)c, (int)o, ctx->stream));
+  return op_download(ctx, y, ylw, ylb, yuw, yub);
+}
+
+fg_status fg_relax(fg_ctx* ctx, int kind, size_t n, const double* lo, const double* hi,
+                   double* a_low, double* b_low, double* a_up, double* b_up) {
+  cudaSetDevice(ctx->device);
+  if (kind < 0 || kind > FG_RELAX_RECIP) return fail(ctx, FG_EINVAL, "relax: unknown kind");
+  DBuf dlo, dhi, out;
+  CK(dlo.alloc(sizeof(double) * n));
+  CK(dhi.alloc(sizeof(double) * n));
+  CK(out.alloc(sizeof(double) * 4 * n));
+  CK(cudaMemcpyAsync(dlo.p, lo, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dhi.p, hi, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  DevScalar sc;
+  fg_status s = op_scalar(ctx, sc, 0.0);
+  if (s) return s;
+  double* o = out.as<double>();
+  LAUNCH(launch_relax(kind, dlo.as<double>(), dhi.as<double>(), (long long)n, o, o + n, o + 2 * n,
+                      o + 3 * n, sc.status.as<int>(), ctx->stream));
+  if ((s = op_status(ctx, sc))) return s;
+  std::vector<double> h(4 * n);
+  CK(cudaMemcpy(h.data(), out.p, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+  std::memcpy(a_low, h.data(), sizeof(double) * n);
+  std::memcpy(b_low, h.data() + n, sizeof(double) * n);
+  std::memcpy(a_up, h.data() + 2 * n, sizeof(double) * n);
+  std::memcpy(b_up, h.data() + 3 * n, sizeof(double) * n);
+  return FG_OK;
+}
+
+fg_status fg_compose(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const double* xlb,
+                     const double* xuw, const double* xub, const double* a_low,
+                     const double* b_low, const double* a_up, const double* b_up, double* ylw,
+                     double* ylb, double* yuw, double* yub) {
+  cudaSetDevice(ctx->device);
+  OpBounds x, y;
+  fg_status s = op_upload(ctx, x, (long long)n, (int)d, xlw, xlb, xuw, xub);
+  if (s) return s;
+  if ((s = op_alloc(ctx, y, (long long)n, (int)d))) return s;
+  DBuf rel;
+  CK(rel.alloc(sizeof(double) * 4 * n));
+  double* r = rel.as<double>();
+  CK(cudaMemcpyAsync(r, a_low, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(r + n, b_low, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(r + 2 * n, a_up, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(r + 3 * n, b_up, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  LAUNCH(launch_compose(x.c(), x.cr(), x.lb.as<double>(), x.ub.as<double>(), r, r + n, r + 2 * n,
+                        r + 3 * n, y.c(), y.cr(), y.lb.as<double>(), y.ub.as<double>(), (long long)n,
+                        x.Dp, ctx->stream));
+  return op_download(ctx, y, ylw, ylb, yuw, yub);
+}
+
+fg_status fg_elementwise_verify(fg_ctx* ctx, int kind, size_t n, size_t d, const double* xlw,
+                                const double* xlb, const double* xuw, const double* xub,
+                                int norm, double eps, double* ylw, double* ylb, double* yuw,
+                                double* yub) {
+  if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  cudaSetDevice(ctx->device);
+  OpBounds x;
+  fg_status s = op_upload(ctx, x, (long long)n, (int)d, xlw, xlb, xuw, xub);
+  if (s) return s;
+  DevScalar sc;
+  if ((s = op_scalar(ctx, sc, eps))) return s;
+  LAUNCH(launch_elementwise_verify(kind, x.c(), x.cr(), x.lb.as<double>(), x.ub.as<double>(),
+                                   (long long)n, (long long)n, x.Dp, norm, sc.eps.as<double>(),
+                                   sc.status.as<int>(), 0, nullptr, nullptr, ctx->stream));
+  if ((s = op_status(ctx, sc))) return s;
+  return op_download(ctx, x, ylw, ylb, yuw, yub);
+}
+
+fg_status fg_dot(fg_ctx* ctx, int layout, size_t len, size_t embed, size_t heads, size_t d,
+                 const double* alw, const double* alb, const double* auw, const double* aub,
+                 const double* blw, const double* blb, const double* buw, const double* bub,
+                 int norm, double eps, double* ylw, double* ylb, double* yuw, double* yub) {
+  if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  if (heads == 0 || embed % heads != 0)
+    return fail(ctx, FG_EINVAL, "propagate_dot_product: feature dim not divisible by heads");
+  cudaSetDevice(ctx->device);
+  const int L = (int)len, E = (int)embed, H = (int)heads, hd = E / H;
+  const bool sim = layout == FG_DOT_SIMILARITY;
+  long long na = sim ? (long long)L * E : (long long)H * L * L;
+  long long nb = (long long)L * E;
+  long long ny = sim ? (long long)H * L * L : (long long)L * E;
+  OpBounds a, b, y;
+  fg_status s = op_upload(ctx, a, na, (int)d, alw, alb, auw, aub);
+  if (s) return s;
+  if ((s = op_upload(ctx, b, nb, (int)d, blw, blb, buw, bub))) return s;
+  if ((s = op_alloc(ctx, y, ny, (int)d))) return s;
+  DevScalar sc;
+  if ((s = op_scalar(ctx, sc, eps))) return s;
+  DBuf alo, ahi, blo, bhi, ws;
+  CK(alo.alloc(sizeof(double) * na));
+  CK(ahi.alloc(sizeof(double) * na));
+  CK(blo.alloc(sizeof(double) * nb));
+  CK(bhi.alloc(sizeof(double) * nb));
+  size_t wsz = sim ? 6ull * hd * L * H : (4ull * L * hd + 2ull * L * L) * H;
+  CK(ws.alloc(sizeof(float) * wsz));
+  const int Dp = a.Dp;
+  LAUNCH(launch_concretize(a.c(), a.cr(), a.lb.as<double>(), a.ub.as<double>(), na, na, Dp, norm,
+                           sc.eps.as<double>(), alo.as<double>(), ahi.as<double>(), ctx->stream));
+  LAUNCH(launch_concretize(b.c(), b.cr(), b.lb.as<double>(), b.ub.as<double>(), nb, nb, Dp, norm,
+                           sc.eps.as<double>(), blo.as<double>(), bhi.as<double>(), ctx->stream));
+  NView va{a.c(), a.cr(), a.lb.as<double>(), a.ub.as<double>(), alo.as<double>(), ahi.as<double>(),
+           na, sim ? E : L, 0};
+  NView vb{b.c(), b.cr(), b.lb.as<double>(), b.ub.as<double>(), blo.as<double>(), bhi.as<double>(),
+           nb, E, 0};
+  NView vy{y.c(), y.cr(), y.lb.as<double>(), y.ub.as<double>(), nullptr, nullptr, ny,
+           sim ? L : E, 0};
+  if (sim) {
+    LAUNCH(launch_dot_similarity(va, vb, vy, 1, L, H, hd, Dp, ws.as<float>(), 1.0f, ctx->stream));
+  } else {
+    LAUNCH(launch_dot_weighted(va, vb, vy, 1, L, H, hd, Dp, ws.as<float>(), ctx->stream));
+  }
+  return op_download(ctx, y, ylw, ylb, yuw, yub);
+}
+
+fg_status fg_softmax(fg_ctx* ctx, size_t rows, size_t n, size_t d, const double* xlw,
+                     const double* xlb, const double* xuw, const double* xub, int norm,
+                     double eps, double* ylw, double* ylb, double* yuw, double* yub) {
+  if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  cudaSetDevice(ctx->device);
+  OpBounds x;
+  long long N = (long long)(rows * n);
+  fg_status s = op_upload(ctx, x, N, (int)d, xlw, xlb, xuw, xub);
+  if (s) return s;
+  DevScalar sc;
+  if ((s = op_scalar(ctx, sc, eps))) return s;
+  DBuf lo, hi;
+  CK(lo.alloc(sizeof(double) * N));
+  CK(hi.alloc(sizeof(double) * N));
+  NView v{x.c(), x.cr(), x.lb.as<double>(), x.ub.as<double>(), lo.as<double>(), hi.as<double>(), N,
+          (int)n, 0};
+  LAUNCH(launch_softmax(v, 1, (int)rows, (int)n, x.Dp, norm, sc.eps.as<double>(),
+                        sc.status.as<int>(), 0, 1, ctx->stream));
+  if ((s = op_status(ctx, sc))) return s;
+  return op_download(ctx, x, ylw, ylb, yuw, yub);
+}
+
+fg_status fg_add(fg_ctx* ctx, size_t n, size_t d, const double* alw, const double* alb,
+                 const double* auw, const double* aub, const double* blw, const double* blb,
+                 const double* buw, const double* bub, double* ylw, double* ylb, double* yuw,
+                 double* yub) {
+  cudaSetDevice(ctx->device);
+  OpBounds a, b, y;
+  fg_status s = op_upload(ctx, a, (long long)n, (int)d, alw, alb, auw, aub);
+  if (s) return s;
+  if ((s = op_upload(ctx, b, (long long)n, (int)d, blw, blb, buw, bub))) return s;
+  if ((s = op_alloc(ctx, y, (long long)n, (int)d))) return s;
+  LAUNCH(launch_add(a.c(), a.cr(), a.lb.as<double>(), a.ub.as<double>(), b.c(), b.cr(),
+                    b.lb.as<double>(), b.ub.as<double>(), y.c(), y.cr(), y.lb.as<double>(),
+                    y.ub.as<double>(), (long long)n, a.Dp, ctx->stream));
+  return op_download(ctx, y, ylw, ylb, yuw, yub);
+}
+
+fg_status fg_scale(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const double* xlb,
+                   const double* xuw, const double* xub, double sv, double* ylw, double* ylb,
+                   double* yuw, double* yub) {
+  cudaSetDevice(ctx->device);
+  OpBounds x, y;
+  fg_status s = op_upload(ctx, x, (long long)n, (int)d, xlw, xlb, xuw, xub);
+  if (s) return s;
+  if ((s = op_alloc(ctx, y, (long long)n, (int)d))) return s;
+  LAUNCH(launch_scale(x.c(), x.cr(), x.lb.as<double>(), x.ub.as<double>(), sv, y.c(), y.cr(),
+                      y.lb.as<double>(), y.ub.as<double>(), (long long)n, x.Dp, ctx->stream));
+  return op_download(ctx, y, ylw, ylb, yuw, yub);
+}
+
+}  // extern "C"
+
+// ============================================================================
+// model level
+// ============================================================================
+namespace {
+
+struct DevLayer {
+  DevAffine qkv, wo, w1, w2;
+};
+
+// Pass workspace for S resident sentences.
+struct Workspace {
+  int S = 0, D = 0, W = 0, Ntot = 0;  // slots, pert dim, words, sentences uploaded
+  DBuf X, R1, QF, SC, CTX;            // Λ planes (f32)
+  long long crX = 0, crQKV = 0, crF = 0, crSC = 0;
+  DBuf X_b, R1_b, QKV_b, SC_b, CTX_b, F_b;  // f64 lb/ub(/lo/hi) blocks
+  DBuf pooled, pooled_b, coef;
+  DBuf eps, status, logits, slot_map, x_all, pos_all;
+  DBuf dump_lo, dump_hi;
+  double* h_eps = nullptr;  // pinned
+  int* h_slot = nullptr;
+  double* h_logits = nullptr;
+  int* h_status = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int graph_norm = -1;
+  uint64_t graph_launches = 0;
+  ~Workspace() { release_host(); }
+  void release_host() {
+    if (graph) cudaGraphExecDestroy(graph);
+    graph = nullptr;
+    if (h_eps) cudaFreeHost(h_eps);
+    if (h_slot) cudaFreeHost(h_slot);
+    if (h_logits) cudaFreeHost(h_logits);
+    if (h_status) cudaFreeHost(h_status);
+    h_eps = nullptr;
+    h_slot = nullptr;
+    h_logits = nullptr;
+    h_status = nullptr;
+  }
+};
+
+size_t bytes_per_sentence(const fg_config& c, int D) {
+  size_t L = c.length, E = c.embed, F = c.ffn, H = c.heads;
+  size_t lam = 2 * sizeof(float) * D;
+  size_t qf = std::max(3 * E, F);
+  size_t n_tok = L * E;
+  size_t total = lam * (n_tok * 3 + L * qf + H * L * L)  // X, R1, CTX, QKV/F, SC
+                 + sizeof(double) * (2 * n_tok * 3 + 4 * L * 3 * E + 4 * H * L * L + 2 * L * F) +
+                 2 * sizeof(double) * E * D + sizeof(float) * H * (6 * (E / H) * L + 2 * L * L);
+  return total;
+}
+
+}  // namespace
+
+struct fg_model {
+  fg_ctx* ctx = nullptr;
+  fg_config cfg{};
+  std::vector<double> params;
+  std::vector<DevLayer> layers;
+  DBuf wc64, bc64;
+  Workspace ws;
+  fg_run_stats stats{};
+  // offsets of the layers in params (gen_synthetic order)
+  size_t layer_off(int l) const {
+    size_t e = cfg.embed, f = cfg.ffn;
+    return (size_t)l * (4 * (e * e + e) + e * f + f + f * e + e);
+  }
+};
+
+namespace {
+
+fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot) {
+  fg_ctx* ctx = m->ctx;
+  Workspace& w = m->ws;
+  const fg_config& c = m->cfg;
+  const int D = W * c.embed;
+  if (w.S == S && w.D == D && w.W == W && w.Ntot >= Ntot) return FG_OK;
+  w.release_host();
+  const long long L = c.length, E = c.embed, F = c.ffn, H = c.heads, hd = E / H;
+  const long long nX = S * L * E, nQKV = S * L * 3 * E, nF = S * L * F, nSC = S * H * L * L;
+  w.crX = nX * D;
+  w.crQKV = nQKV * D;
+  w.crF = nF * D;
+  w.crSC = nSC * D;
+  CK(w.X.alloc(sizeof(float) * 2 * w.crX));
+  CK(w.R1.alloc(sizeof(float) * 2 * w.crX));
+  CK(w.CTX.alloc(sizeof(float) * 2 * w.crX));
+  CK(w.QF.alloc(sizeof(float) * 2 * std::max(w.crQKV, w.crF)));
+  CK(w.SC.alloc(sizeof(float) * 2 * w.crSC));
+  CK(w.X_b.alloc(sizeof(double) * 2 * nX));
+  CK(w.R1_b.alloc(sizeof(double) * 2 * nX));
+  CK(w.CTX_b.alloc(sizeof(double) * 4 * nX));
+  CK(w.QKV_b.alloc(sizeof(double) * 4 * nQKV));
+  CK(w.F_b.alloc(sizeof(double) * 4 * nF));
+  CK(w.SC_b.alloc(sizeof(double) * 4 * nSC));
+  CK(w.pooled.alloc(sizeof(double) * 2 * S * E * D));
+  CK(w.pooled_b.alloc(sizeof(double) * 4 * S * E));
+  CK(w.coef.alloc(sizeof(float) * S * H * std::max(6 * hd * L, 4 * L * hd + 2 * L * L)));
+  CK(w.eps.alloc(sizeof(double) * S));
+  CK(w.status.alloc(sizeof(int) * S));
+  CK(w.logits.alloc(sizeof(double) * 2 * S * c.classes));
+  CK(w.slot_map.alloc(sizeof(int) * S));
+  CK(w.x_all.alloc(sizeof(double) * (size_t)std::max(Ntot, 1) * L * E));
+  CK(w.pos_all.alloc(sizeof(int) * (size_t)std::max(Ntot, 1) * W));
+  size_t dmax = std::max({(size_t)nQKV, (size_t)nF, (size_t)nSC});
+  CK(w.dump_lo.alloc(sizeof(double) * dmax));
+  CK(w.dump_hi.alloc(sizeof(double) * dmax));
+  CK(cudaMallocHost(&w.h_eps, sizeof(double) * S));
+  CK(cudaMallocHost(&w.h_slot, sizeof(int) * S));
+  CK(cudaMallocHost(&w.h_logits, sizeof(double) * 2 * S * c.classes));
+  CK(cudaMallocHost(&w.h_status, sizeof(int) * S));
+  w.S = S;
+  w.D = D;
+  w.W = W;
+  w.Ntot = Ntot;
+  return FG_OK;
+}
+
+// Host-side dump helper (S = 1 debug pass): copies device lo/hi into node slots.
+struct Dumper {
+  double* lo = nullptr;
+  double* hi = nullptr;
+  fg_ctx* ctx = nullptr;
+  fg_status copy(size_t off, const double* dlo, const double* dhi, size_t n, size_t src_stride = 1,
+                 size_t src_cols = 0, size_t src_col0 = 0, size_t rows = 0) {
+    if (!lo) return FG_OK;
+    std::vector<double> a, b;
+    size_t total = src_cols ? rows * src_stride : n;
+    a.resize(total);
+    b.resize(total);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(a.data(), dlo, sizeof(double) * total, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), dhi, sizeof(double) * total, cudaMemcpyDeviceToHost));
+    if (!src_cols) {
+      std::memcpy(lo + off, a.data(), sizeof(double) * n);
+      std::memcpy(hi + off, b.data(), sizeof(double) * n);
+    } else {  // strided slice: rows x src_cols starting at src_col0 of each src_stride row
+      for (size_t r = 0; r < rows; ++r)
+        for (size_t k = 0; k < src_cols; ++k) {
+          lo[off + r * src_cols + k] = a[r * src_stride + src_col0 + k];
+          hi[off + r * src_cols + k] = b[r * src_stride + src_col0 + k];
+        }
+    }
+    return FG_OK;
+  }
+};
+
+// One batched bound pass over the resident slots (graph.cpp:531-673 node order).
+// Reads ws.eps / ws.slot_map; writes ws.logits / ws.status.
+fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
+  fg_ctx* ctx = m->ctx;
+  Workspace& w = m->ws;
+  const fg_config& c = m->cfg;
+  const int S = w.S, D = w.D, L = c.length, E = c.embed, F = c.ffn, H = c.heads, hd = E / H;
+  const int C = c.classes;
+  cudaStream_t st = ctx->stream;
+  const long long nX = (long long)S * L * E, nQKV = (long long)S * L * 3 * E,
+                  nF = (long long)S * L * F, nSC = (long long)S * H * L * L;
+  float* X = w.X.as<float>();
+  float* R1 = w.R1.as<float>();
+  float* QKV = w.QF.as<float>();
+  float* Fl = w.QF.as<float>();
+  float* SC = w.SC.as<float>();
+  float* CTX = w.CTX.as<float>();
+  double *X_lb = w.X_b.as<double>(), *X_ub = X_lb + nX;
+  double *R1_lb = w.R1_b.as<double>(), *R1_ub = R1_lb + nX;
+  double *CTX_lb = w.CTX_b.as<double>(), *CTX_ub = CTX_lb + nX, *CTX_lo = CTX_ub + nX,
+         *CTX_hi = CTX_lo + nX;
+  double *Q_lb = w.QKV_b.as<double>(), *Q_ub = Q_lb + nQKV, *Q_lo = Q_ub + nQKV, *Q_hi = Q_lo + nQKV;
+  double *F_lb = w.F_b.as<double>(), *F_ub = F_lb + nF, *F_lo = F_ub + nF, *F_hi = F_lo + nF;
+  double *S_lb = w.SC_b.as<double>(), *S_ub = S_lb + nSC, *S_lo = S_ub + nSC, *S_hi = S_lo + nSC;
+  double* eps = w.eps.as<double>();
+  int* status = w.status.as<int>();
+  double* dlo = w.dump_lo.as<double>();
+  double* dhi = w.dump_hi.as<double>();
+  const size_t per_layer = 8ull * L * E + 4ull * H * L * L + 2ull * H * L + 2ull * L * F;
+  auto site = [](int l, int k) { return l * 8 + k; };
+
+  g_tag = "init";
+  LAUNCH(launch_fill_int(status, kStatusClear, S, st));
+  LAUNCH(launch_init_input(X, w.crX, X_lb, X_ub, w.x_all.as<double>(), w.pos_all.as<int>(),
+                           w.slot_map.as<int>(), S, L, E, w.W, st));
+  for (int l = 0; l < c.layers; ++l) {
+    const DevLayer& lw = m->layers[l];
+    const size_t base = (size_t)l * per_layer;
+    // Q, K, V = propagate_affine(cur, Wq|Wk|Wv)   (one N=3E affine)
+    g_tag = "affine_gemm";
+    LAUNCH(launch_gemm(affine_gemm(lw.qkv, X, w.crX, QKV, w.crQKV, nullptr, 0, (long long)S * L, D), st));
+    g_tag = "affine_bias";
+    LAUNCH(launch_affine_bias(X_lb, X_ub, lw.qkv.w64.as<double>(), lw.qkv.b64.as<double>(), nullptr,
+                              nullptr, Q_lb, Q_ub, S, L, E, 3 * E, st));
+    g_tag = "concretize";
+    LAUNCH(launch_concretize(QKV, w.crQKV, Q_lb, Q_ub, (long long)L * 3 * E, nQKV, D, norm, eps, Q_lo,
+                             Q_hi, st));
+    if (dump) {
+      for (int t = 0; t < 3; ++t)
+        if (fg_status s = dump->copy(base + (size_t)t * L * E, Q_lo, Q_hi, 0, 3 * E, E, (size_t)t * E, L)) return s;
+    }
+    NView q{QKV, w.crQKV, Q_lb, Q_ub, Q_lo, Q_hi, (long long)L * 3 * E, 3 * E, 0};
+    NView k = q, v = q;
+    k.col0 = E;
+    v.col0 = 2 * E;
+    NView sc{SC, w.crSC, S_lb, S_ub, S_lo, S_hi, (long long)H * L * L, L, 0};
+    // scores = DotProduct(q, k); scaled = Scale(scores, 1/sqrt(hd))   (model.cpp:410-418)
+    const double scale = 1.0 / std::sqrt((double)hd);
+    g_tag = "dot_similarity";
+    LAUNCH(launch_dot_similarity(q, k, sc, S, L, H, hd, D, w.coef.as<float>(), (float)scale, st));
+    if (dump) {
+      LAUNCH(launch_concretize(SC, w.crSC, S_lb, S_ub, (long long)H * L * L, nSC, D, norm, eps, dlo, dhi, st));
+      if (fg_status s = dump->copy(base + 3ull * L * E + (size_t)H * L * L, dlo, dhi, (size_t)H * L * L)) return s;
+    }
+    // softmax: exp -> sum -> recip -> mul (graph.cpp:237-240), in place
+    g_tag = "softmax";
+    LAUNCH(launch_softmax(sc, S, H * L, L, D, norm, eps, status, site(l, 0), site(l, 1), st));
+    if (dump) {
+      if (fg_status s = dump->copy(base + 3ull * L * E + 3ull * H * L * L + 2ull * H * L, S_lo, S_hi,
+                                   (size_t)H * L * L)) return s;
+    }
+    // ctx = DotProduct(probs, v)
+    NView cx{CTX, w.crX, CTX_lb, CTX_ub, nullptr, nullptr, (long long)L * E, E, 0};
+    g_tag = "dot_weighted";
+    LAUNCH(launch_dot_weighted(sc, v, cx, S, L, H, hd, D, w.coef.as<float>(), st));
+    const size_t off_ctx = 3ull * L * E + 4ull * H * L * L + 2ull * H * L;
+    if (dump) {
+      LAUNCH(launch_concretize(CTX, w.crX, CTX_lb, CTX_ub, (long long)L * E, nX, D, norm, eps, CTX_lo, CTX_hi, st));
+      if (fg_status s = dump->copy(base + off_ctx, CTX_lo, CTX_hi, (size_t)L * E)) return s;
+    }
+    // res1 = cur + affine(ctx, Wo)
+    g_tag = "affine_gemm";
+    LAUNCH(launch_gemm(affine_gemm(lw.wo, CTX, w.crX, R1, w.crX, X, w.crX, (long long)S * L, D), st));
+    g_tag = "affine_bias";
+    LAUNCH(launch_affine_bias(CTX_lb, CTX_ub, lw.wo.w64.as<double>(), lw.wo.b64.as<double>(), X_lb, X_ub,
+                              R1_lb, R1_ub, S, L, E, E, st));
+    if (dump) {
+      LAUNCH(launch_concretize(R1, w.crX, R1_lb, R1_ub, (long long)L * E, nX, D, norm, eps, dlo, dhi, st));
+      if (fg_status s = dump->copy(base + off_ctx + 2ull * L * E, dlo, dhi, (size_t)L * E)) return s;
+    }
+    // f1 = affine(res1, W1); act = ReluVerify/TanhVerify/SiluVerify(f1)
+    g_tag = "affine_gemm";
+    LAUNCH(launch_gemm(affine_gemm(lw.w1, R1, w.crX, Fl, w.crF, nullptr, 0, (long long)S * L, D), st));
+    g_tag = "affine_bias";
+    LAUNCH(launch_affine_bias(R1_lb, R1_ub, lw.w1.w64.as<double>(), lw.w1.b64.as<double>(), nullptr,
+                              nullptr, F_lb, F_ub, S, L, E, F, st));
+    g_tag = "act_verify";
+    LAUNCH(launch_elementwise_verify(c.activation, Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm,
+                                     eps, status, site(l, 2), dump ? F_lo : nullptr,
+                                     dump ? F_hi : nullptr, st));
+    const size_t off_f1 = off_ctx + 3ull * L * E;
+    if (dump) {
+      if (fg_status s = dump->copy(base + off_f1, F_lo, F_hi, (size_t)L * F)) return s;
+      LAUNCH(launch_concretize(Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm, eps, F_lo, F_hi, st));
+      if (fg_status s = dump->copy(base + off_f1 + (size_t)L * F, F_lo, F_hi, (size_t)L * F)) return s;
+    }
+    // cur = res1 + affine(act, W2)
+    g_tag = "affine_gemm";
+    LAUNCH(launch_gemm(affine_gemm(lw.w2, Fl, w.crF, X, w.crX, R1, w.crX, (long long)S * L, D), st));
+    g_tag = "affine_bias";
+    LAUNCH(launch_affine_bias(F_lb, F_ub, lw.w2.w64.as<double>(), lw.w2.b64.as<double>(), R1_lb, R1_ub,
+                              X_lb, X_ub, S, L, F, E, st));
+    if (dump) {
+      LAUNCH(launch_concretize(X, w.crX, X_lb, X_ub, (long long)L * E, nX, D, norm, eps, dlo, dhi, st));
+      if (fg_status s = dump->copy(base + off_f1 + 2ull * L * F + (size_t)L * E, dlo, dhi, (size_t)L * E)) return s;
+    }
+  }
+  // MeanPool + classifier head + final concretization (graph.cpp:628-634, 663-671; cli.cpp:90)
+  double* pc = w.pooled.as<double>();
+  double* pr = pc + (long long)S * E * D;
+  double* plb = w.pooled_b.as<double>();
+  double* pub = plb + (long long)S * E;
+  double* plo = pub + (long long)S * E;
+  double* phi = plo + (long long)S * E;
+  g_tag = "head";
+  LAUNCH(launch_meanpool(X, w.crX, X_lb, X_ub, pc, pr, plb, pub, S, L, E, D, st));
+  double* lg = w.logits.as<double>();
+  LAUNCH(launch_head(pc, pr, plb, pub, m->wc64.as<double>(), m->bc64.as<double>(), S, E, C, D, norm,
+                     eps, lg, lg + (long long)S * C, status, c.layers * 8, dump ? plo : nullptr,
+                     dump ? phi : nullptr, st));
+  if (dump) {
+    size_t off = (size_t)c.layers * per_layer;
+    if (fg_status s = dump->copy(off, plo, phi, (size_t)E)) return s;
+    if (fg_status s = dump->copy(off + E, lg, lg + C, (size_t)C)) return s;
+  }
+  return FG_OK;
+}
+
+bool use_graphs() {
+  const char* e = std::getenv("FG_NO_GRAPH");
+  return !(e && e[0] == '1');
+}
+
+// Runs one pass over all slots; eps/slot_map must be staged in the pinned host
+// buffers.  Results land in w.h_logits / w.h_status after the call returns.
+fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, float* ms) {
+  fg_ctx* ctx = m->ctx;
+  Workspace& w = m->ws;
+  cudaStream_t st = ctx->stream;
+  const int S = w.S, C = m->cfg.classes;
+  CK(cudaMemcpyAsync(w.eps.p, w.h_eps, sizeof(double) * S, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(w.slot_map.p, w.h_slot, sizeof(int) * S, cudaMemcpyHostToDevice, st));
+  if (ev0) CK(cudaEventRecord(ev0, st));
+  if (use_graphs()) {
+    if (!w.graph || w.graph_norm != norm) {
+      if (w.graph) cudaGraphExecDestroy(w.graph);
+      w.graph = nullptr;
+      cudaGraph_t g;
+      uint64_t before = ctx->launches;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      fg_status s = enqueue_pass(m, norm, nullptr);
+      cudaError_t ce = cudaStreamEndCapture(st, &g);
+      if (s) return s;
+      if (ce != cudaSuccess) return fail(ctx, FG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+      CK(cudaGraphInstantiate(&w.graph, g, 0));
+      cudaGraphDestroy(g);
+      w.graph_norm = norm;
+      w.graph_launches = ctx->launches - before;
+      ctx->launches = before;
+    }
+    CK(cudaGraphLaunch(w.graph, st));
+    ctx->launches += w.graph_launches;
+  } else {
+    fg_status s = enqueue_pass(m, norm, nullptr);
+    if (s) return s;
+  }
+  if (ev1) CK(cudaEventRecord(ev1, st));
+  CK(cudaMemcpyAsync(w.h_logits, w.logits.p, sizeof(double) * 2 * S * C, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(w.h_status, w.status.p, sizeof(int) * S, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (ev0 && ev1 && ms) CK(cudaEventElapsedTime(ms, ev0, ev1));
+  return FG_OK;
+}
+
+fg_status stage_inputs(fg_model* m, int S, const double* x, const int* positions, int words) {
+  fg_ctx* ctx = m->ctx;
+  const fg_config& c = m->cfg;
+  for (int s = 0; s < S; ++s)
+    for (int wd = 0; wd < words; ++wd) {
+      int p = positions[(size_t)s * words + wd];
+      if (p < 0 || p >= c.length) return fail(ctx, FG_EINVAL, "word position out of range");
+      for (int u = 0; u < wd; ++u)
+        if (positions[(size_t)s * words + u] == p) return fail(ctx, FG_EINVAL, "duplicate word position");
+    }
+  Workspace& w = m->ws;
+  CK(cudaMemcpyAsync(w.x_all.p, x, sizeof(double) * (size_t)S * c.length * c.embed,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(w.pos_all.p, positions, sizeof(int) * (size_t)S * words, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  return FG_OK;
+}
+
+// Exact f64 forward pass (model.cpp:470-564): dense layers, softmax attention,
+// residuals, mean pool, linear head.  Same loop order as the reference.
+void forward_host(const fg_config& c, const double* p, const double* x, double* logits) {
+  const size_t L = c.length, E = c.embed, F = c.ffn, H = c.heads, hd = E / H, C = c.classes;
+  auto dense = [](const std::vector<double>& in, size_t rows, size_t ci, size_t o, const double* w,
+                  const double* b, std::vector<double>& out) {
+    out.assign(rows * o, 0.0);
+    for (size_t r = 0; r < rows; ++r) {
+      for (size_t i = 0; i < ci; ++i) {
+        double xv = in[r * ci + i];
+        const double* wr = w + i * o;
+        double* orow = out.data() + r * o;
+        for (size_t j = 0; j < o; ++j) orow[j] += xv * wr[j];
+      }
+      for (size_t j = 0; j < o; ++j) out[r * o + j] += b[j];
+    }
+  };
+  std::vector<double> cur(x, x + L * E), q, k, v, sc(H * L * L), ctx, attn, ffn;
+  const double inv = 1.0 / std::sqrt((double)hd);
+  const double* pp = p;
+  for (int l = 0; l < c.layers; ++l) {
+    const double *wq = pp, *bq = wq + E * E, *wk = bq + E, *bk = wk + E * E, *wv = bk + E,
+                 *bv = wv + E * E, *wo = bv + E, *bo = wo + E * E, *w1 = bo + E, *b1 = w1 + E * F,
+                 *w2 = b1 + F, *b2 = w2 + F * E;
+    pp = b2 + E;
+    dense(cur, L, E, E, wq, bq, q);
+    dense(cur, L, E, E, wk, bk, k);
+    dense(cur, L, E, E, wv, bv, v);
+    for (size_t h = 0; h < H; ++h)
+      for (size_t i = 0; i < L; ++i) {
+        for (size_t j = 0; j < L; ++j) {
+          double acc = 0.0;
+          for (size_t d = 0; d < hd; ++d) acc += q[i * E + h * hd + d] * k[j * E + h * hd + d];
+          sc[(h * L + i) * L + j] = acc * inv;
+        }
+        double* row = sc.data() + (h * L + i) * L;
+        double mx = row[0];
+        for (size_t j = 1; j < L; ++j) mx = std::max(mx, row[j]);
+        double sum = 0.0;
+        for (size_t j = 0; j < L; ++j) {
+          row[j] = std::exp(row[j] - mx);
+          sum += row[j];
+        }
+        for (size_t j = 0; j < L; ++j) row[j] /= sum;
+      }
+    ctx.assign(L * E, 0.0);
+    for (size_t h = 0; h < H; ++h)
+      for (size_t i = 0; i < L; ++i)
+        for (size_t j = 0; j < L; ++j) {
+          double pv = sc[(h * L + i) * L + j];
+          for (size_t d = 0; d < hd; ++d) ctx[i * E + h * hd + d] += pv * v[j * E + h * hd + d];
+        }
+    dense(ctx, L, E, E, wo, bo, attn);
+    for (size_t i = 0; i < L * E; ++i) cur[i] += attn[i];
+    dense(cur, L, E, F, w1, b1, ffn);
+    for (double& t : ffn) {
+      if (c.activation == FG_RELAX_TANH) t = std::tanh(t);
+      else if (c.activation == FG_RELAX_SILU) t = t * (1.0 / (1.0 + std::exp(-t)));
+      else t = t > 0.0 ? t : 0.0;
+    }
+    dense(ffn, L, F, E, w2, b2, attn);
+    for (size_t i = 0; i < L * E; ++i) cur[i] += attn[i];
+  }
+  std::vector<double> pooled(E, 0.0), out;
+  for (size_t i = 0; i < L; ++i)
+    for (size_t d = 0; d < E; ++d) pooled[d] += cur[i * E + d];
+  for (size_t d = 0; d < E; ++d) pooled[d] /= (double)L;
+  dense(pooled, 1, E, C, pp, pp + E * C, out);
+  std::memcpy(logits, out.data(), sizeof(double) * C);
+}
+
+std::vector<int> predict_all(const fg_model* m, int S, const double* x) {
+  const fg_config& c = m->cfg;
+  std::vector<int> pred(S, 0);
+  unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), (unsigned)S));
+  std::atomic<int> next{0};
+  auto worker = [&] {
+    std::vector<double> logits(c.classes);
+    for (int s; (s = next.fetch_add(1)) < S;) {
+      forward_host(c, m->params.data(), x + (size_t)s * c.length * c.embed, logits.data());
+      int best = 0;  // argmax (cli.cpp:54-60)
+      for (int i = 1; i < c.classes; ++i)
+        if (logits[i] > logits[best]) best = i;
+      pred[s] = best;
+    }
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t) th.emplace_back(worker);
+  for (auto& t : th) t.join();
+  return pred;
+}
+
+int default_slots(const fg_model* m, int S, int D) {
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  size_t per = bytes_per_sentence(m->cfg, D);
+  size_t cap = (size_t)(0.8 * (double)free_b) / std::max<size_t>(per, 1);
+  if (const char* e = std::getenv("FG_SLOTS")) cap = std::min<size_t>(cap, (size_t)std::atoi(e));
+  int slots = (int)std::min<size_t>({cap, (size_t)S, (size_t)64});
+  int maxb = 65535 / (2 * m->cfg.length);  // GEMM batch-grid limit
+  return std::max(1, std::min(slots, maxb));
+}
+
+}  // namespace
+
+extern "C" {
+
+fg_status fg_model_create(fg_ctx* ctx, const fg_config* cfg, const double* params, fg_model** out) {
+  *out = nullptr;
+  if (!cfg || cfg->layers < 1 || cfg->heads < 1 || cfg->embed % cfg->heads != 0 || cfg->classes < 1 ||
+      cfg->length < 1 || cfg->ffn < 1 || cfg->embed % 4 != 0)
+    return fail(ctx, FG_EINVAL, "fg_model_create: invalid config");
+  if (cfg->activation != FG_RELAX_RELU && cfg->activation != FG_RELAX_TANH &&
+      cfg->activation != FG_RELAX_SILU)
+    return fail(ctx, FG_EINVAL, "fg_model_create: activation must be relu/tanh/silu");
+  cudaSetDevice(ctx->device);
+  auto m = std::make_unique<fg_model>();
+  m->ctx = ctx;
+  m->cfg = *cfg;
+  const size_t E = cfg->embed, F = cfg->ffn, C = cfg->classes;
+  const size_t per_layer = 4 * (E * E + E) + E * F + F + F * E + E;
+  m->params.assign(params, params + cfg->layers * per_layer + E * C + C);
+  m->layers.resize(cfg->layers);
+  for (int l = 0; l < cfg->layers; ++l) {
+    const double* p = m->params.data() + m->layer_off(l);
+    const double *wq = p, *bq = wq + E * E, *wk = bq + E, *bk = wk + E * E, *wv = bk + E, *bv = wv + E * E,
+                 *wo = bv + E, *bo = wo + E * E, *w1 = bo + E, *b1 = w1 + E * F, *w2 = b1 + F, *b2 = w2 + F * E;
+    std::vector<double> qkv(E * 3 * E), bqkv(3 * E);
+    for (size_t i = 0; i < E; ++i)
+      for (size_t j = 0; j < E; ++j) {
+        qkv[i * 3 * E + j] = wq[i * E + j];
+        qkv[i * 3 * E + E + j] = wk[i * E + j];
+        qkv[i * 3 * E + 2 * E + j] = wv[i * E + j];
+      }
+    for (size_t j = 0; j < E; ++j) {
+      bqkv[j] = bq[j];
+      bqkv[E + j] = bk[j];
+      bqkv[2 * E + j] = bv[j];
+    }
+    fg_status s;
+    if ((s = upload_affine(ctx, m->layers[l].qkv, (int)E, (int)(3 * E), qkv, bqkv.data()))) return s;
+    if ((s = upload_affine(ctx, m->layers[l].wo, (int)E, (int)E, std::vector<double>(wo, wo + E * E), bo))) return s;
+    if ((s = upload_affine(ctx, m->layers[l].w1, (int)E, (int)F, std::vector<double>(w1, w1 + E * F), b1))) return s;
+    if ((s = upload_affine(ctx, m->layers[l].w2, (int)F, (int)E, std::vector<double>(w2, w2 + F * E), b2))) return s;
+  }
+  const double* wc = m->params.data() + m->layer_off(cfg->layers);
+  CK(m->wc64.alloc(sizeof(double) * E * C));
+  CK(m->bc64.alloc(sizeof(double) * C));
+  CK(cudaMemcpy(m->wc64.p, wc, sizeof(double) * E * C, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(m->bc64.p, wc + E * C, sizeof(double) * C, cudaMemcpyHostToDevice));
+  *out = m.release();
+  return FG_OK;
+}
+
+void fg_model_destroy(fg_model* m) {
+  if (!m) return;
+  cudaSetDevice(m->ctx->device);
+  delete m;
+}
+
+fg_status fg_forward(fg_model* m, const double* x, double* logits) {
+  forward_host(m->cfg, m->params.data(), x, logits);
+  for (int i = 0; i < m->cfg.classes; ++i)
+    if (!std::isfinite(logits[i])) return fail(m->ctx, FG_EINVAL, "forward: non-finite logits");
+  return FG_OK;
+}
+
+size_t fg_node_dump_size(const fg_config* c) {
+  size_t L = c->length, E = c->embed, H = c->heads, F = c->ffn;
+  return c->layers * (8 * L * E + 4 * H * L * L + 2 * H * L + 2 * L * F) + E + c->classes;
+}
+
+fg_status fg_bound_pass(fg_model* m, int S, const double* x, const int* positions, int words, int norm,
+                        const double* eps, double* logits_lo, double* logits_hi, int* status) {
+  fg_ctx* ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  if (S < 1 || words < 1 || words > m->cfg.length) return fail(ctx, FG_EINVAL, "fg_bound_pass: bad sizes");
+  for (int s = 0; s < S; ++s)
+    if (!eps_ok(eps[s])) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  const int C = m->cfg.classes;
+  int slots = default_slots(m, S, words * m->cfg.embed);
+  fg_status st = ensure_workspace(m, slots, words, S);
+  if (st) return st;
+  if ((st = stage_inputs(m, S, x, positions, words))) return st;
+  Workspace& w = m->ws;
+  cudaEvent_t e0, e1, t0, t1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&t0); cudaEventCreate(&t1);
+  uint64_t launches0 = ctx->launches;
+  double total_ms = 0.0;
+  int passes = 0;
+  for (int s0 = 0; s0 < S; s0 += slots) {
+    for (int i = 0; i < slots; ++i) {
+      int s = std::min(s0 + i, S - 1);
+      w.h_slot[i] = s;
+      w.h_eps[i] = eps[s];
+    }
+    float ms = 0.f;
+    if ((st = run_pass(m, norm, e0, e1, &ms))) break;
+    total_ms += ms;
+    ++passes;
+    for (int i = 0; i < slots && s0 + i < S; ++i) {
+      int s = s0 + i;
+      for (int k = 0; k < C; ++k) {
+        logits_lo[(size_t)s * C + k] = w.h_logits[(size_t)i * C + k];
+        logits_hi[(size_t)s * C + k] = w.h_logits[(size_t)slots * C + (size_t)i * C + k];
+      }
+      status[s] = decode_status(w.h_status[i]);
+    }
+  }
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(t0); cudaEventDestroy(t1);
+  m->stats = fg_run_stats{total_ms, passes ? total_ms / passes : 0.0, passes, slots,
+                          ctx->launches - launches0, (double)S};
+  return st;
+}
+
+fg_status fg_bound_pass_dump(fg_model* m, const double* x, const int* positions, int words, int norm,
+                             double eps, double* logits_lo, double* logits_hi, double* node_lo,
+                             double* node_hi, int* status) {
+  fg_ctx* ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  fg_status st = ensure_workspace(m, 1, words, 1);
+  if (st) return st;
+  if ((st = stage_inputs(m, 1, x, positions, words))) return st;
+  Workspace& w = m->ws;
+  size_t nd = fg_node_dump_size(&m->cfg);
+  for (size_t i = 0; i < nd; ++i) node_lo[i] = node_hi[i] = std::numeric_limits<double>::quiet_NaN();
+  w.h_eps[0] = eps;
+  w.h_slot[0] = 0;
+  CK(cudaMemcpyAsync(w.eps.p, w.h_eps, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(w.slot_map.p, w.h_slot, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  Dumper d{node_lo, node_hi, ctx};
+  if ((st = enqueue_pass(m, norm, &d))) return st;
+  const int C = m->cfg.classes;
+  std::vector<double> lg(2 * C);
+  int sv = 0;
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(lg.data(), w.logits.p, sizeof(double) * 2 * C, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&sv, w.status.p, sizeof(int), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < C; ++k) {
+    logits_lo[k] = lg[k];
+    logits_hi[k] = lg[C + k];
+  }
+  *status = decode_status(sv);
+  return FG_OK;
+}
+
+fg_status fg_certify(fg_model* m, int S, const double* x, const int* positions, int words, int norm,
+                     const double* eps, double margin, int* verified, int* bounded, int* predicted,
+                     double* logits_lo, double* logits_hi, int* status) {
+  if (margin < 0.0) return fail(m->ctx, FG_EINVAL, "check_robust: margin must be >= 0");
+  std::vector<int> pred = predict_all(m, S, x);
+  fg_status st = fg_bound_pass(m, S, x, positions, words, norm, eps, logits_lo, logits_hi, status);
+  if (st) return st;
+  const int C = m->cfg.classes;
+  for (int s = 0; s < S; ++s) {
+    predicted[s] = pred[s];
+    bounded[s] = status[s] != FG_EDOMAIN;  // cli.cpp:92-94
+    verified[s] = 0;
+    if (status[s] == FG_OK)
+      fg_check_robust((size_t)C, logits_lo + (size_t)s * C, logits_hi + (size_t)s * C, (size_t)pred[s],
+                      margin, &verified[s]);
+  }
+  return FG_OK;
+}
+
+fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, int words, int norm,
+                    double eps_max, double tol, int slots, double* eps_out, int* calls_out,
+                    int* predicted_out, int* status_out) {
+  fg_ctx* ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  if (S < 1 || words < 1 || words > m->cfg.length) return fail(ctx, FG_EINVAL, "fg_maxeps: bad sizes");
+  if (!eps_ok(eps_max)) return fail(ctx, FG_EINVAL, "fg_maxeps: eps_max must be finite and >= 0");
+  const int C = m->cfg.classes;
+  if (slots <= 0) slots = default_slots(m, S, words * m->cfg.embed);
+  slots = std::min(slots, S);
+  fg_status st = ensure_workspace(m, slots, words, S);
+  if (st) return st;
+  if ((st = stage_inputs(m, S, x, positions, words))) return st;
+  Workspace& w = m->ws;
+  cudaEvent_t c0, c1, e0, e1;
+  cudaEventCreate(&c0); cudaEventCreate(&c1); cudaEventCreate(&e0); cudaEventCreate(&e1);
+  CK(cudaEventRecord(c0, ctx->stream));
+  uint64_t launches0 = ctx->launches;
+  // predicted classes on host threads, overlapped with the first passes
+  std::future<std::vector<int>> fut = std::async(std::launch::async, predict_all, m, S, x);
+  std::vector<int> pred;
+  bool have_pred = false;
+
+  // bisection state per sentence (cli.cpp:144-177)
+  enum Phase { P_ZERO = 0, P_MAX = 1, P_BISECT = 2, P_DONE = 3 };
+  struct Sent { int phase = P_ZERO; double lo = 0.0, hi = 0.0, eps = 0.0; int calls = 0; };
+  std::vector<Sent> sent(S);
+  std::vector<int> slot(slots, -1);
+  int next = 0, done = 0, passes = 0;
+  double pass_ms_sum = 0.0, sentence_passes = 0.0;
+  for (int s = 0; s < S; ++s) status_out[s] = FG_OK;
+  while (done < S) {
+    for (int i = 0; i < slots; ++i) {
+      if (slot[i] < 0 && next < S) slot[i] = next++;
+      int s = slot[i];
+      w.h_slot[i] = s >= 0 ? s : 0;
+      w.h_eps[i] = s >= 0 ? sent[s].eps : 0.0;
+    }
+    float ms = 0.f;
+    if ((st = run_pass(m, norm, e0, e1, &ms))) break;
+    pass_ms_sum += ms;
+    ++passes;
+    if (!have_pred) {
+      pred = fut.get();
+      have_pred = true;
+    }
+    for (int i = 0; i < slots; ++i) {
+      int s = slot[i];
+      if (s < 0) continue;
+      sentence_passes += 1.0;
+      Sent& t = sent[s];
+      ++t.calls;
+      fg_status ps = decode_status(w.h_status[i]);
+      int ok = 0;
+      if (ps == FG_OK)
+        fg_check_robust((size_t)C, w.h_logits + (size_t)i * C, w.h_logits + (size_t)slots * C + (size_t)i * C,
+                        (size_t)pred[s], 0.0, &ok);
+      bool finished = false;
+      if (t.phase == P_ZERO) {  // verified_at(0, tolerate=false)
+        if (ps != FG_OK) {
+          status_out[s] = ps;
+          finished = true;
+        } else if (!ok) {
+          status_out[s] = FG_ERUNTIME;  // misclassified input (cli.cpp:159-161)
+          finished = true;
+        } else {
+          t.phase = P_MAX;
+          t.eps = eps_max;
+        }
+      } else if (t.phase == P_MAX) {
+        if (ok) {
+          t.lo = eps_max;
+          finished = true;
+        } else {
+          t.lo = 0.0;
+          t.hi = eps_max;
+          t.phase = P_BISECT;
+        }
+      } else {
+        if (ok) t.lo = t.eps;
+        else t.hi = t.eps;
+      }
+      if (!finished && t.phase == P_BISECT) {
+        if (t.hi - t.lo > tol) t.eps = 0.5 * (t.lo + t.hi);
+        else finished = true;
+      }
+      if (finished) {
+        t.phase = P_DONE;
+        eps_out[s] = status_out[s] == FG_OK ? t.lo : std::numeric_limits<double>::quiet_NaN();
+        calls_out[s] = t.calls;
+        ++done;
+        slot[i] = -1;
+      }
+    }
+  }
+  if (!have_pred) pred = fut.get();
+  for (int s = 0; s < S; ++s) predicted_out[s] = pred[s];
+  CK(cudaEventRecord(c1, ctx->stream));
+  CK(cudaEventSynchronize(c1));
+  float total = 0.f;
+  cudaEventElapsedTime(&total, c0, c1);
+  cudaEventDestroy(c0); cudaEventDestroy(c1); cudaEventDestroy(e0); cudaEventDestroy(e1);
+  m->stats = fg_run_stats{(double)total, passes ? pass_ms_sum / passes : 0.0, passes, slots,
+                          ctx->launches - launches0, sentence_passes};
+  return st;
+}
+
+
+}  // extern "C"
+
+// ---- synthetic model / inputs: the reference's seeded generators (model.cpp:87-141,
+// rng.hpp:11-32) so that a user of the library gets bit-identical weights/inputs.
+namespace {
+struct Rng64 {  // faith::Rng over std::mt19937_64 (rng.hpp:11-54)
+  std::mt19937_64 eng;
+  explicit Rng64(uint64_t s) : eng(s) {}
+  double uniform() { return (double)(eng() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  uint64_t uniform_index(uint64_t n) {
+    uint64_t limit = UINT64_MAX - UINT64_MAX % n, v;
+    do {
+      v = eng();
+    } while (v >= limit);
+    return v % n;
+  }
+};
+}  // namespace
+
+extern "C" {
+
+fg_status fg_gen_synthetic(const fg_config* c, uint64_t seed, double* p) {
+  if (!c || c->layers < 1 || c->heads < 1 || c->embed % c->heads) return FG_EINVAL;
+  Rng64 rng(seed);
+  const size_t e = c->embed, f = c->ffn, k = c->classes;
+  auto gen = [&](size_t n, size_t fan_in) {  // gen_tensor (model.cpp:87-95)
+    double bound = 0.5 / std::sqrt((double)fan_in);
+    for (size_t i = 0; i < n; ++i) *p++ = (double)(float)rng.uniform(-bound, bound);
+  };
+  for (int l = 0; l < c->layers; ++l) {
+    gen(e * e, e); gen(e, e); gen(e * e, e); gen(e, e); gen(e * e, e); gen(e, e);
+    gen(e * e, e); gen(e, e); gen(e * f, e); gen(f, e); gen(f * e, f); gen(e, f);
+  }
+  gen(e * k, e);
+  gen(k, e);
+  return FG_OK;
+}
+
+size_t fg_param_count(const fg_config* c) {
+  size_t e = c->embed, f = c->ffn, k = c->classes;
+  return c->layers * (4 * (e * e + e) + e * f + f + f * e + e) + e * k + k;
+}
+
+fg_status fg_gen_input(const fg_config* c, uint64_t seed, double* x) {  // model.cpp:133-141
+  Rng64 rng(seed ^ 0x9e3779b97f4a7c15ull);
+  for (size_t i = 0; i < (size_t)c->length * c->embed; ++i) x[i] = (double)(float)rng.uniform(-0.5, 0.5);
+  return FG_OK;
+}
+
+fg_status fg_gen_positions(uint64_t seed, int length, int words, int* pos) {
+  if (words < 1 || words > length) return FG_EINVAL;
+  Rng64 rng(seed);
+  int n = 0;
+  while (n < words) {
+    int v = (int)rng.uniform_index((uint64_t)length);
+    bool dup = false;
+    for (int i = 0; i < n; ++i) dup |= pos[i] == v;
+    if (!dup) pos[n++] = v;
+  }
+  std::sort(pos, pos + n);
+  return FG_OK;
+}
+
+// One eager (non-graph) pass over the resident slots with CUDA events around every
+// launch site; per-site device time (ms) and kernel counts.
+fg_status fg_profile_pass(fg_model* m, int norm, double eps, int max_sites, char* names, double* ms,
+                          int* kernels, int* nsites) {
+  fg_ctx* ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  Workspace& w = m->ws;
+  if (w.S <= 0) return fail(ctx, FG_EINVAL, "fg_profile_pass: run fg_maxeps/fg_bound_pass first");
+  for (int i = 0; i < w.S; ++i) {
+    w.h_eps[i] = eps;
+    w.h_slot[i] = i % std::max(1, w.Ntot);
+  }
+  CK(cudaMemcpyAsync(w.eps.p, w.h_eps, sizeof(double) * w.S, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(w.slot_map.p, w.h_slot, sizeof(int) * w.S, cudaMemcpyHostToDevice, ctx->stream));
+  Profiler prof;
+  prof.st = ctx->stream;
+  g_prof = &prof;
+  fg_status st = enqueue_pass(m, norm, nullptr);
+  g_prof = nullptr;
+  g_tag = "other";
+  if (st) return st;
+  CK(cudaStreamSynchronize(ctx->stream));
+  int n = 0;
+  for (auto& site : prof.sites) {
+    double t = 0.0;
+    for (auto& be : site.ev) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, be.first, be.second);
+      t += x;
+      cudaEventDestroy(be.first);
+      cudaEventDestroy(be.second);
+    }
+    if (n < max_sites) {
+      std::snprintf(names + 32 * n, 32, "%s", site.tag.c_str());
+      ms[n] = t;
+      kernels[n] = site.kernels;
+      ++n;
+    }
+  }
+  *nsites = n;
+  return FG_OK;
+}
+
+fg_status fg_last_run_stats(const fg_model* m, fg_run_stats* out) {
+  *out = m->stats;
+  return FG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// fg_internal.cuh -- shared declarations of the B200 bound-propagation kernels.
+//
+// Data model on the device:
+//   A bound tensor over N neurons with D perturbation columns is stored as
+//   * Λ in CENTER/RADIUS form, f32, two planes of [N, D] (D contiguous):
+//       c = (Λᵁ + Λᴸ) / 2,   r = (Λᵁ − Λᴸ) / 2       (plane r at +cr elements)
+//     so the sign-split affine bound  Λᵁ' = W⁺Λᵁ + W⁻Λᴸ,  Λᴸ' = W⁺Λᴸ + W⁻Λᵁ
+//     (relax.cpp:237-307) becomes two dense GEMMs  c' = Wc,  r' = |W| r;
+//   * lb, ub (and concretized lo, hi) in f64, [N].
+//   Sentences of a batch are the outermost axis of every tensor.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fg {
+
+// Per-sentence status word: atomicMin of (site << 4 | code).  The smallest site
+// wins (the reference throws at the first failing node); within a site
+// EINVAL (1) beats EDOMAIN (2) because ConcreteBounds::validate runs over all
+// neurons before any domain check (relax.cpp:314-335, 364-392, 397-410).
+constexpr int kStatusClear = 0x7fffffff;
+constexpr int kCodeInval = 1;
+constexpr int kCodeDomain = 2;
+
+enum Norm { NORM_L1 = 0, NORM_L2 = 1, NORM_LINF = 2 };
+enum Relax { RELAX_RELU = 0, RELAX_TANH = 1, RELAX_SILU = 2, RELAX_EXP = 3, RELAX_RECIP = 4 };
+
+// A neuron-indexed view into a batched bound tensor.
+//   neuron(s, row, f) = s*s_stride + row*row_stride + col0 + f
+struct NView {
+  float* lam;           // plane c; plane r at lam + cr
+  long long cr;
+  double* lb;
+  double* ub;
+  double* lo;           // concretized bounds (may be null when not needed)
+  double* hi;
+  long long s_stride;   // neurons per sentence
+  int row_stride;       // neurons per token row
+  int col0;             // first neuron of the slice
+};
+
+// Generic batched f32 GEMM on N-contiguous operands:
+//   C[b][m, n] = alpha * sum_k A[b][m, k] * B[b][k, n]  (+ C[b] if accumulate) (+ R[b])
+//   A is M-major: A[m, k] at A + k*lda + m.
+//   B rows k <  K0 at B + k*ldb,  rows k >= K0 at B + b_off1 + (k-K0)*ldb.
+//   Batch index b = ((b0*nb1 + b1)*nb2 + b2)*nb3 + b3 with per-level strides.
+struct GemmArgs {
+  int M, N, K, K0;
+  const float* A;
+  long long lda;
+  const float* B;
+  long long ldb, b_off1;
+  float* C;
+  long long ldc;
+  const float* R;
+  long long ldr;
+  float alpha;
+  int accumulate;
+  int nb[4];
+  long long sA[4], sB[4], sC[4], sR[4];
+};
+
+// ---- launchers (fg_kernels.cu / fg_gemm.cu); all return the number of kernels launched
+int launch_gemm(const GemmArgs& g, cudaStream_t st);
+
+int launch_concretize(const float* lam, long long cr, const double* lb, const double* ub,
+                      long long rows_per_s, long long nrows, int D, int norm, const double* eps,
+                      double* lo, double* hi, cudaStream_t st);
+
+int launch_elementwise_verify(int kind, float* lam, long long cr, double* lb, double* ub,
+                              long long rows_per_s, long long nrows, int D, int norm,
+                              const double* eps, int* status, int site, double* lo_out,
+                              double* hi_out, cudaStream_t st);
+
+// Standalone envelope / compose (operator-level API).
+int launch_relax(int kind, const double* lo, const double* hi, long long n, double* a_low,
+                 double* b_low, double* a_up, double* b_up, int* status, cudaStream_t st);
+int launch_compose(float* lam_in, long long cr_in, const double* lb_in, const double* ub_in,
+                   const double* a_low, const double* b_low, const double* a_up,
+                   const double* b_up, float* lam_out, long long cr_out, double* lb_out,
+                   double* ub_out, long long n, int D, cudaStream_t st);
+
+// Affine bias path in f64 with the reference's accumulation order (relax.cpp:273-299),
+// optional residual add (propagate_add(res, y), relax.cpp:656-674).
+int launch_affine_bias(const double* lb_in, const double* ub_in, const double* w64,
+                       const double* bias, const double* res_lb, const double* res_ub,
+                       double* lb_out, double* ub_out, int S, int rows, int C, int O,
+                       cudaStream_t st);
+
+// Pairwise-similarity McCormick dot product Q.K^T (relax.cpp:573-617) scaled by `scale`
+// (the following Scale node, model.cpp:416-418).  out: [S, H, L, L] neurons.
+int launch_dot_similarity(const NView& q, const NView& k, const NView& out, int S, int L, int H,
+                          int hd, int D, float* coef_ws, float scale, cudaStream_t st);
+// Weighted-values McCormick dot product P.V (relax.cpp:618-652).  p: [S, H, L, L] neurons;
+// v: token rows; out: token rows [S, L, E].
+int launch_dot_weighted(const NView& p, const NView& v, const NView& out, int S, int L, int H,
+                        int hd, int D, float* coef_ws, cudaStream_t st);
+
+// Softmax chain along the key axis of scores [S, H*L rows, L keys] (graph.cpp:237-240):
+// exp -> sum -> recip -> McCormick multiply, in place; also writes probs lo/hi.
+int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int norm,
+                   const double* eps, int* status, int site_exp, int site_recip,
+                   cudaStream_t st);
+
+// Word-level input binding: lb = ub = x, Λ rows of perturbed positions one-hot.
+int launch_init_input(float* lam, long long cr, double* lb, double* ub, const double* x,
+                      const int* positions, const int* slot_map, int S, int L, int E, int W,
+                      cudaStream_t st);
+// MeanPool (graph.cpp:628-634) -> pooled f64 planes [S, E, D] (+ lb/ub [S, E]).
+int launch_meanpool(const float* lam, long long cr, const double* lb, const double* ub,
+                    double* pooled_c, double* pooled_r, double* plb, double* pub, int S, int L,
+                    int E, int D, cudaStream_t st);
+// Classifier affine + final concretization + finiteness check (graph.cpp:663-671).
+int launch_head(const double* pooled_c, const double* pooled_r, const double* plb,
+                const double* pub, const double* wc, const double* bc, int S, int E, int C,
+                int D, int norm, const double* eps, double* logits_lo, double* logits_hi,
+                int* status, int site, double* pooled_lo, double* pooled_hi,
+                cudaStream_t st);
+
+// Layout conversion for the operator-level API: reference (lw, uw) f64 <-> (c, r) f32.
+int launch_ul_to_cr(const double* lw, const double* uw, float* lam, long long cr, long long n,
+                    int d, int Dp, cudaStream_t st);
+int launch_cr_to_ul(const float* lam, long long cr, double* lw, double* uw, long long n, int d,
+                    int Dp, cudaStream_t st);
+int launch_add(const float* a, long long acr, const double* alb, const double* aub,
+               const float* b, long long bcr, const double* blb, const double* bub, float* y,
+               long long ycr, double* ylb, double* yub, long long n, int D, cudaStream_t st);
+int launch_scale(const float* x, long long xcr, const double* xlb, const double* xub, double s,
+                 float* y, long long ycr, double* ylb, double* yub, long long n, int D,
+                 cudaStream_t st);
+int launch_fill_int(int* p, int v, long long n, cudaStream_t st);
+
+}  // namespace fg

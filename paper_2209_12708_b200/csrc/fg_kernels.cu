@@ -1,0 +1,1204 @@
+// fg_kernels.cu -- memory-bound and f64 kernels of the B200 bound pass.
+//
+// Compiled with -fmad=false: the O(N) f64 scalar paths (biases, envelopes,
+// softmax chain) then round exactly like the reference's host arithmetic
+// (no FMA contraction), so on identical inputs they are bit-identical to
+// proj/src/relax.cpp.  The dense Λ contractions live in fg_gemm.cu.
+#include <math.h>
+
+#include "fg_internal.cuh"
+
+namespace fg {
+
+namespace {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Dual norm q of the perturbation norm p (bounds.cpp:9-19).
+__host__ __device__ __forceinline__ int dual_norm(int p) {
+  return p == NORM_L1 ? NORM_LINF : (p == NORM_L2 ? NORM_L2 : NORM_L1);
+}
+
+// Accumulates the q-norm partials of the upper (u = c + r) and lower (l = c - r) rows.
+template <int Q>
+struct NormAcc {
+  double u = 0.0, l = 0.0;
+  __device__ __forceinline__ void add(float c, float r) {
+    double dc = c, dr = r;
+    double uu = dc + dr, ll = dc - dr;
+    if (Q == NORM_L1) {
+      u += fabs(uu);
+      l += fabs(ll);
+    } else if (Q == NORM_L2) {
+      u += uu * uu;
+      l += ll * ll;
+    } else {
+      u = fmax(u, fabs(uu));
+      l = fmax(l, fabs(ll));
+    }
+  }
+  __device__ __forceinline__ void add4(float4 c, float4 r) {
+    add(c.x, r.x);
+    add(c.y, r.y);
+    add(c.z, r.z);
+    add(c.w, r.w);
+  }
+  __device__ __forceinline__ void warp_reduce() {
+    if (Q == NORM_LINF) {
+      u = warp_max(u);
+      l = warp_max(l);
+    } else {
+      u = warp_sum(u);
+      l = warp_sum(l);
+    }
+  }
+  __device__ __forceinline__ double fin(double v) const { return Q == NORM_L2 ? sqrt(v) : v; }
+};
+
+template <int Q>
+__device__ __forceinline__ double qcombine(double a, double b) {
+  return Q == NORM_LINF ? fmax(a, b) : a + b;
+}
+
+__device__ __forceinline__ void set_status(int* status, int s, int site, int code) {
+  atomicMin(status + s, (site << 4) | code);
+}
+
+// ---------------------------------------------------------------------------
+// Envelope lines in f64 (relax.cpp:12-108, 313-468).  Return 0, kCodeInval or
+// kCodeDomain exactly where the reference throws.
+// ---------------------------------------------------------------------------
+struct Lines {
+  double al, bl, au, bu;
+};
+
+__device__ __forceinline__ double sech2(double x) {
+  double t = tanh(x);
+  return 1.0 - t * t;
+}
+
+__device__ void chord(double lo, double hi, double flo, double fhi, double& a, double& b) {
+  double s = (fhi - flo) / (hi - lo);
+  a = s;
+  b = flo - s * lo;
+}
+
+__device__ double bisect_tanh_tangent(double anchor, double blo, double bhi) {  // relax.cpp:33
+  double fa = tanh(anchor);
+  double a = blo, b = bhi;
+  for (int it = 0; it < 60 && (b - a) > 1e-9; ++it) {
+    double mid = 0.5 * (a + b);
+    double g = tanh(mid) + sech2(mid) * (anchor - mid) - fa;
+    if (g >= 0.0) b = mid;
+    else a = mid;
+  }
+  return b;
+}
+
+__device__ void tanh_nonneg(double lo, double hi, double& la, double& lb, double& ua,
+                            double& ub) {  // relax.cpp:56-62
+  chord(lo, hi, tanh(lo), tanh(hi), la, lb);
+  double m = 0.5 * (lo + hi);
+  double a = sech2(m);
+  ua = a;
+  ub = tanh(m) - a * m;
+}
+
+__device__ Lines tanh_lines(double lo, double hi) {  // relax.cpp:64-108
+  Lines r;
+  if (lo == hi) {
+    double a = sech2(lo);
+    double b = tanh(lo) - a * lo;
+    r.al = a; r.bl = b; r.au = a; r.bu = b;
+    return r;
+  }
+  if (lo >= 0.0) {
+    tanh_nonneg(lo, hi, r.al, r.bl, r.au, r.bu);
+    return r;
+  }
+  if (hi <= 0.0) {
+    double mla, mlb, mua, mub;
+    tanh_nonneg(-hi, -lo, mla, mlb, mua, mub);
+    r.al = mua; r.bl = -mub;
+    r.au = mla; r.bu = -mlb;
+    return r;
+  }
+  double flo = tanh(lo);
+  double gap_hi = tanh(hi) + sech2(hi) * (lo - hi) - flo;
+  if (gap_hi < 0.0) {
+    chord(lo, hi, flo, tanh(hi), r.au, r.bu);
+  } else {
+    double d = bisect_tanh_tangent(lo, 0.0, hi);
+    double a = sech2(d);
+    r.au = a;
+    r.bu = tanh(d) - a * d;
+  }
+  double mua, mub;
+  double mflo = tanh(-hi);
+  double mgap = tanh(-lo) + sech2(-lo) * (-hi + lo) - mflo;
+  if (mgap < 0.0) {
+    chord(-hi, -lo, mflo, tanh(-lo), mua, mub);
+  } else {
+    double d = bisect_tanh_tangent(-hi, 0.0, -lo);
+    double a = sech2(d);
+    mua = a;
+    mub = tanh(d) - a * d;
+  }
+  r.al = mua;
+  r.bl = -mub;
+  return r;
+}
+
+__device__ __forceinline__ double silu_scalar(double x) { return x * (1.0 / (1.0 + exp(-x))); }
+__device__ __forceinline__ double silu_derivative(double x) {
+  double s = 1.0 / (1.0 + exp(-x));
+  return s * (1.0 + x * (1.0 - s));
+}
+
+// Envelope of `kind` on [lo, hi].  For SiLU the 257-point grid (relax.cpp:452-460) is
+// spread over the lanes of a warp when `lane`/`lanes` say so (min/max are exact, so the
+// result does not depend on the split).
+__device__ int envelope(int kind, double lo, double hi, Lines& r, int lane = 0, int lanes = 1) {
+  r.al = r.bl = r.au = r.bu = 0.0;
+  if (lo > hi) return kCodeInval;  // ConcreteBounds::validate (bounds.cpp:69-78)
+  switch (kind) {
+    case RELAX_RELU:  // relax.cpp:313-337
+      if (lo >= 0.0) {
+        r.al = 1.0;
+        r.au = 1.0;
+      } else if (hi <= 0.0) {
+      } else {
+        double s = hi / (hi - lo);
+        r.au = s;
+        r.bu = -s * lo;
+        r.al = (fabs(lo) > fabs(hi)) ? 0.0 : 1.0;
+      }
+      return 0;
+    case RELAX_TANH:
+      r = tanh_lines(lo, hi);
+      return 0;
+    case RELAX_EXP: {  // relax.cpp:363-394
+      double m = 0.5 * (lo + hi), c2 = lo + 15.0 / 16.0;
+      double d = (c2 < m) ? c2 : m;
+      double ed = exp(d);
+      r.al = ed;
+      r.bl = ed - ed * d;
+      if (lo == hi) {
+        r.au = ed;
+        r.bu = ed - ed * d;
+      } else {
+        chord(lo, hi, exp(lo), exp(hi), r.au, r.bu);
+      }
+      if (!isfinite(r.bl) || !isfinite(r.au) || !isfinite(r.bu)) return kCodeDomain;
+      return 0;
+    }
+    case RELAX_RECIP: {  // relax.cpp:396-424
+      if (lo <= 0.0) return kCodeDomain;
+      double m = 0.5 * (lo + hi);
+      double am = -1.0 / (m * m);
+      r.al = am;
+      r.bl = 2.0 / m;
+      if (lo == hi) {
+        r.au = am;
+        r.bu = 2.0 / m;
+      } else {
+        chord(lo, hi, 1.0 / lo, 1.0 / hi, r.au, r.bu);
+      }
+      return 0;
+    }
+    case RELAX_SILU: {  // relax.cpp:426-468
+      if (lo == hi) {
+        double a = silu_derivative(lo);
+        r.al = a;
+        r.au = a;
+        r.bl = silu_scalar(lo) - a * lo;
+        r.bu = r.bl;
+        return 0;
+      }
+      double s = (silu_scalar(hi) - silu_scalar(lo)) / (hi - lo);
+      double step = (hi - lo) / 256;
+      double gmin = HUGE_VAL, gmax = -HUGE_VAL;
+      for (int k = lane; k <= 256; k += lanes) {
+        double x = (k == 256) ? hi : lo + step * k;
+        double g = silu_scalar(x) - s * x;
+        gmin = fmin(gmin, g);
+        gmax = fmax(gmax, g);
+      }
+      if (lanes > 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          gmin = fmin(gmin, __shfl_xor_sync(0xffffffffu, gmin, o));
+          gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+        }
+      }
+      double margin = 0.6 * step * step / 8.0 + 1e-12;
+      r.al = s;
+      r.au = s;
+      r.bl = gmin - margin;
+      r.bu = gmax + margin;
+      return 0;
+    }
+  }
+  return kCodeInval;
+}
+
+// compose_elementwise on one element (relax.cpp:484-494) in center/radius form.
+__device__ __forceinline__ void compose_cr(const Lines& e, float c, float r, float& oc,
+                                           float& orr) {
+  double dc = c, dr = r;
+  double u = dc + dr, l = dc - dr;
+  double yu = e.au * (e.au >= 0.0 ? u : l);
+  double yl = e.al * (e.al >= 0.0 ? l : u);
+  oc = (float)(0.5 * (yu + yl));
+  orr = (float)(0.5 * (yu - yl));
+}
+
+// ---------------------------------------------------------------------------
+// concretize (bounds.cpp:122-140): one warp per neuron row.
+// ---------------------------------------------------------------------------
+template <int Q>
+__global__ void __launch_bounds__(256) concretize_kernel(const float* __restrict__ lam, long long cr,
+                                                         const double* __restrict__ lb,
+                                                         const double* __restrict__ ub,
+                                                         long long rows_per_s, long long nrows, int D,
+                                                         const double* __restrict__ eps,
+                                                         double* __restrict__ lo,
+                                                         double* __restrict__ hi) {
+  long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+  int lane = threadIdx.x & (kWarp - 1);
+  if (row >= nrows) return;
+  const float* c = lam + row * D;
+  const float* r = c + cr;
+  NormAcc<Q> acc;
+  for (int d = lane * 4; d < D; d += 4 * kWarp)
+    acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
+  acc.warp_reduce();
+  if (lane == 0) {
+    double e = eps[row / rows_per_s];
+    lo[row] = lb[row] - e * acc.fin(acc.l);
+    hi[row] = ub[row] + e * acc.fin(acc.u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// elementwise_verify (graph.cpp:484-501) fused: concretize -> envelope -> compose,
+// in place, one warp per neuron row.  Λ is read from HBM once (the second sweep
+// re-reads the warp's own row from L1/L2) and written once.
+// ---------------------------------------------------------------------------
+template <int Q>
+__global__ void __launch_bounds__(256) elementwise_verify_kernel(
+    int kind, float* __restrict__ lam, long long cr, double* __restrict__ lb, double* __restrict__ ub,
+    long long rows_per_s, long long nrows, int D, const double* __restrict__ eps,
+    int* __restrict__ status, int site, double* __restrict__ lo_out, double* __restrict__ hi_out) {
+  long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+  int lane = threadIdx.x & (kWarp - 1);
+  if (row >= nrows) return;
+  float* c = lam + row * D;
+  float* r = c + cr;
+  NormAcc<Q> acc;
+  for (int d = lane * 4; d < D; d += 4 * kWarp)
+    acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
+  acc.warp_reduce();
+  long long s = row / rows_per_s;
+  double e = eps[s];
+  double xlb = lb[row], xub = ub[row];
+  double lo = xlb - e * acc.fin(acc.l);
+  double hi = xub + e * acc.fin(acc.u);
+  Lines ln;
+  int code = envelope(kind, lo, hi, ln, lane, kind == RELAX_SILU ? kWarp : 1);
+  if (lane == 0) {
+    if (code) set_status(status, (int)s, site, code);
+    if (lo_out) {
+      lo_out[row] = lo;
+      hi_out[row] = hi;
+    }
+    ub[row] = ln.au * (ln.au >= 0.0 ? xub : xlb) + ln.bu;
+    lb[row] = ln.al * (ln.al >= 0.0 ? xlb : xub) + ln.bl;
+  }
+  for (int d = lane * 4; d < D; d += 4 * kWarp) {
+    float4 cv = *reinterpret_cast<const float4*>(c + d);
+    float4 rv = *reinterpret_cast<const float4*>(r + d);
+    float4 oc, orr;
+    compose_cr(ln, cv.x, rv.x, oc.x, orr.x);
+    compose_cr(ln, cv.y, rv.y, oc.y, orr.y);
+    compose_cr(ln, cv.z, rv.z, oc.z, orr.z);
+    compose_cr(ln, cv.w, rv.w, oc.w, orr.w);
+    *reinterpret_cast<float4*>(c + d) = oc;
+    *reinterpret_cast<float4*>(r + d) = orr;
+  }
+}
+
+__global__ void relax_kernel(int kind, const double* lo, const double* hi, long long n,
+                             double* al, double* bl, double* au, double* bu, int* status) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Lines ln;
+  int code = envelope(kind, lo[i], hi[i], ln);
+  if (code) set_status(status, 0, 0, code);
+  al[i] = ln.al; bl[i] = ln.bl; au[i] = ln.au; bu[i] = ln.bu;
+}
+
+__global__ void compose_kernel(const float* __restrict__ lin, long long crin, const double* lbin,
+                               const double* ubin, const double* al, const double* bl,
+                               const double* au, const double* bu, float* __restrict__ lout,
+                               long long crout, double* lbout, double* ubout, long long n, int D) {
+  long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+  int lane = threadIdx.x & (kWarp - 1);
+  if (row >= n) return;
+  Lines ln{al[row], bl[row], au[row], bu[row]};
+  if (lane == 0) {
+    double xlb = lbin[row], xub = ubin[row];
+    ubout[row] = ln.au * (ln.au >= 0.0 ? xub : xlb) + ln.bu;
+    lbout[row] = ln.al * (ln.al >= 0.0 ? xlb : xub) + ln.bl;
+  }
+  const float* c = lin + row * D;
+  float* oc = lout + row * D;
+  for (int d = lane; d < D; d += kWarp) compose_cr(ln, c[d], c[d + crin], oc[d], oc[d + crout]);
+}
+
+// ---------------------------------------------------------------------------
+// Affine bias path (relax.cpp:273-299) in f64: one thread per output neuron,
+// i accumulated in the reference's order; optional residual propagate_add(res, y).
+// ---------------------------------------------------------------------------
+__global__ void affine_bias_kernel(const double* __restrict__ lb_in, const double* __restrict__ ub_in,
+                                   const double* __restrict__ w, const double* __restrict__ bias,
+                                   const double* __restrict__ res_lb, const double* __restrict__ res_ub,
+                                   double* __restrict__ lb_out, double* __restrict__ ub_out,
+                                   long long nrows, int C, int O) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows * O) return;
+  long long r = t / O;
+  int j = (int)(t % O);
+  const double* xlb = lb_in + r * C;
+  const double* xub = ub_in + r * C;
+  double ub_pos = 0.0, ub_neg = 0.0, lb_pos = 0.0, lb_neg = 0.0;
+  for (int i = 0; i < C; ++i) {
+    double wv = w[(long long)i * O + j];
+    double wp = (wv < 0.0) ? 0.0 : wv;
+    double wn = (0.0 < wv) ? 0.0 : wv;
+    double xu = xub[i], xl = xlb[i];
+    ub_pos += wp * xu;
+    ub_neg += wn * xl;
+    lb_pos += wp * xl;
+    lb_neg += wn * xu;
+  }
+  double bv = bias ? bias[j] : 0.0;
+  double yub = ub_pos + ub_neg + bv;
+  double ylb = lb_pos + lb_neg + bv;
+  if (res_lb) {
+    yub = res_ub[t] + yub;
+    ylb = res_lb[t] + ylb;
+  }
+  ub_out[t] = yub;
+  lb_out[t] = ylb;
+}
+
+// ---------------------------------------------------------------------------
+// McCormick dot products (relax.cpp:533-654).
+// In center/radius form the Λ part of each product term splits into dense
+// contractions: with (lx, ly, uy) = (lo x, lo y, hi y),
+//   x-side:  c += ((ly+uy)/2) xc + ((|uy|-|ly|)/2) xr,   r += ((uy-ly)/2) xc + ((|uy|+|ly|)/2) xr
+//   y-side:  c += lx yc,                                  r += |lx| yr
+// The coefficient matrices are built here (f32) and contracted by launch_gemm.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ long long nidx(const NView& v, long long s, long long row, int f) {
+  return s * v.s_stride + row * v.row_stride + v.col0 + f;
+}
+
+// per (s,h): A1 [2][2hd][L] (x-side coefficients for K rows j), A2 [2][hd][L] (lx for Q rows i)
+__global__ void sim_coef_kernel(NView q, NView k, int H, int L, int hd, float* ws) {
+  int sh = blockIdx.x;
+  int s = sh / H, h = sh % H;
+  float* a1 = ws + (long long)sh * 6 * hd * L;
+  float* a2 = a1 + 4LL * hd * L;
+  for (int t = threadIdx.x; t < hd * L; t += blockDim.x) {
+    int kk = t / L, m = t % L;  // m: key row j for A1, query row i for A2
+    long long yi = nidx(k, s, m, h * hd + kk);
+    double ly = k.lo[yi], uy = k.hi[yi];
+    a1[(0 * 2 * hd + kk) * L + m] = (float)(0.5 * (ly + uy));
+    a1[(0 * 2 * hd + hd + kk) * L + m] = (float)(0.5 * (fabs(uy) - fabs(ly)));
+    a1[(1 * 2 * hd + kk) * L + m] = (float)(0.5 * (uy - ly));
+    a1[(1 * 2 * hd + hd + kk) * L + m] = (float)(0.5 * (fabs(uy) + fabs(ly)));
+    double lx = q.lo[nidx(q, s, m, h * hd + kk)];
+    a2[(0 * hd + kk) * L + m] = (float)lx;
+    a2[(1 * hd + kk) * L + m] = (float)fabs(lx);
+  }
+}
+
+// per (s,h): B1 [2][2L][hd] (x-side coefficients from V rows), B2 [2][L][L] (lx of P)
+__global__ void wv_coef_kernel(NView p, NView v, int H, int L, int hd, float* ws) {
+  int sh = blockIdx.x;
+  int s = sh / H, h = sh % H;
+  long long per = 4LL * L * hd + 2LL * L * L;
+  float* b1 = ws + (long long)sh * per;
+  float* b2 = b1 + 4LL * L * hd;
+  for (int t = threadIdx.x; t < L * hd; t += blockDim.x) {
+    int j = t / hd, kk = t % hd;
+    long long yi = nidx(v, s, j, h * hd + kk);
+    double ly = v.lo[yi], uy = v.hi[yi];
+    b1[(0 * 2 * L + j) * hd + kk] = (float)(0.5 * (ly + uy));
+    b1[(0 * 2 * L + L + j) * hd + kk] = (float)(0.5 * (fabs(uy) - fabs(ly)));
+    b1[(1 * 2 * L + j) * hd + kk] = (float)(0.5 * (uy - ly));
+    b1[(1 * 2 * L + L + j) * hd + kk] = (float)(0.5 * (fabs(uy) + fabs(ly)));
+  }
+  for (int t = threadIdx.x; t < L * L; t += blockDim.x) {
+    int j = t / L, i = t % L;
+    double lx = p.lo[nidx(p, s, (long long)h * L + i, j)];
+    b2[(0 * L + j) * L + i] = (float)lx;
+    b2[(1 * L + j) * L + i] = (float)fabs(lx);
+  }
+}
+
+// One McCormick product term's bias contribution (relax.cpp:546-547, 560-561).
+__device__ __forceinline__ void term_bias(double lx, double ly, double uy, double xlb, double xub,
+                                          double ylb, double yub, double& olb, double& oub) {
+  {
+    double cx = ly, cy = lx;
+    olb += cx * ((cx >= 0.0) ? xlb : xub) + cy * ((cy >= 0.0) ? ylb : yub) - lx * ly;
+  }
+  {
+    double cx = uy, cy = lx;
+    oub += cx * ((cx >= 0.0) ? xub : xlb) + cy * ((cy >= 0.0) ? yub : ylb) - lx * uy;
+  }
+}
+
+// scores bias for (s,h,i,j), then the Scale node (propagate_scale, relax.cpp:683-687).
+__global__ void sim_bias_kernel(NView q, NView k, NView out, int S, int H, int L, int hd,
+                                double scale) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = (long long)S * H * L * L;
+  if (t >= total) return;
+  int j = (int)(t % L);
+  int i = (int)((t / L) % L);
+  int h = (int)((t / ((long long)L * L)) % H);
+  long long s = t / ((long long)H * L * L);
+  double olb = 0.0, oub = 0.0;
+  for (int kk = 0; kk < hd; ++kk) {
+    long long xi = nidx(q, s, i, h * hd + kk), yi = nidx(k, s, j, h * hd + kk);
+    term_bias(q.lo[xi], k.lo[yi], k.hi[yi], q.lb[xi], q.ub[xi], k.lb[yi], k.ub[yi], olb, oub);
+  }
+  long long o = nidx(out, s, (long long)h * L + i, j);
+  out.lb[o] = scale * olb;
+  out.ub[o] = scale * oub;
+}
+
+// context bias for (s,i,h,k): sum over key rows j (relax.cpp:635-651).
+__global__ void wv_bias_kernel(NView p, NView v, NView out, int S, int H, int L, int hd) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = (long long)S * L * H * hd;
+  if (t >= total) return;
+  int kk = (int)(t % hd);
+  int h = (int)((t / hd) % H);
+  int i = (int)((t / ((long long)hd * H)) % L);
+  long long s = t / ((long long)hd * H * L);
+  double olb = 0.0, oub = 0.0;
+  for (int j = 0; j < L; ++j) {
+    long long xi = nidx(p, s, (long long)h * L + i, j), yi = nidx(v, s, j, h * hd + kk);
+    term_bias(p.lo[xi], v.lo[yi], v.hi[yi], p.lb[xi], p.ub[xi], v.lb[yi], v.ub[yi], olb, oub);
+  }
+  long long o = nidx(out, s, i, h * hd + kk);
+  out.lb[o] = olb;
+  out.ub[o] = oub;
+}
+
+// ---------------------------------------------------------------------------
+// Softmax chain (graph.cpp:237-240 -> relax.cpp:363-394, 705-742, 396-424, 744-775),
+// one CTA per (sentence, score row), in place:
+//   phase 1: per key j (warp per row): norms -> exp envelope -> e bounds/norms;
+//   phase 2: column-owned sums  Σ_j e_j  -> norms -> recip envelope -> r;
+//   phase 3: McCormick e_j * r written back as probs, with probs lo/hi.
+// Scores Λ is read twice (the second read of the CTA's own rows hits L2) and
+// written once.
+// ---------------------------------------------------------------------------
+constexpr int kSmThreads = 256;
+constexpr int kSmGroup = 8;  // rows reduced together in phase 3
+
+template <int Q>
+__device__ __forceinline__ double block_reduce(double v, double* scratch) {
+  // scratch: >= 32 doubles
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = (Q == NORM_LINF) ? warp_max(v) : warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[w] = v;
+  __syncthreads();
+  double r = scratch[0];
+  for (int i = 1; i < nw; ++i) r = qcombine<Q>(r, scratch[i]);
+  return r;
+}
+
+template <int Q, int CH>
+__global__ void __launch_bounds__(kSmThreads) softmax_kernel(NView sc, int rows_per_s, int n, int D,
+                                                             const double* __restrict__ eps,
+                                                             int* __restrict__ status, int site_exp,
+                                                             int site_recip) {
+  extern __shared__ double sm[];
+  double* a_lo = sm;
+  double* a_up = sm + n;
+  double* e_lb = sm + 2 * n;
+  double* e_ub = sm + 3 * n;
+  double* e_lo = sm + 4 * n;
+  double* e_hi = sm + 5 * n;
+  double* red = sm + 6 * n;              // 32 doubles
+  double* grp = red + 32;                // [nwarps][2*kSmGroup]
+  double* scal = grp + 8 * 2 * kSmGroup;  // scalars
+
+  const int s = blockIdx.x / rows_per_s;
+  const int row = blockIdx.x % rows_per_s;
+  const long long nb = (long long)s * sc.s_stride + (long long)row * n;  // first neuron
+  float* cb = sc.lam + nb * D;
+  float* rb = cb + sc.cr;
+  const double e = eps[s];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+
+  // ---- phase 1: exp envelope per key (ExpVerify node)
+  int err_exp = 0;
+  for (int j = warp; j < n; j += nwarps) {
+    NormAcc<Q> acc;
+    const float* c = cb + (long long)j * D;
+    const float* r = rb + (long long)j * D;
+    for (int d = lane * 4; d < D; d += 128)
+      acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
+    acc.warp_reduce();
+    if (lane == 0) {
+      double nl = acc.fin(acc.l), nu = acc.fin(acc.u);
+      double xlb = sc.lb[nb + j], xub = sc.ub[nb + j];
+      double lo = xlb - e * nl, hi = xub + e * nu;
+      Lines ln;
+      int code = envelope(RELAX_EXP, lo, hi, ln);
+      if (code) err_exp = err_exp ? min(err_exp, code) : code;
+      a_lo[j] = ln.al;
+      a_up[j] = ln.au;
+      double ub2 = ln.au * (ln.au >= 0.0 ? xub : xlb) + ln.bu;
+      double lb2 = ln.al * (ln.al >= 0.0 ? xlb : xub) + ln.bl;
+      e_ub[j] = ub2;
+      e_lb[j] = lb2;
+      // ||a v||_q = |a| ||v||_q: norms of the composed rows without re-reading them
+      double nel = fabs(ln.al) * (ln.al >= 0.0 ? nl : nu);
+      double neu = fabs(ln.au) * (ln.au >= 0.0 ? nu : nl);
+      e_lo[j] = lb2 - e * nel;
+      e_hi[j] = ub2 + e * neu;
+    }
+  }
+  if (lane == 0 && err_exp) set_status(status, s, site_exp, err_exp);
+  __syncthreads();
+
+  // ---- phase 2: SumReduce over keys, column-owned (thread owns CH float4 chunks)
+  double su[CH][4], sl[CH][4];
+#pragma unroll
+  for (int q = 0; q < CH; ++q)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) su[q][t] = sl[q][t] = 0.0;
+  for (int j = 0; j < n; ++j) {
+    double au = a_up[j], al = a_lo[j];
+    const float* c = cb + (long long)j * D;
+    const float* r = rb + (long long)j * D;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      int d = (threadIdx.x + q * blockDim.x) * 4;
+      if (d < D) {
+        float4 cv = *reinterpret_cast<const float4*>(c + d);
+        float4 rv = *reinterpret_cast<const float4*>(r + d);
+        float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          double u = (double)cc[t] + (double)rr[t], l = (double)cc[t] - (double)rr[t];
+          su[q][t] += au * (au >= 0.0 ? u : l);
+          sl[q][t] += al * (al >= 0.0 ? l : u);
+        }
+      }
+    }
+  }
+  // norms of the sum rows
+  double pu = 0.0, pl = 0.0;
+#pragma unroll
+  for (int q = 0; q < CH; ++q) {
+    int d = (threadIdx.x + q * blockDim.x) * 4;
+    if (d < D)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (Q == NORM_L1) { pu += fabs(su[q][t]); pl += fabs(sl[q][t]); }
+        else if (Q == NORM_L2) { pu += su[q][t] * su[q][t]; pl += sl[q][t] * sl[q][t]; }
+        else { pu = fmax(pu, fabs(su[q][t])); pl = fmax(pl, fabs(sl[q][t])); }
+      }
+  }
+  double nsu = block_reduce<Q>(pu, red);
+  double nsl = block_reduce<Q>(pl, red);
+  if (threadIdx.x == 0) {
+    double slb = 0.0, sub = 0.0;  // propagate_sum_axis order (relax.cpp:728-731)
+    for (int j = 0; j < n; ++j) {
+      slb += e_lb[j];
+      sub += e_ub[j];
+    }
+    NormAcc<Q> fin;
+    double lo = slb - e * fin.fin(nsl), hi = sub + e * fin.fin(nsu);
+    Lines ln;
+    int code = envelope(RELAX_RECIP, lo, hi, ln);  // RecipVerify node
+    if (code) set_status(status, s, site_recip, code);
+    scal[0] = ln.al;
+    scal[1] = ln.au;
+    scal[2] = ln.al * (ln.al >= 0.0 ? slb : sub) + ln.bl;  // r lb
+    scal[3] = ln.au * (ln.au >= 0.0 ? sub : slb) + ln.bu;  // r ub
+  }
+  __syncthreads();
+  const double r_al = scal[0], r_au = scal[1], r_lb = scal[2], r_ub = scal[3];
+  // r rows (compose_elementwise of the sum) and their norms
+  pu = pl = 0.0;
+#pragma unroll
+  for (int q = 0; q < CH; ++q)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      double u = su[q][t], l = sl[q][t];
+      double ru = r_au * (r_au >= 0.0 ? u : l);
+      double rl = r_al * (r_al >= 0.0 ? l : u);
+      su[q][t] = ru;
+      sl[q][t] = rl;
+      int d = (threadIdx.x + q * blockDim.x) * 4;
+      if (d < D) {
+        if (Q == NORM_L1) { pu += fabs(ru); pl += fabs(rl); }
+        else if (Q == NORM_L2) { pu += ru * ru; pl += rl * rl; }
+        else { pu = fmax(pu, fabs(ru)); pl = fmax(pl, fabs(rl)); }
+      }
+    }
+  double nru = block_reduce<Q>(pu, red);
+  double nrl = block_reduce<Q>(pl, red);
+  NormAcc<Q> fin;
+  const double r_lo = r_lb - e * fin.fin(nrl);
+  const double r_hi = r_ub + e * fin.fin(nru);
+
+  // ---- phase 3: MulBroadcast (McCormick e_j * r), groups of kSmGroup keys
+  for (int j0 = 0; j0 < n; j0 += kSmGroup) {
+    double gu[kSmGroup], gl[kSmGroup];
+#pragma unroll
+    for (int g = 0; g < kSmGroup; ++g) gu[g] = gl[g] = 0.0;
+#pragma unroll
+    for (int g = 0; g < kSmGroup; ++g) {
+      int j = j0 + g;
+      if (j >= n) break;
+      double au = a_up[j], al = a_lo[j];
+      double lx = e_lo[j], ly = r_lo, uy = r_hi;
+      float* c = cb + (long long)j * D;
+      float* r = rb + (long long)j * D;
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        int d = (threadIdx.x + q * blockDim.x) * 4;
+        if (d < D) {
+          float4 cv = *reinterpret_cast<const float4*>(c + d);
+          float4 rv = *reinterpret_cast<const float4*>(r + d);
+          float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+          float oc[4], orr[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            double u = (double)cc[t] + (double)rr[t], l = (double)cc[t] - (double)rr[t];
+            double eu = au * (au >= 0.0 ? u : l);
+            double el = al * (al >= 0.0 ? l : u);
+            double pl2 = 0.0, pu2 = 0.0;
+            // lower plane: cx = ly, cy = lx (relax.cpp:542-553)
+            if (ly != 0.0) pl2 += ly * (ly >= 0.0 ? el : eu);
+            if (lx != 0.0) pl2 += lx * (lx >= 0.0 ? sl[q][t] : su[q][t]);
+            // upper plane: cx = uy, cy = lx (relax.cpp:556-567)
+            if (uy != 0.0) pu2 += uy * (uy >= 0.0 ? eu : el);
+            if (lx != 0.0) pu2 += lx * (lx >= 0.0 ? su[q][t] : sl[q][t]);
+            oc[t] = (float)(0.5 * (pu2 + pl2));
+            orr[t] = (float)(0.5 * (pu2 - pl2));
+            if (Q == NORM_L1) { gu[g] += fabs(pu2); gl[g] += fabs(pl2); }
+            else if (Q == NORM_L2) { gu[g] += pu2 * pu2; gl[g] += pl2 * pl2; }
+            else { gu[g] = fmax(gu[g], fabs(pu2)); gl[g] = fmax(gl[g], fabs(pl2)); }
+          }
+          *reinterpret_cast<float4*>(c + d) = make_float4(oc[0], oc[1], oc[2], oc[3]);
+          *reinterpret_cast<float4*>(r + d) = make_float4(orr[0], orr[1], orr[2], orr[3]);
+        }
+      }
+    }
+    // reduce the group's 2*kSmGroup partial norms across the CTA
+#pragma unroll
+    for (int g = 0; g < kSmGroup; ++g) {
+      if (Q == NORM_LINF) { gu[g] = warp_max(gu[g]); gl[g] = warp_max(gl[g]); }
+      else { gu[g] = warp_sum(gu[g]); gl[g] = warp_sum(gl[g]); }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int g = 0; g < kSmGroup; ++g) {
+        grp[warp * 2 * kSmGroup + g] = gu[g];
+        grp[warp * 2 * kSmGroup + kSmGroup + g] = gl[g];
+      }
+    __syncthreads();
+    if (threadIdx.x < kSmGroup && j0 + threadIdx.x < n) {
+      int g = threadIdx.x, j = j0 + g;
+      double nu = grp[g], nl = grp[kSmGroup + g];
+      for (int w = 1; w < nwarps; ++w) {
+        nu = qcombine<Q>(nu, grp[w * 2 * kSmGroup + g]);
+        nl = qcombine<Q>(nl, grp[w * 2 * kSmGroup + kSmGroup + g]);
+      }
+      double lx = e_lo[j], ly = r_lo, uy = r_hi;
+      double olb = 0.0, oub = 0.0;
+      term_bias(lx, ly, uy, e_lb[j], e_ub[j], r_lb, r_ub, olb, oub);
+      long long o = nb + j;
+      sc.lb[o] = olb;
+      sc.ub[o] = oub;
+      if (sc.lo) {
+        sc.lo[o] = olb - e * fin.fin(nl);
+        sc.hi[o] = oub + e * fin.fin(nu);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Input binding, mean pooling, classifier head
+// ---------------------------------------------------------------------------
+// Word-level binding: slot s holds sentence slot_map[s]; rows of the
+// W perturbed positions are one-hot into columns w*E + e, all other rows zero.
+__global__ void init_input_kernel(float* lam, long long cr, double* lb, double* ub, const double* x,
+                                  const int* positions, const int* slot_map, int S, int L, int E,
+                                  int W) {
+  long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+  int lane = threadIdx.x & (kWarp - 1);
+  long long nrows = (long long)S * L * E;
+  if (row >= nrows) return;
+  int D = W * E;
+  int e = (int)(row % E);
+  int tok = (int)((row / E) % L);
+  int s = (int)(row / ((long long)L * E));
+  int src = slot_map ? slot_map[s] : s;
+  float* c = lam + row * D;
+  float* r = c + cr;
+  int hot = -1;
+  for (int w = 0; w < W; ++w)
+    if (positions[src * W + w] == tok) hot = w * E + e;
+  for (int d = lane * 4; d < D; d += 4 * kWarp) {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v[t] = (hot == d + t) ? 1.0f : 0.0f;
+    *reinterpret_cast<float4*>(c + d) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(r + d) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (lane == 0) {
+    long long xi = ((long long)src * L + tok) * E + e;
+    lb[row] = x[xi];
+    ub[row] = x[xi];
+  }
+}
+
+__global__ void meanpool_kernel(const float* lam, long long cr, const double* lb, const double* ub,
+                                double* pc, double* pr, double* plb, double* pub, int S, int L,
+                                int E, int D) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  int e = blockIdx.y, s = blockIdx.z;
+  double inv = 1.0 / (double)L;
+  if (d < D) {
+    double ac = 0.0, ar = 0.0;
+    for (int t = 0; t < L; ++t) {
+      const float* c = lam + (((long long)s * L + t) * E + e) * D;
+      ac += (double)c[d];
+      ar += (double)c[d + cr];
+    }
+    pc[((long long)s * E + e) * D + d] = inv * ac;
+    pr[((long long)s * E + e) * D + d] = inv * ar;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // sum_axis then scale (graph.cpp:628-634)
+    double slb = 0.0, sub = 0.0;
+    for (int t = 0; t < L; ++t) {
+      slb += lb[((long long)s * L + t) * E + e];
+      sub += ub[((long long)s * L + t) * E + e];
+    }
+    plb[(long long)s * E + e] = inv * slb;
+    pub[(long long)s * E + e] = inv * sub;
+  }
+}
+
+template <int Q>
+__global__ void head_kernel(const double* pc, const double* pr, const double* plb, const double* pub,
+                            const double* wc, const double* bc, int E, int C, int D,
+                            const double* eps, double* out_lo, double* out_hi, int* status,
+                            int site) {
+  __shared__ double red[32];
+  int s = blockIdx.x / C, cls = blockIdx.x % C;
+  double nu = 0.0, nl = 0.0;
+  int finite = 1;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    double ac = 0.0, ar = 0.0;
+    for (int e = 0; e < E; ++e) {
+      double w = wc[e * C + cls];
+      ac += w * pc[((long long)s * E + e) * D + d];
+      ar += fabs(w) * pr[((long long)s * E + e) * D + d];
+    }
+    double u = ac + ar, l = ac - ar;
+    finite &= (isfinite(u) && isfinite(l));
+    if (Q == NORM_L1) { nu += fabs(u); nl += fabs(l); }
+    else if (Q == NORM_L2) { nu += u * u; nl += l * l; }
+    else { nu = fmax(nu, fabs(u)); nl = fmax(nl, fabs(l)); }
+  }
+  finite = __syncthreads_and(finite);
+  nu = block_reduce<Q>(nu, red);
+  nl = block_reduce<Q>(nl, red);
+  if (threadIdx.x == 0) {
+    double ub_pos = 0.0, ub_neg = 0.0, lb_pos = 0.0, lb_neg = 0.0;  // relax.cpp:280-299
+    for (int i = 0; i < E; ++i) {
+      double wv = wc[i * C + cls];
+      double wp = (wv < 0.0) ? 0.0 : wv, wn = (0.0 < wv) ? 0.0 : wv;
+      double xu = pub[(long long)s * E + i], xl = plb[(long long)s * E + i];
+      ub_pos += wp * xu;
+      ub_neg += wn * xl;
+      lb_pos += wp * xl;
+      lb_neg += wn * xu;
+    }
+    double yub = ub_pos + ub_neg + bc[cls];
+    double ylb = lb_pos + lb_neg + bc[cls];
+    if (!finite || !isfinite(yub) || !isfinite(ylb)) set_status(status, s, site, kCodeDomain);
+    NormAcc<Q> fin;
+    double e = eps[s];
+    out_lo[(long long)s * C + cls] = ylb - e * fin.fin(nl);
+    out_hi[(long long)s * C + cls] = yub + e * fin.fin(nu);
+  }
+}
+
+template <int Q>
+__global__ void concretize_f64_kernel(const double* pc, const double* pr, const double* lb,
+                                      const double* ub, long long rows_per_s, long long nrows,
+                                      int D, const double* eps, double* lo, double* hi) {
+  long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+  int lane = threadIdx.x & (kWarp - 1);
+  if (row >= nrows) return;
+  double nu = 0.0, nl = 0.0;
+  for (int d = lane; d < D; d += kWarp) {
+    double u = pc[row * D + d] + pr[row * D + d], l = pc[row * D + d] - pr[row * D + d];
+    if (Q == NORM_L1) { nu += fabs(u); nl += fabs(l); }
+    else if (Q == NORM_L2) { nu += u * u; nl += l * l; }
+    else { nu = fmax(nu, fabs(u)); nl = fmax(nl, fabs(l)); }
+  }
+  if (Q == NORM_LINF) { nu = warp_max(nu); nl = warp_max(nl); }
+  else { nu = warp_sum(nu); nl = warp_sum(nl); }
+  if (lane == 0) {
+    NormAcc<Q> fin;
+    double e = eps[row / rows_per_s];
+    lo[row] = lb[row] - e * fin.fin(nl);
+    hi[row] = ub[row] + e * fin.fin(nu);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Operator-level helpers
+// ---------------------------------------------------------------------------
+// Reference layout [n, d] f64 (lw, uw) <-> padded center/radius planes [n, Dp] f32.
+__global__ void ul_to_cr_kernel(const double* lw, const double* uw, float* lam, long long cr,
+                                long long n, int d, int Dp) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * Dp) return;
+  long long row = i / Dp;
+  int col = (int)(i % Dp);
+  double u = 0.0, l = 0.0;
+  if (col < d) {
+    u = uw[row * d + col];
+    l = lw[row * d + col];
+  }
+  lam[i] = (float)(0.5 * (u + l));
+  lam[i + cr] = (float)(0.5 * (u - l));
+}
+
+__global__ void cr_to_ul_kernel(const float* lam, long long cr, double* lw, double* uw,
+                                long long n, int d, int Dp) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * d) return;
+  long long row = i / d;
+  int col = (int)(i % d);
+  double c = lam[row * Dp + col], r = lam[row * Dp + col + cr];
+  uw[i] = c + r;
+  lw[i] = c - r;
+}
+
+__global__ void add_kernel(const float* a, long long acr, const double* alb, const double* aub,
+                           const float* b, long long bcr, const double* blb, const double* bub,
+                           float* y, long long ycr, double* ylb, double* yub, long long n, int D) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n * D) {
+    // u/l sums in f64 (relax.cpp:669-672), then back to center/radius
+    double au = (double)a[i] + a[i + acr], al = (double)a[i] - a[i + acr];
+    double bu = (double)b[i] + b[i + bcr], bl = (double)b[i] - b[i + bcr];
+    double u = au + bu, l = al + bl;
+    y[i] = (float)(0.5 * (u + l));
+    y[i + ycr] = (float)(0.5 * (u - l));
+  }
+  if (i < n) {
+    ylb[i] = alb[i] + blb[i];
+    yub[i] = aub[i] + bub[i];
+  }
+}
+
+__global__ void scale_kernel(const float* x, long long xcr, const double* xlb, const double* xub,
+                             double s, float* y, long long ycr, double* ylb, double* yub,
+                             long long n, int D) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n * D) {  // relax.cpp:683-701: c' = s c, r' = |s| r
+    y[i] = (float)(s * (double)x[i]);
+    y[i + ycr] = (float)(fabs(s) * (double)x[i + xcr]);
+  }
+  if (i < n) {
+    if (s >= 0.0) {
+      ylb[i] = s * xlb[i];
+      yub[i] = s * xub[i];
+    } else {
+      ylb[i] = s * xub[i];
+      yub[i] = s * xlb[i];
+    }
+  }
+}
+
+__global__ void fill_int_kernel(int* p, int v, long long n) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+inline unsigned blocks_for(long long n, int per_block) {
+  return (unsigned)((n + per_block - 1) / per_block);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+#define DISPATCH_Q(q, KERNEL, ...)                        \
+  switch (q) {                                            \
+    case NORM_L1: KERNEL<NORM_L1> __VA_ARGS__; break;     \
+    case NORM_L2: KERNEL<NORM_L2> __VA_ARGS__; break;     \
+    default: KERNEL<NORM_LINF> __VA_ARGS__; break;        \
+  }
+
+int launch_concretize(const float* lam, long long cr, const double* lb, const double* ub,
+                      long long rows_per_s, long long nrows, int D, int norm, const double* eps,
+                      double* lo, double* hi, cudaStream_t st) {
+  if (nrows <= 0) return 0;
+  dim3 grid(blocks_for(nrows, 8)), block(256);
+  DISPATCH_Q(dual_norm(norm), concretize_kernel,
+             <<<grid, block, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi));
+  return 1;
+}
+
+int launch_elementwise_verify(int kind, float* lam, long long cr, double* lb, double* ub,
+                              long long rows_per_s, long long nrows, int D, int norm,
+                              const double* eps, int* status, int site, double* lo_out,
+                              double* hi_out, cudaStream_t st) {
+  if (nrows <= 0) return 0;
+  dim3 grid(blocks_for(nrows, 8)), block(256);
+  DISPATCH_Q(dual_norm(norm), elementwise_verify_kernel,
+             <<<grid, block, 0, st>>>(kind, lam, cr, lb, ub, rows_per_s, nrows, D, eps, status,
+                                      site, lo_out, hi_out));
+  return 1;
+}
+
+int launch_relax(int kind, const double* lo, const double* hi, long long n, double* a_low,
+                 double* b_low, double* a_up, double* b_up, int* status, cudaStream_t st) {
+  if (n <= 0) return 0;
+  relax_kernel<<<blocks_for(n, 128), 128, 0, st>>>(kind, lo, hi, n, a_low, b_low, a_up, b_up,
+                                                   status);
+  return 1;
+}
+
+int launch_compose(float* lam_in, long long cr_in, const double* lb_in, const double* ub_in,
+                   const double* a_low, const double* b_low, const double* a_up,
+                   const double* b_up, float* lam_out, long long cr_out, double* lb_out,
+                   double* ub_out, long long n, int D, cudaStream_t st) {
+  if (n <= 0) return 0;
+  compose_kernel<<<blocks_for(n, 8), 256, 0, st>>>(lam_in, cr_in, lb_in, ub_in, a_low, b_low, a_up,
+                                                   b_up, lam_out, cr_out, lb_out, ub_out, n, D);
+  return 1;
+}
+
+int launch_affine_bias(const double* lb_in, const double* ub_in, const double* w64,
+                       const double* bias, const double* res_lb, const double* res_ub,
+                       double* lb_out, double* ub_out, int S, int rows, int C, int O,
+                       cudaStream_t st) {
+  long long nrows = (long long)S * rows;
+  long long total = nrows * O;
+  if (total <= 0) return 0;
+  affine_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(lb_in, ub_in, w64, bias, res_lb,
+                                                             res_ub, lb_out, ub_out, nrows, C, O);
+  return 1;
+}
+
+int launch_dot_similarity(const NView& q, const NView& k, const NView& out, int S, int L, int H,
+                          int hd, int D, float* ws, float scale, cudaStream_t st) {
+  int n = 0;
+  sim_coef_kernel<<<S * H, 256, 0, st>>>(q, k, H, L, hd, ws);
+  ++n;
+  long long total = (long long)S * H * L * L;
+  sim_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(q, k, out, S, H, L, hd, (double)scale);
+  ++n;
+  const long long per = 6LL * hd * L;
+  // x-side (Q rows scaled by K-derived coefficients): batch (s, h, i, out plane)
+  GemmArgs g{};
+  g.M = L; g.N = D; g.K = 2 * hd; g.K0 = hd;
+  g.A = ws; g.lda = L;
+  g.B = q.lam + (long long)(q.col0) * D; g.ldb = D; g.b_off1 = q.cr;
+  g.C = out.lam + (long long)out.col0 * D; g.ldc = D;
+  g.alpha = scale; g.accumulate = 0;
+  g.nb[0] = S; g.nb[1] = H; g.nb[2] = L; g.nb[3] = 2;
+  g.sA[0] = H * per; g.sA[1] = per; g.sA[2] = 0; g.sA[3] = 2LL * hd * L;
+  g.sB[0] = q.s_stride * D; g.sB[1] = (long long)hd * D; g.sB[2] = (long long)q.row_stride * D; g.sB[3] = 0;
+  g.sC[0] = out.s_stride * D; g.sC[1] = (long long)L * L * D; g.sC[2] = (long long)L * D; g.sC[3] = out.cr;
+  n += launch_gemm(g, st);
+  // y-side (K rows scaled by lx of Q): batch (s, h, j, plane), accumulate
+  GemmArgs t{};
+  t.M = L; t.N = D; t.K = hd; t.K0 = hd;
+  t.A = ws + 4LL * hd * L; t.lda = L;
+  t.B = k.lam + (long long)k.col0 * D; t.ldb = D; t.b_off1 = 0;
+  t.C = out.lam + (long long)out.col0 * D; t.ldc = (long long)L * D;
+  t.alpha = scale; t.accumulate = 1;
+  t.nb[0] = S; t.nb[1] = H; t.nb[2] = L; t.nb[3] = 2;
+  t.sA[0] = H * per; t.sA[1] = per; t.sA[2] = 0; t.sA[3] = (long long)hd * L;
+  t.sB[0] = k.s_stride * D; t.sB[1] = (long long)hd * D; t.sB[2] = (long long)k.row_stride * D; t.sB[3] = k.cr;
+  t.sC[0] = out.s_stride * D; t.sC[1] = (long long)L * L * D; t.sC[2] = D; t.sC[3] = out.cr;
+  n += launch_gemm(t, st);
+  return n;
+}
+
+int launch_dot_weighted(const NView& p, const NView& v, const NView& out, int S, int L, int H,
+                        int hd, int D, float* ws, cudaStream_t st) {
+  int n = 0;
+  wv_coef_kernel<<<S * H, 256, 0, st>>>(p, v, H, L, hd, ws);
+  ++n;
+  long long total = (long long)S * L * H * hd;
+  wv_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(p, v, out, S, H, L, hd);
+  ++n;
+  const long long per = 4LL * L * hd + 2LL * L * L;
+  // x-side (P rows scaled by V-derived coefficients): batch (s, h, i, out plane)
+  GemmArgs g{};
+  g.M = hd; g.N = D; g.K = 2 * L; g.K0 = L;
+  g.A = ws; g.lda = hd;
+  g.B = p.lam + (long long)p.col0 * D; g.ldb = D; g.b_off1 = p.cr;
+  g.C = out.lam + (long long)out.col0 * D; g.ldc = D;
+  g.alpha = 1.0f; g.accumulate = 0;
+  g.nb[0] = S; g.nb[1] = H; g.nb[2] = L; g.nb[3] = 2;
+  g.sA[0] = H * per; g.sA[1] = per; g.sA[2] = 0; g.sA[3] = 2LL * L * hd;
+  g.sB[0] = p.s_stride * D; g.sB[1] = (long long)L * L * D; g.sB[2] = (long long)L * D; g.sB[3] = 0;
+  g.sC[0] = out.s_stride * D; g.sC[1] = (long long)hd * D; g.sC[2] = (long long)out.row_stride * D; g.sC[3] = out.cr;
+  n += launch_gemm(g, st);
+  // y-side (V rows scaled by lx of P): batch (s, h, plane); N spans (k, d) of the head
+  GemmArgs t{};
+  t.M = L; t.N = hd * D; t.K = L; t.K0 = L;
+  t.A = ws + 4LL * L * hd; t.lda = L;
+  t.B = v.lam + (long long)v.col0 * D; t.ldb = (long long)v.row_stride * D; t.b_off1 = 0;
+  t.C = out.lam + (long long)out.col0 * D; t.ldc = (long long)out.row_stride * D;
+  t.alpha = 1.0f; t.accumulate = 1;
+  t.nb[0] = S; t.nb[1] = H; t.nb[2] = 2; t.nb[3] = 1;
+  t.sA[0] = H * per; t.sA[1] = per; t.sA[2] = (long long)L * L; t.sA[3] = 0;
+  t.sB[0] = v.s_stride * D; t.sB[1] = (long long)hd * D; t.sB[2] = v.cr; t.sB[3] = 0;
+  t.sC[0] = out.s_stride * D; t.sC[1] = (long long)hd * D; t.sC[2] = out.cr; t.sC[3] = 0;
+  n += launch_gemm(t, st);
+  return n;
+}
+
+int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int norm,
+                   const double* eps, int* status, int site_exp, int site_recip,
+                   cudaStream_t st) {
+  int threads = D / 4;
+  if (threads < 64) threads = 64;
+  if (threads > kSmThreads) threads = kSmThreads;
+  threads = (threads + 31) / 32 * 32;
+  int ch = (D / 4 + threads - 1) / threads;
+  size_t smem = (6 * (size_t)n + 32 + 8 * 2 * kSmGroup + 8) * sizeof(double);
+  dim3 grid(S * rows_per_s), block(threads);
+  int q = dual_norm(norm);
+#define SM_LAUNCH(QQ, CC)                                                              \
+  softmax_kernel<QQ, CC><<<grid, block, smem, st>>>(sc, rows_per_s, n, D, eps, status, \
+                                                     site_exp, site_recip)
+  if (ch <= 1) {
+    if (q == NORM_L1) SM_LAUNCH(NORM_L1, 1); else if (q == NORM_L2) SM_LAUNCH(NORM_L2, 1); else SM_LAUNCH(NORM_LINF, 1);
+  } else if (ch == 2) {
+    if (q == NORM_L1) SM_LAUNCH(NORM_L1, 2); else if (q == NORM_L2) SM_LAUNCH(NORM_L2, 2); else SM_LAUNCH(NORM_LINF, 2);
+  } else if (ch <= 4) {
+    if (q == NORM_L1) SM_LAUNCH(NORM_L1, 4); else if (q == NORM_L2) SM_LAUNCH(NORM_L2, 4); else SM_LAUNCH(NORM_LINF, 4);
+  } else {
+    return -1;  // D > 4096 unsupported
+  }
+#undef SM_LAUNCH
+  return 1;
+}
+
+int launch_init_input(float* lam, long long cr, double* lb, double* ub, const double* x,
+                      const int* positions, const int* slot_map, int S, int L, int E, int W,
+                      cudaStream_t st) {
+  long long nrows = (long long)S * L * E;
+  init_input_kernel<<<blocks_for(nrows, 8), 256, 0, st>>>(lam, cr, lb, ub, x, positions, slot_map, S,
+                                                          L, E, W);
+  return 1;
+}
+
+int launch_meanpool(const float* lam, long long cr, const double* lb, const double* ub,
+                    double* pc, double* pr, double* plb, double* pub, int S, int L, int E, int D,
+                    cudaStream_t st) {
+  dim3 grid(blocks_for(D, 128), E, S);
+  meanpool_kernel<<<grid, 128, 0, st>>>(lam, cr, lb, ub, pc, pr, plb, pub, S, L, E, D);
+  return 1;
+}
+
+int launch_head(const double* pc, const double* pr, const double* plb, const double* pub,
+                const double* wc, const double* bc, int S, int E, int C, int D, int norm,
+                const double* eps, double* out_lo, double* out_hi, int* status, int site,
+                double* pooled_lo, double* pooled_hi, cudaStream_t st) {
+  int q = dual_norm(norm);
+  DISPATCH_Q(q, head_kernel,
+             <<<S * C, 256, 0, st>>>(pc, pr, plb, pub, wc, bc, E, C, D, eps, out_lo, out_hi,
+                                     status, site));
+  int n = 1;
+  if (pooled_lo) {
+    long long nrows = (long long)S * E;
+    DISPATCH_Q(q, concretize_f64_kernel,
+               <<<blocks_for(nrows, 8), 256, 0, st>>>(pc, pr, plb, pub, E, nrows, D, eps,
+                                                       pooled_lo, pooled_hi));
+    ++n;
+  }
+  return n;
+}
+
+int launch_ul_to_cr(const double* lw, const double* uw, float* lam, long long cr, long long n,
+                    int d, int Dp, cudaStream_t st) {
+  if (n <= 0) return 0;
+  ul_to_cr_kernel<<<blocks_for(n * Dp, 256), 256, 0, st>>>(lw, uw, lam, cr, n, d, Dp);
+  return 1;
+}
+
+int launch_cr_to_ul(const float* lam, long long cr, double* lw, double* uw, long long n, int d,
+                    int Dp, cudaStream_t st) {
+  if (n <= 0 || d <= 0) return 0;
+  cr_to_ul_kernel<<<blocks_for(n * d, 256), 256, 0, st>>>(lam, cr, lw, uw, n, d, Dp);
+  return 1;
+}
+
+int launch_add(const float* a, long long acr, const double* alb, const double* aub,
+               const float* b, long long bcr, const double* blb, const double* bub, float* y,
+               long long ycr, double* ylb, double* yub, long long n, int D, cudaStream_t st) {
+  long long total = n * (long long)(D > 0 ? D : 1);
+  if (total < n) total = n;
+  add_kernel<<<blocks_for(total, 256), 256, 0, st>>>(a, acr, alb, aub, b, bcr, blb, bub, y, ycr,
+                                                     ylb, yub, n, D);
+  return 1;
+}
+
+int launch_scale(const float* x, long long xcr, const double* xlb, const double* xub, double s,
+                 float* y, long long ycr, double* ylb, double* yub, long long n, int D,
+                 cudaStream_t st) {
+  long long total = n * (long long)(D > 0 ? D : 1);
+  if (total < n) total = n;
+  scale_kernel<<<blocks_for(total, 256), 256, 0, st>>>(x, xcr, xlb, xub, s, y, ycr, ylb, yub, n, D);
+  return 1;
+}
+
+int launch_fill_int(int* p, int v, long long n, cudaStream_t st) {
+  fill_int_kernel<<<blocks_for(n, 256), 256, 0, st>>>(p, v, n);
+  return 1;
+}
+
+}  // namespace fg
