@@ -129,6 +129,12 @@ def load_library():
     L.fg_maxeps.argtypes = [vp, C.c_int, _dp, _ip, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _dp, _ip,
                             _ip, _ip]
     L.fg_last_run_stats.argtypes = [vp, C.POINTER(RunStats)]
+    L.fg_param_count.restype = sz
+    L.fg_param_count.argtypes = [C.POINTER(FgConfig)]
+    L.fg_gen_synthetic.argtypes = [C.POINTER(FgConfig), C.c_uint64, _dp]
+    L.fg_gen_input.argtypes = [C.POINTER(FgConfig), C.c_uint64, _dp]
+    L.fg_gen_positions.argtypes = [C.c_uint64, C.c_int, C.c_int, _ip]
+    L.fg_profile_pass.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_char_p, _dp, _ip, _ip]
     _lib = L
     return L
 
@@ -317,6 +323,32 @@ class ModelConfig:
                         RELAX[self.activation])
 
 
+def gen_synthetic(cfg: "ModelConfig", seed: int) -> np.ndarray:
+    """model::gen_synthetic weights (model.cpp:99-131) in gen_synthetic order."""
+    lib = load_library()
+    fc = cfg.fg()
+    p = np.zeros(int(lib.fg_param_count(C.byref(fc))))
+    if lib.fg_gen_synthetic(C.byref(fc), seed, _d(p)) != FG_OK:
+        raise InvalidArgument("gen_synthetic: invalid config")
+    return p
+
+
+def gen_input(cfg: "ModelConfig", seed: int) -> np.ndarray:
+    """model::gen_synthetic_input (model.cpp:133-141) -> [L*E]."""
+    lib = load_library()
+    x = np.zeros(cfg.length * cfg.embed)
+    lib.fg_gen_input(C.byref(cfg.fg()), seed, _d(x))
+    return x
+
+
+def gen_positions(seed: int, length: int, words: int) -> np.ndarray:
+    lib = load_library()
+    p = np.zeros(words, dtype=np.int32)
+    if lib.fg_gen_positions(seed, length, words, _i(p)) != FG_OK:
+        raise InvalidArgument("gen_positions: words must be in [1, length]")
+    return p
+
+
 class Model:
     """fg_model: weights resident in HBM; batched bound passes, certify and max-epsilon."""
 
@@ -398,6 +430,21 @@ class Model:
         self.ctx._check(self.lib.fg_maxeps(self.handle, S, _d(x), _i(pos), pos.shape[1], NORM[norm], eps_max, tol,
                                            slots, _d(eps), _i(calls), _i(pred), _i(st)), "fg_maxeps")
         return {"eps": eps, "calls": calls, "predicted": pred, "status": st}
+
+    def profile_pass(self, norm: str, eps: float) -> dict:
+        """One eager pass with CUDA events around every launch site -> {site: (ms, kernels)}."""
+        names = C.create_string_buffer(32 * 64)
+        ms = np.zeros(64)
+        kern = np.zeros(64, dtype=np.int32)
+        n = np.zeros(1, dtype=np.int32)
+        self.ctx._check(self.lib.fg_profile_pass(self.handle, NORM[norm], eps, 64, names, _d(ms), _i(kern), _i(n)),
+                        "fg_profile_pass")
+        raw = names.raw
+        out = {}
+        for i in range(int(n[0])):
+            tag = raw[32 * i:32 * (i + 1)].split(b"\0", 1)[0].decode()
+            out[tag] = (float(ms[i]), int(kern[i]))
+        return out
 
     def last_stats(self) -> dict:
         s = RunStats()
