@@ -186,6 +186,13 @@ fg_status fg_gen_positions(uint64_t seed, int length, int words, int* positions)
 fg_status fg_profile_pass(fg_model* model, int norm, double eps, int max_sites, char* names,
                           double* ms, int* kernels, int* nsites);
 
+/* Self-test of the affine bound GEMM (propagate_affine's Λ contraction) on random data:
+ * tcgen05 3xTF32 kernel and FP32 SIMT kernel vs an f64 device reference.  err_* =
+ * max|Y - Y_ref| / max|Y_ref| (err_umma = -1 if the shape is not tcgen05-eligible:
+ * O % 128, C % 32, D % 128); ms_* = CUDA-event time of one launch. */
+fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_t seed, double* err_umma,
+                             double* err_simt, double* ms_umma, double* ms_simt);
+
 /* Timing of the last fg_maxeps / fg_bound_pass call, measured with CUDA events on the
  * library's stream (device time), and pass counts. */
 typedef struct {

@@ -20,6 +20,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + os.pat
 SOURCES = {
     "fg_kernels.cu": ["-fmad=false"],
     "fg_gemm.cu": [],
+    "fg_umma.cu": [],
     "fg_host.cu": [],
 }
 

@@ -225,8 +225,27 @@ bool eps_ok(double eps) { return eps >= 0.0 && std::isfinite(eps); }  // bounds.
 
 // Weights of one affine layer on the device: W and |W| as f32 [C][O] (M-major
 // GEMM A operand: A[m=j, k=i] = W[i*O + j]), W as f64 for the bias path, bias f64.
+struct alignas(64) TensorMap {
+  unsigned char bytes[128];
+};
+
+// Round to the nearest TF32 value (ties away from zero), as cvt.rna.tf32.f32.
+float tf32_rna(float x) {
+  uint32_t b;
+  std::memcpy(&b, &x, 4);
+  if ((b & 0x7f800000u) != 0x7f800000u) {
+    b += 0x1000u;
+    b &= 0xffffe000u;
+  }
+  std::memcpy(&x, &b, 4);
+  return x;
+}
+
 struct DevAffine {
   DBuf w32, w64, b64;
+  DBuf a_hi, a_lo;        // [2][O][C] f32: (W^T, |W|^T) split for 3xTF32 (tcgen05 path)
+  TensorMap tm_hi, tm_lo;
+  bool umma = false;
   int C = 0, O = 0;
 };
 
@@ -249,7 +268,46 @@ fg_status upload_affine(fg_ctx* ctx, DevAffine& a, int C, int O, const std::vect
   } else {
     CK(cudaMemset(a.b64.p, 0, sizeof(double) * O));
   }
+  // tcgen05 operands: transposed (K-major) and split into TF32 hi/lo parts once.
+  if (umma_supported(O, 128, C)) {
+    std::vector<float> hi(2 * (size_t)C * O), lo(2 * (size_t)C * O);
+    for (int plane = 0; plane < 2; ++plane)
+      for (int j = 0; j < O; ++j)
+        for (int i = 0; i < C; ++i) {
+          float v = w32[(size_t)plane * C * O + (size_t)i * O + j];
+          float h = tf32_rna(v);
+          size_t o = (size_t)plane * O * C + (size_t)j * C + i;
+          hi[o] = h;
+          lo[o] = v - h;
+        }
+    CK(a.a_hi.alloc(sizeof(float) * hi.size()));
+    CK(a.a_lo.alloc(sizeof(float) * lo.size()));
+    CK(cudaMemcpy(a.a_hi.p, hi.data(), sizeof(float) * hi.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(a.a_lo.p, lo.data(), sizeof(float) * lo.size(), cudaMemcpyHostToDevice));
+    a.umma = umma_tmap_weights(a.tm_hi.bytes, a.a_hi.as<float>(), C, O) &&
+             umma_tmap_weights(a.tm_lo.bytes, a.a_lo.as<float>(), C, O);
+  }
   return FG_OK;
+}
+
+GemmArgs affine_gemm(const DevAffine& a, const float* in, long long in_cr, float* out, long long out_cr,
+                     const float* res, long long res_cr, long long nrows, int D);
+
+bool umma_enabled() {
+  const char* e = std::getenv("FG_NO_UMMA");
+  return !(e && e[0] == '1');
+}
+
+// Λ bound GEMM of one affine over `rows` token rows: tcgen05 3xTF32 when the shape and
+// the input tensor map allow it, the FP32 SIMT kernel otherwise.
+int launch_affine_lambda(const DevAffine& a, const TensorMap* tm_in, const float* in, long long in_cr,
+                         float* out, long long out_cr, const float* res, long long res_cr, long long rows,
+                         int D, cudaStream_t st) {
+  if (a.umma && tm_in && umma_enabled() && umma_supported(a.O, D, a.C)) {
+    return launch_affine_umma(a.tm_hi.bytes, a.tm_lo.bytes, tm_in->bytes, out, (long long)a.O * D, out_cr, res,
+                              (long long)a.O * D, res_cr, a.O, D, a.C, rows, 1.0f, st);
+  }
+  return launch_gemm(affine_gemm(a, in, in_cr, out, out_cr, res, res_cr, rows, D), st);
 }
 
 // Λ GEMM of propagate_affine for `rows` token rows per sentence:
@@ -546,6 +604,8 @@ struct DevLayer {
 struct Workspace {
   int S = 0, D = 0, W = 0, Ntot = 0;  // slots, pert dim, words, sentences uploaded
   DBuf X, R1, QF, SC, CTX;            // Λ planes (f32)
+  TensorMap tm_X, tm_R1, tm_CTX, tm_F;  // tcgen05 input maps of the four affine inputs
+  bool tm_ok = false;
   long long crX = 0, crQKV = 0, crF = 0, crSC = 0;
   DBuf X_b, R1_b, QKV_b, SC_b, CTX_b, F_b;  // f64 lb/ub(/lo/hi) blocks
   DBuf pooled, pooled_b, coef;
@@ -647,6 +707,11 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot) {
   w.D = D;
   w.W = W;
   w.Ntot = Ntot;
+  const long long rows = (long long)S * L;
+  w.tm_ok = umma_tmap_lambda(w.tm_X.bytes, w.X.as<float>(), w.crX, D, (int)E, rows) &&
+            umma_tmap_lambda(w.tm_R1.bytes, w.R1.as<float>(), w.crX, D, (int)E, rows) &&
+            umma_tmap_lambda(w.tm_CTX.bytes, w.CTX.as<float>(), w.crX, D, (int)E, rows) &&
+            umma_tmap_lambda(w.tm_F.bytes, w.QF.as<float>(), w.crF, D, (int)F, rows);
   return FG_OK;
 }
 
@@ -719,7 +784,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     const size_t base = (size_t)l * per_layer;
     // Q, K, V = propagate_affine(cur, Wq|Wk|Wv)   (one N=3E affine)
     g_tag = "affine_gemm";
-    LAUNCH(launch_gemm(affine_gemm(lw.qkv, X, w.crX, QKV, w.crQKV, nullptr, 0, (long long)S * L, D), st));
+    LAUNCH(launch_affine_lambda(lw.qkv, w.tm_ok ? &w.tm_X : nullptr, X, w.crX, QKV, w.crQKV, nullptr, 0,
+                                (long long)S * L, D, st));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(X_lb, X_ub, lw.qkv.w64.as<double>(), lw.qkv.b64.as<double>(), nullptr,
                               nullptr, Q_lb, Q_ub, S, L, E, 3 * E, st));
@@ -761,7 +827,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     }
     // res1 = cur + affine(ctx, Wo)
     g_tag = "affine_gemm";
-    LAUNCH(launch_gemm(affine_gemm(lw.wo, CTX, w.crX, R1, w.crX, X, w.crX, (long long)S * L, D), st));
+    LAUNCH(launch_affine_lambda(lw.wo, w.tm_ok ? &w.tm_CTX : nullptr, CTX, w.crX, R1, w.crX, X, w.crX,
+                                (long long)S * L, D, st));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(CTX_lb, CTX_ub, lw.wo.w64.as<double>(), lw.wo.b64.as<double>(), X_lb, X_ub,
                               R1_lb, R1_ub, S, L, E, E, st));
@@ -771,7 +838,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     }
     // f1 = affine(res1, W1); act = ReluVerify/TanhVerify/SiluVerify(f1)
     g_tag = "affine_gemm";
-    LAUNCH(launch_gemm(affine_gemm(lw.w1, R1, w.crX, Fl, w.crF, nullptr, 0, (long long)S * L, D), st));
+    LAUNCH(launch_affine_lambda(lw.w1, w.tm_ok ? &w.tm_R1 : nullptr, R1, w.crX, Fl, w.crF, nullptr, 0,
+                                (long long)S * L, D, st));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(R1_lb, R1_ub, lw.w1.w64.as<double>(), lw.w1.b64.as<double>(), nullptr,
                               nullptr, F_lb, F_ub, S, L, E, F, st));
@@ -787,7 +855,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     }
     // cur = res1 + affine(act, W2)
     g_tag = "affine_gemm";
-    LAUNCH(launch_gemm(affine_gemm(lw.w2, Fl, w.crF, X, w.crX, R1, w.crX, (long long)S * L, D), st));
+    LAUNCH(launch_affine_lambda(lw.w2, w.tm_ok ? &w.tm_F : nullptr, Fl, w.crF, X, w.crX, R1, w.crX,
+                                (long long)S * L, D, st));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(F_lb, F_ub, lw.w2.w64.as<double>(), lw.w2.b64.as<double>(), R1_lb, R1_ub,
                               X_lb, X_ub, S, L, F, E, st));
@@ -1359,6 +1428,81 @@ fg_status fg_profile_pass(fg_model* m, int norm, double eps, int max_sites, char
     }
   }
   *nsites = n;
+  return FG_OK;
+}
+
+// Self-test of the affine bound GEMM paths on random data: both planes of
+// Y = A X over `rows` token rows (A = W^T / |W|^T) by the tcgen05 3xTF32 kernel and
+// by the FP32 SIMT kernel, each compared with an f64 device reference.
+// err_* = max |Y - Y_ref| / max |Y_ref|; err_umma = -1 when the shape is not
+// eligible for tcgen05.
+fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_t seed, double* err_umma,
+                             double* err_simt, double* ms_umma, double* ms_simt) {
+  cudaSetDevice(ctx->device);
+  std::mt19937_64 rng(seed);
+  auto uni = [&](double lo, double hi) { return lo + (hi - lo) * ((rng() >> 11) * 0x1.0p-53); };
+  std::vector<double> w((size_t)C * O);
+  for (double& v : w) v = (double)(float)uni(-0.5 / std::sqrt((double)C), 0.5 / std::sqrt((double)C));
+  DevAffine a;
+  fg_status s = upload_affine(ctx, a, C, O, w, nullptr);
+  if (s) return s;
+  const long long nin = (long long)rows * C * D, nout = (long long)rows * O * D;
+  std::vector<float> x(2 * nin);
+  for (auto& v : x) v = (float)uni(-1.0, 1.0);
+  DBuf X, Y1, Y2, Yref;
+  CK(X.alloc(sizeof(float) * 2 * nin));
+  CK(Y1.alloc(sizeof(float) * 2 * nout));
+  CK(Y2.alloc(sizeof(float) * 2 * nout));
+  CK(Yref.alloc(sizeof(double) * 2 * nout));
+  CK(cudaMemcpy(X.p, x.data(), sizeof(float) * x.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemset(Y1.p, 0, sizeof(float) * 2 * nout));
+  CK(cudaMemset(Y2.p, 0, sizeof(float) * 2 * nout));
+  TensorMap tm;
+  bool have_tm = umma_tmap_lambda(tm.bytes, X.as<float>(), nin, D, C, rows);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float t = 0.f;
+  CK(cudaEventRecord(e0, ctx->stream));
+  LAUNCH(launch_gemm(affine_gemm(a, X.as<float>(), nin, Y1.as<float>(), nout, nullptr, 0, rows, D), ctx->stream));
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  cudaEventElapsedTime(&t, e0, e1);
+  *ms_simt = t;
+  *ms_umma = -1.0;
+  bool umma = a.umma && have_tm && umma_supported(O, D, C);
+  if (umma) {
+    CK(cudaEventRecord(e0, ctx->stream));
+    LAUNCH(launch_affine_umma(a.tm_hi.bytes, a.tm_lo.bytes, tm.bytes, Y2.as<float>(), (long long)O * D, nout,
+                              nullptr, 0, 0, O, D, C, rows, 1.0f, ctx->stream));
+    CK(cudaEventRecord(e1, ctx->stream));
+    CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&t, e0, e1);
+    *ms_umma = t;
+  }
+  LAUNCH(launch_ref_affine_f64(a.w32.as<float>(), X.as<float>(), nin, Yref.as<double>(), C, O, D, rows,
+                               ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  std::vector<float> y1(2 * nout), y2(2 * nout);
+  std::vector<double> yr(2 * nout);
+  CK(cudaMemcpy(y1.data(), Y1.p, sizeof(float) * y1.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(y2.data(), Y2.p, sizeof(float) * y2.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(yr.data(), Yref.p, sizeof(double) * yr.size(), cudaMemcpyDeviceToHost));
+  // reference kernel output order is (row, plane, j, d); kernels write plane-major (plane, row, j, d)
+  double mx = 0.0, e1s = 0.0, e2s = 0.0;
+  for (long long r = 0; r < rows; ++r)
+    for (int plane = 0; plane < 2; ++plane)
+      for (long long jd = 0; jd < (long long)O * D; ++jd) {
+        double ref = yr[(r * 2 + plane) * (long long)O * D + jd];
+        long long k = plane * nout + r * (long long)O * D + jd;
+        mx = std::max(mx, std::fabs(ref));
+        e1s = std::max(e1s, std::fabs((double)y1[k] - ref));
+        e2s = std::max(e2s, std::fabs((double)y2[k] - ref));
+      }
+  *err_simt = e1s / std::max(mx, 1e-300);
+  *err_umma = umma ? e2s / std::max(mx, 1e-300) : -1.0;
   return FG_OK;
 }
 

@@ -131,4 +131,17 @@ int launch_scale(const float* x, long long xcr, const double* xlb, const double*
                  cudaStream_t st);
 int launch_fill_int(int* p, int v, long long n, cudaStream_t st);
 
+// ---- tcgen05 3xTF32 affine GEMM (fg_umma.cu) ----------------------------------------
+// Tensor maps are opaque 128-byte CUtensorMap objects (64-byte aligned storage).
+bool umma_supported(int M, int N, int K);
+// weights: [2][O][C] f32 (plane 0 = W^T, plane 1 = |W|^T), K-major
+bool umma_tmap_weights(void* tm, const float* a, int C, int O);
+// Λ input: two planes (c at lam, r at lam + cr) of [rows][C][D]
+bool umma_tmap_lambda(void* tm, const float* lam, long long cr, int D, int C, long long rows);
+int launch_affine_umma(const void* tm_ahi, const void* tm_alo, const void* tm_b, float* C, long long c_sr,
+                       long long c_plane, const float* R, long long r_sr, long long r_plane, int M, int N, int K,
+                       long long rows, float alpha, cudaStream_t st);
+int launch_ref_affine_f64(const float* W, const float* X, long long x_cr, double* Y, int C, int O, int D,
+                          long long rows, cudaStream_t st);
+
 }  // namespace fg

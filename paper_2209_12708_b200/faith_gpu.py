@@ -135,6 +135,7 @@ def load_library():
     L.fg_gen_input.argtypes = [C.POINTER(FgConfig), C.c_uint64, _dp]
     L.fg_gen_positions.argtypes = [C.c_uint64, C.c_int, C.c_int, _ip]
     L.fg_profile_pass.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_char_p, _dp, _ip, _ip]
+    L.fg_selftest_affine.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _dp, _dp, _dp, _dp]
     _lib = L
     return L
 
@@ -186,6 +187,14 @@ class Context:
         if st != FG_OK:
             msg = self.lib.fg_last_error(self.handle).decode()
             raise _EXC.get(st, FaithGPUError)(f"{what}: {msg}")
+
+    def selftest_affine(self, rows: int, c: int, o: int, d: int, seed: int = 1) -> dict:
+        """tcgen05 3xTF32 and FP32 SIMT affine GEMMs vs an f64 reference (fg_selftest_affine)."""
+        out = [np.zeros(1) for _ in range(4)]
+        self._check(self.lib.fg_selftest_affine(self.handle, rows, c, o, d, seed, *map(_d, out)),
+                    "fg_selftest_affine")
+        return {"err_umma": float(out[0][0]), "err_simt": float(out[1][0]), "ms_umma": float(out[2][0]),
+                "ms_simt": float(out[3][0])}
 
     # ---- bounds.hpp ------------------------------------------------------------------
     def concretize(self, b, norm: str, eps: float):
