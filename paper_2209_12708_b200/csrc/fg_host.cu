@@ -246,6 +246,7 @@ struct DevAffine {
   DBuf a_hi, a_lo;        // [2][O][C] f32: (W^T, |W|^T) split for 3xTF32 (tcgen05 path)
   TensorMap tm_hi, tm_lo;
   bool umma = false;
+  int bn = 0;
   int C = 0, O = 0;
 };
 
@@ -269,7 +270,8 @@ fg_status upload_affine(fg_ctx* ctx, DevAffine& a, int C, int O, const std::vect
     CK(cudaMemset(a.b64.p, 0, sizeof(double) * O));
   }
   // tcgen05 operands: transposed (K-major) and split into TF32 hi/lo parts once.
-  if (umma_supported(O, 128, C)) {
+  a.bn = umma_pick_bn(O);
+  if (umma_available() && a.bn > 0 && C % 32 == 0) {
     std::vector<float> hi(2 * (size_t)C * O), lo(2 * (size_t)C * O);
     for (int plane = 0; plane < 2; ++plane)
       for (int j = 0; j < O; ++j)
@@ -284,8 +286,8 @@ fg_status upload_affine(fg_ctx* ctx, DevAffine& a, int C, int O, const std::vect
     CK(a.a_lo.alloc(sizeof(float) * lo.size()));
     CK(cudaMemcpy(a.a_hi.p, hi.data(), sizeof(float) * hi.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(a.a_lo.p, lo.data(), sizeof(float) * lo.size(), cudaMemcpyHostToDevice));
-    a.umma = umma_tmap_weights(a.tm_hi.bytes, a.a_hi.as<float>(), C, O) &&
-             umma_tmap_weights(a.tm_lo.bytes, a.a_lo.as<float>(), C, O);
+    a.umma = umma_tmap_wop(a.tm_hi.bytes, a.a_hi.as<float>(), C, O, 2, 1, a.bn) &&
+             umma_tmap_wop(a.tm_lo.bytes, a.a_lo.as<float>(), C, O, 2, 1, a.bn);
   }
   return FG_OK;
 }
@@ -300,14 +302,39 @@ bool umma_enabled() {
 
 // Λ bound GEMM of one affine over `rows` token rows: tcgen05 3xTF32 when the shape and
 // the input tensor map allow it, the FP32 SIMT kernel otherwise.
+// tcgen05 descriptor of the affine: batch (token row, plane); Λ map (d, C, rows, 2).
+LamGemm affine_lam(const DevAffine& a, float* out, long long out_cr, const float* res, long long res_cr,
+                   long long rows, int D) {
+  LamGemm g{};
+  g.M = D; g.N = a.O; g.K = a.C; g.K0 = a.C;
+  g.nb[0] = (int)rows; g.nb[1] = 2; g.nb[2] = 1; g.nb[3] = 1;
+  g.kdim = 1;
+  g.lam_c[1][0] = 1;  // c2 = token row
+  g.lam_c[2][1] = 1;  // c3 = plane
+  g.w_c[0][1] = 1;    // weights plane: W^T (c) or |W|^T (r)
+  g.out = out;
+  g.out_c[0] = (long long)a.O * D; g.out_c[1] = out_cr; g.ldn_out = D;
+  g.res = res;
+  g.res_c[0] = (long long)a.O * D; g.res_c[1] = res_cr; g.ldn_res = D;
+  g.alpha = 1.0f;
+  return g;
+}
+
 int launch_affine_lambda(const DevAffine& a, const TensorMap* tm_in, const float* in, long long in_cr,
                          float* out, long long out_cr, const float* res, long long res_cr, long long rows,
                          int D, cudaStream_t st) {
-  if (a.umma && tm_in && umma_enabled() && umma_supported(a.O, D, a.C)) {
-    return launch_affine_umma(a.tm_hi.bytes, a.tm_lo.bytes, tm_in->bytes, out, (long long)a.O * D, out_cr, res,
-                              (long long)a.O * D, res_cr, a.O, D, a.C, rows, 1.0f, st);
+  if (a.umma && tm_in && umma_enabled() && D % 128 == 0) {
+    return launch_lam_gemm(tm_in->bytes, a.tm_hi.bytes, a.tm_lo.bytes,
+                           affine_lam(a, out, out_cr, res, res_cr, rows, D), a.bn, st);
   }
   return launch_gemm(affine_gemm(a, in, in_cr, out, out_cr, res, res_cr, rows, D), st);
+}
+
+bool lam_map(TensorMap& tm, const float* base, long long cr, int D, int C, long long rows, int kdim) {
+  unsigned long long dims[4] = {(unsigned long long)D, (unsigned long long)C, (unsigned long long)rows, 2};
+  unsigned long long strides[3] = {(unsigned long long)D * 4, (unsigned long long)C * D * 4,
+                                   (unsigned long long)cr * 4};
+  return umma_tmap_lam(tm.bytes, base, dims, strides, kdim);
 }
 
 // Λ GEMM of propagate_affine for `rows` token rows per sentence:
@@ -606,6 +633,12 @@ struct Workspace {
   DBuf X, R1, QF, SC, CTX;            // Λ planes (f32)
   TensorMap tm_X, tm_R1, tm_CTX, tm_F;  // tcgen05 input maps of the four affine inputs
   bool tm_ok = false;
+  // tcgen05 McCormick dot products: Λ maps of the operands, split coefficient buffers + maps
+  TensorMap tm_QKVk, tm_QKVrow, tm_SC;
+  DBuf cf_sim_x[2], cf_sim_y[2], cf_wv_x[2], cf_wv_y[2];  // [hi, lo]
+  TensorMap tm_sim_x[2], tm_sim_y[2], tm_wv_x[2], tm_wv_y[2];
+  int bn_sim = 0, bn_wvx = 0;
+  bool dots_ok = false;
   long long crX = 0, crQKV = 0, crF = 0, crSC = 0;
   DBuf X_b, R1_b, QKV_b, SC_b, CTX_b, F_b;  // f64 lb/ub(/lo/hi) blocks
   DBuf pooled, pooled_b, coef;
@@ -708,10 +741,32 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot) {
   w.W = W;
   w.Ntot = Ntot;
   const long long rows = (long long)S * L;
-  w.tm_ok = umma_tmap_lambda(w.tm_X.bytes, w.X.as<float>(), w.crX, D, (int)E, rows) &&
-            umma_tmap_lambda(w.tm_R1.bytes, w.R1.as<float>(), w.crX, D, (int)E, rows) &&
-            umma_tmap_lambda(w.tm_CTX.bytes, w.CTX.as<float>(), w.crX, D, (int)E, rows) &&
-            umma_tmap_lambda(w.tm_F.bytes, w.QF.as<float>(), w.crF, D, (int)F, rows);
+  const bool dok = umma_available() && D % 128 == 0;
+  w.tm_ok = dok && lam_map(w.tm_X, w.X.as<float>(), w.crX, D, (int)E, rows, 1) &&
+            lam_map(w.tm_R1, w.R1.as<float>(), w.crX, D, (int)E, rows, 1) &&
+            lam_map(w.tm_CTX, w.CTX.as<float>(), w.crX, D, (int)E, rows, 1) &&
+            lam_map(w.tm_F, w.QF.as<float>(), w.crF, D, (int)F, rows, 1);
+  // McCormick dot products on tcgen05 (shapes: K multiples of 32, N multiples of 32)
+  w.bn_sim = umma_pick_bn((int)L);
+  w.bn_wvx = umma_pick_bn((int)hd);
+  w.dots_ok = false;
+  if (w.tm_ok && w.bn_sim > 0 && w.bn_wvx > 0 && hd % 32 == 0 && L % 32 == 0) {
+    const long long SH = (long long)S * H;
+    bool ok = lam_map(w.tm_QKVk, w.QF.as<float>(), w.crQKV, D, (int)(3 * E), rows, 1) &&
+              lam_map(w.tm_QKVrow, w.QF.as<float>(), w.crQKV, D, (int)(3 * E), rows, 2) &&
+              lam_map(w.tm_SC, w.SC.as<float>(), w.crSC, D, (int)L, SH * L, 1);
+    for (int part = 0; part < 2 && ok; ++part) {
+      CK(w.cf_sim_x[part].alloc(sizeof(float) * SH * 2 * L * 2 * hd));
+      CK(w.cf_sim_y[part].alloc(sizeof(float) * SH * 2 * L * hd));
+      CK(w.cf_wv_x[part].alloc(sizeof(float) * SH * 2 * hd * 2 * L));
+      CK(w.cf_wv_y[part].alloc(sizeof(float) * SH * 2 * L * L));
+      ok = ok && umma_tmap_wop(w.tm_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), (int)(2 * hd), (int)L, 2, (int)SH, w.bn_sim) &&
+           umma_tmap_wop(w.tm_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), (int)hd, (int)L, 2, (int)SH, w.bn_sim) &&
+           umma_tmap_wop(w.tm_wv_x[part].bytes, w.cf_wv_x[part].as<float>(), (int)(2 * L), (int)hd, 2, (int)SH, w.bn_wvx) &&
+           umma_tmap_wop(w.tm_wv_y[part].bytes, w.cf_wv_y[part].as<float>(), (int)L, (int)L, 2, (int)SH, w.bn_sim);
+    }
+    w.dots_ok = ok;
+  }
   return FG_OK;
 }
 
@@ -804,7 +859,43 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     // scores = DotProduct(q, k); scaled = Scale(scores, 1/sqrt(hd))   (model.cpp:410-418)
     const double scale = 1.0 / std::sqrt((double)hd);
     g_tag = "dot_similarity";
-    LAUNCH(launch_dot_similarity(q, k, sc, S, L, H, hd, D, w.coef.as<float>(), (float)scale, st));
+    if (w.dots_ok && umma_enabled()) {
+      LAUNCH(launch_sim_coef_split(q, k, S, H, L, hd, w.cf_sim_x[0].as<float>(), w.cf_sim_x[1].as<float>(),
+                                   w.cf_sim_y[0].as<float>(), w.cf_sim_y[1].as<float>(), st));
+      LAUNCH(launch_sim_bias(q, k, sc, S, H, L, hd, scale, st));
+      // x-side: scores[s,h,i,j,:] = sum_k2 Cx[j,k2] (Qc|Qr)[i, h*hd + k2]   (K0 = hd: c|r concat)
+      LamGemm gx{};
+      gx.M = D; gx.N = L; gx.K = 2 * hd; gx.K0 = hd;
+      gx.nb[0] = S; gx.nb[1] = H; gx.nb[2] = L; gx.nb[3] = 2;
+      gx.kdim = 1;
+      gx.lam_c[0][1] = hd;                    // neuron h*hd (+k)
+      gx.lam_c[1][0] = L; gx.lam_c[1][2] = 1;  // row s*L + i
+      gx.w_c[0][3] = 1;                       // coefficient plane = output plane
+      gx.w_c[1][0] = H; gx.w_c[1][1] = 1;      // (s, h)
+      gx.out = SC;
+      gx.out_c[0] = (long long)H * L * L * D; gx.out_c[1] = (long long)L * L * D; gx.out_c[2] = (long long)L * D;
+      gx.out_c[3] = w.crSC; gx.ldn_out = D;
+      gx.alpha = (float)scale;
+      LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_x[0].bytes, w.tm_sim_x[1].bytes, gx, w.bn_sim, st));
+      // y-side: scores[s,h,i,j,:] += sum_k lx[i,k] K_p[j, E + h*hd + k]   (per plane p)
+      LamGemm gy{};
+      gy.M = D; gy.N = L; gy.K = hd; gy.K0 = hd;
+      gy.nb[0] = S; gy.nb[1] = H; gy.nb[2] = L; gy.nb[3] = 2;
+      gy.kdim = 1;
+      gy.lam_c[0][1] = hd; gy.lam_c[0][4] = E;
+      gy.lam_c[1][0] = L; gy.lam_c[1][2] = 1;
+      gy.lam_c[2][3] = 1;
+      gy.w_c[0][3] = 1;
+      gy.w_c[1][0] = H; gy.w_c[1][1] = 1;
+      gy.out = SC;
+      gy.out_c[0] = (long long)H * L * L * D; gy.out_c[1] = (long long)L * L * D; gy.out_c[2] = D;
+      gy.out_c[3] = w.crSC; gy.ldn_out = (long long)L * D;
+      gy.alpha = (float)scale;
+      gy.accumulate = 1;
+      LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_y[0].bytes, w.tm_sim_y[1].bytes, gy, w.bn_sim, st));
+    } else {
+      LAUNCH(launch_dot_similarity(q, k, sc, S, L, H, hd, D, w.coef.as<float>(), (float)scale, st));
+    }
     if (dump) {
       LAUNCH(launch_concretize(SC, w.crSC, S_lb, S_ub, (long long)H * L * L, nSC, D, norm, eps, dlo, dhi, st));
       if (fg_status s = dump->copy(base + 3ull * L * E + (size_t)H * L * L, dlo, dhi, (size_t)H * L * L)) return s;
@@ -819,7 +910,42 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     // ctx = DotProduct(probs, v)
     NView cx{CTX, w.crX, CTX_lb, CTX_ub, nullptr, nullptr, (long long)L * E, E, 0};
     g_tag = "dot_weighted";
-    LAUNCH(launch_dot_weighted(sc, v, cx, S, L, H, hd, D, w.coef.as<float>(), st));
+    if (w.dots_ok && umma_enabled()) {
+      LAUNCH(launch_wv_coef_split(sc, v, S, H, L, hd, w.cf_wv_x[0].as<float>(), w.cf_wv_x[1].as<float>(),
+                                  w.cf_wv_y[0].as<float>(), w.cf_wv_y[1].as<float>(), st));
+      LAUNCH(launch_wv_bias(sc, v, cx, S, H, L, hd, st));
+      // x-side: ctx[s,i,h*hd+k,:] = sum_j2 Cx[k,j2] (Pc|Pr)[s,h,i,j2]   (K0 = L: c|r concat)
+      LamGemm gx{};
+      gx.M = D; gx.N = hd; gx.K = 2 * L; gx.K0 = L;
+      gx.nb[0] = S; gx.nb[1] = H; gx.nb[2] = L; gx.nb[3] = 2;
+      gx.kdim = 1;
+      gx.lam_c[1][0] = H * L; gx.lam_c[1][1] = L; gx.lam_c[1][2] = 1;  // score row (s, h, i)
+      gx.w_c[0][3] = 1;
+      gx.w_c[1][0] = H; gx.w_c[1][1] = 1;
+      gx.out = CTX;
+      gx.out_c[0] = (long long)L * E * D; gx.out_c[1] = (long long)hd * D; gx.out_c[2] = (long long)E * D;
+      gx.out_c[3] = w.crX; gx.ldn_out = D;
+      gx.alpha = 1.0f;
+      LAUNCH(launch_lam_gemm(w.tm_SC.bytes, w.tm_wv_x[0].bytes, w.tm_wv_x[1].bytes, gx, w.bn_wvx, st));
+      // y-side: ctx[s,i,h*hd+k,:] += sum_j lx[i,j] V_p[j, 2E + h*hd + k]   (K along token rows)
+      LamGemm gy{};
+      gy.M = D; gy.N = L; gy.K = L; gy.K0 = L;
+      gy.nb[0] = S; gy.nb[1] = H; gy.nb[2] = hd; gy.nb[3] = 2;
+      gy.kdim = 2;
+      gy.lam_c[0][1] = hd; gy.lam_c[0][2] = 1; gy.lam_c[0][4] = 2 * E;  // neuron 2E + h*hd + k
+      gy.lam_c[1][0] = L;                                               // row s*L (+ j)
+      gy.lam_c[2][3] = 1;
+      gy.w_c[0][3] = 1;
+      gy.w_c[1][0] = H; gy.w_c[1][1] = 1;
+      gy.out = CTX;
+      gy.out_c[0] = (long long)L * E * D; gy.out_c[1] = (long long)hd * D; gy.out_c[2] = D;
+      gy.out_c[3] = w.crX; gy.ldn_out = (long long)E * D;
+      gy.alpha = 1.0f;
+      gy.accumulate = 1;
+      LAUNCH(launch_lam_gemm(w.tm_QKVrow.bytes, w.tm_wv_y[0].bytes, w.tm_wv_y[1].bytes, gy, w.bn_sim, st));
+    } else {
+      LAUNCH(launch_dot_weighted(sc, v, cx, S, L, H, hd, D, w.coef.as<float>(), st));
+    }
     const size_t off_ctx = 3ull * L * E + 4ull * H * L * L + 2ull * H * L;
     if (dump) {
       LAUNCH(launch_concretize(CTX, w.crX, CTX_lb, CTX_ub, (long long)L * E, nX, D, norm, eps, CTX_lo, CTX_hi, st));
@@ -1458,7 +1584,7 @@ fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_
   CK(cudaMemset(Y1.p, 0, sizeof(float) * 2 * nout));
   CK(cudaMemset(Y2.p, 0, sizeof(float) * 2 * nout));
   TensorMap tm;
-  bool have_tm = umma_tmap_lambda(tm.bytes, X.as<float>(), nin, D, C, rows);
+  bool have_tm = D % 128 == 0 && lam_map(tm, X.as<float>(), nin, D, C, rows, 1);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -1470,11 +1596,11 @@ fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_
   cudaEventElapsedTime(&t, e0, e1);
   *ms_simt = t;
   *ms_umma = -1.0;
-  bool umma = a.umma && have_tm && umma_supported(O, D, C);
+  bool umma = a.umma && have_tm;
   if (umma) {
     CK(cudaEventRecord(e0, ctx->stream));
-    LAUNCH(launch_affine_umma(a.tm_hi.bytes, a.tm_lo.bytes, tm.bytes, Y2.as<float>(), (long long)O * D, nout,
-                              nullptr, 0, 0, O, D, C, rows, 1.0f, ctx->stream));
+    LAUNCH(launch_lam_gemm(tm.bytes, a.tm_hi.bytes, a.tm_lo.bytes, affine_lam(a, Y2.as<float>(), nout, nullptr, 0, rows, D),
+                           a.bn, ctx->stream));
     CK(cudaEventRecord(e1, ctx->stream));
     CK(cudaEventSynchronize(e1));
     cudaEventElapsedTime(&t, e0, e1);

@@ -131,17 +131,52 @@ int launch_scale(const float* x, long long xcr, const double* xlb, const double*
                  cudaStream_t st);
 int launch_fill_int(int* p, int v, long long n, cudaStream_t st);
 
-// ---- tcgen05 3xTF32 affine GEMM (fg_umma.cu) ----------------------------------------
+// ---- tcgen05 3xTF32 engine for Λ contractions (fg_umma.cu) ---------------------------
+// Out_b[n, d] (+)= alpha * sum_k Wop_b[n, k] * Λ_b[k, d] (+ R_b[n, d]), computed as
+// C^T[d, n] tiles with M = 128 d-rows, N = BN output neurons, K in steps of 32.
+//   Λ: 4-D tensor map (d, c1, c2, c3) over a Λ buffer (c3 = plane); the K index runs along
+//      coordinate `kdim` (1 or 2); for k >= K0 it continues in plane c3 + 1 at k - K0 (the
+//      c/r concatenation of the McCormick x-side terms).
+//   Wop: two 4-D tensor maps (k, n, c2, c3) over the TF32 hi / lo parts, K-major.
+//   Batch b = ((b0*nb1 + b1)*nb2 + b2)*nb3 + b3; every coordinate / offset is
+//   co[0]*b0 + co[1]*b1 + co[2]*b2 + co[3]*b3 + co[4].
 // Tensor maps are opaque 128-byte CUtensorMap objects (64-byte aligned storage).
-bool umma_supported(int M, int N, int K);
-// weights: [2][O][C] f32 (plane 0 = W^T, plane 1 = |W|^T), K-major
-bool umma_tmap_weights(void* tm, const float* a, int C, int O);
-// Λ input: two planes (c at lam, r at lam + cr) of [rows][C][D]
-bool umma_tmap_lambda(void* tm, const float* lam, long long cr, int D, int C, long long rows);
-int launch_affine_umma(const void* tm_ahi, const void* tm_alo, const void* tm_b, float* C, long long c_sr,
-                       long long c_plane, const float* R, long long r_sr, long long r_plane, int M, int N, int K,
-                       long long rows, float alpha, cudaStream_t st);
+struct LamGemm {
+  int M, N, K, K0;
+  int nb[4];
+  int kdim;
+  int lam_c[3][5];
+  int w_c[2][5];
+  long long out_c[5], res_c[5];
+  long long ldn_out, ldn_res;
+  float* out;
+  const float* res;
+  float alpha;
+  int accumulate;
+  int tiles_m, tiles_n, num_tiles;  // set by launch_lam_gemm
+};
+bool umma_available();
+int umma_pick_bn(int N);  // 256 / 128 / 64, or 0 when N is not a multiple of 64
+bool umma_tmap_lam(void* tm, const float* base, const unsigned long long dims[4],
+                   const unsigned long long strides_bytes[3], int kdim);
+bool umma_tmap_wop(void* tm, const float* base, int K, int N, int P2, int P3, int bn);
+int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, LamGemm p, int bn,
+                    cudaStream_t st);
 int launch_ref_affine_f64(const float* W, const float* X, long long x_cr, double* Y, int C, int O, int D,
                           long long rows, cudaStream_t st);
+
+// McCormick coefficient matrices split into TF32 hi/lo, K-major, per (sentence, head):
+//   sim_x [S*H][2][L][2hd]   x-side of Q.K^T (rows j, K = (c | r) of the Q slice)
+//   sim_y [S*H][2][L][hd]    y-side (lx, |lx| of Q rows i)
+//   wv_x  [S*H][2][hd][2L]   x-side of P.V (rows k, K = (c | r) of the P rows)
+//   wv_y  [S*H][2][L][L]     y-side (lx, |lx| of P, rows i, K = j)
+int launch_sim_coef_split(const NView& q, const NView& k, int S, int H, int L, int hd, float* x_hi,
+                          float* x_lo, float* y_hi, float* y_lo, cudaStream_t st);
+int launch_wv_coef_split(const NView& p, const NView& v, int S, int H, int L, int hd, float* x_hi,
+                         float* x_lo, float* y_hi, float* y_lo, cudaStream_t st);
+int launch_sim_bias(const NView& q, const NView& k, const NView& out, int S, int H, int L, int hd,
+                    double scale, cudaStream_t st);
+int launch_wv_bias(const NView& p, const NView& v, const NView& out, int S, int H, int L, int hd,
+                   cudaStream_t st);
 
 }  // namespace fg

@@ -960,6 +960,59 @@ __global__ void fill_int_kernel(int* p, int v, long long n) {
   if (i < n) p[i] = v;
 }
 
+// TF32 split of a coefficient: hi = rna_tf32(v), lo = v - hi (exact).
+__device__ __forceinline__ void split_store(float* hi, float* lo, long long i, double v) {
+  float f = (float)v;
+  uint32_t hb;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(f));
+  float h = __uint_as_float(hb);
+  hi[i] = h;
+  lo[i] = f - h;
+}
+
+// McCormick coefficients of Q.K^T for the tcgen05 engine (K-major, see fg_internal.cuh).
+__global__ void sim_coef_split_kernel(NView q, NView k, int H, int L, int hd, float* xh, float* xl,
+                                      float* yh, float* yl) {
+  const int sh = blockIdx.x;
+  const int s = sh / H, h = sh % H;
+  for (int t = threadIdx.x; t < L * hd; t += blockDim.x) {
+    const int j = t / hd, kk = t % hd;
+    const long long yi = nidx(k, s, j, h * hd + kk);
+    const double ly = k.lo[yi], uy = k.hi[yi];
+    const long long x0 = ((long long)(sh * 2 + 0) * L + j) * 2 * hd, x1 = ((long long)(sh * 2 + 1) * L + j) * 2 * hd;
+    split_store(xh, xl, x0 + kk, 0.5 * (ly + uy));
+    split_store(xh, xl, x0 + hd + kk, 0.5 * (fabs(uy) - fabs(ly)));
+    split_store(xh, xl, x1 + kk, 0.5 * (uy - ly));
+    split_store(xh, xl, x1 + hd + kk, 0.5 * (fabs(uy) + fabs(ly)));
+    const double lx = q.lo[nidx(q, s, j, h * hd + kk)];  // row i = j of Q
+    split_store(yh, yl, ((long long)(sh * 2 + 0) * L + j) * hd + kk, lx);
+    split_store(yh, yl, ((long long)(sh * 2 + 1) * L + j) * hd + kk, fabs(lx));
+  }
+}
+
+// McCormick coefficients of P.V for the tcgen05 engine.
+__global__ void wv_coef_split_kernel(NView p, NView v, int H, int L, int hd, float* xh, float* xl, float* yh,
+                                     float* yl) {
+  const int sh = blockIdx.x;
+  const int s = sh / H, h = sh % H;
+  for (int t = threadIdx.x; t < hd * L; t += blockDim.x) {
+    const int kk = t / L, j = t % L;
+    const long long yi = nidx(v, s, j, h * hd + kk);
+    const double ly = v.lo[yi], uy = v.hi[yi];
+    const long long x0 = ((long long)(sh * 2 + 0) * hd + kk) * 2 * L, x1 = ((long long)(sh * 2 + 1) * hd + kk) * 2 * L;
+    split_store(xh, xl, x0 + j, 0.5 * (ly + uy));
+    split_store(xh, xl, x0 + L + j, 0.5 * (fabs(uy) - fabs(ly)));
+    split_store(xh, xl, x1 + j, 0.5 * (uy - ly));
+    split_store(xh, xl, x1 + L + j, 0.5 * (fabs(uy) + fabs(ly)));
+  }
+  for (int t = threadIdx.x; t < L * L; t += blockDim.x) {
+    const int i = t / L, j = t % L;
+    const double lx = p.lo[nidx(p, s, (long long)h * L + i, j)];
+    split_store(yh, yl, ((long long)(sh * 2 + 0) * L + i) * L + j, lx);
+    split_store(yh, yl, ((long long)(sh * 2 + 1) * L + i) * L + j, fabs(lx));
+  }
+}
+
 inline unsigned blocks_for(long long n, int per_block) {
   return (unsigned)((n + per_block - 1) / per_block);
 }
@@ -1193,6 +1246,32 @@ int launch_scale(const float* x, long long xcr, const double* xlb, const double*
   long long total = n * (long long)(D > 0 ? D : 1);
   if (total < n) total = n;
   scale_kernel<<<blocks_for(total, 256), 256, 0, st>>>(x, xcr, xlb, xub, s, y, ycr, ylb, yub, n, D);
+  return 1;
+}
+
+int launch_sim_coef_split(const NView& q, const NView& k, int S, int H, int L, int hd, float* x_hi,
+                          float* x_lo, float* y_hi, float* y_lo, cudaStream_t st) {
+  sim_coef_split_kernel<<<S * H, 256, 0, st>>>(q, k, H, L, hd, x_hi, x_lo, y_hi, y_lo);
+  return 1;
+}
+
+int launch_wv_coef_split(const NView& p, const NView& v, int S, int H, int L, int hd, float* x_hi,
+                         float* x_lo, float* y_hi, float* y_lo, cudaStream_t st) {
+  wv_coef_split_kernel<<<S * H, 256, 0, st>>>(p, v, H, L, hd, x_hi, x_lo, y_hi, y_lo);
+  return 1;
+}
+
+int launch_sim_bias(const NView& q, const NView& k, const NView& out, int S, int H, int L, int hd,
+                    double scale, cudaStream_t st) {
+  long long total = (long long)S * H * L * L;
+  sim_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(q, k, out, S, H, L, hd, scale);
+  return 1;
+}
+
+int launch_wv_bias(const NView& p, const NView& v, const NView& out, int S, int H, int L, int hd,
+                   cudaStream_t st) {
+  long long total = (long long)S * L * H * hd;
+  wv_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(p, v, out, S, H, L, hd);
   return 1;
 }
 

@@ -1,21 +1,28 @@
-// fg_umma.cu -- tcgen05 (UMMA) bound GEMM of propagate_affine for sm_100a.
+// fg_umma.cu -- tcgen05 (UMMA) engine for the Λ contractions of the bound pass (sm_100a).
 //
-// Per (sentence s, token row r, plane p) the affine bound in center/radius form is
-//   Y_p[j, d] = sum_i A_p[j, i] X_p[i, d],   A_c = W^T, A_r = |W|^T      (relax.cpp:237-307)
-// i.e. a batched GEMM with M = O (output neurons), N = D (perturbation columns), K = C.
+// Every Λ contraction of the pass has the form (per batch b, both Λ planes c / r)
+//     Out_b[n, d] (+)= alpha * sum_k  Wop_b[n, k] * Λ_b[k, d]                (+ R_b[n, d])
+// with Λ stored [neuron][d] (d contiguous):
+//   * propagate_affine (relax.cpp:237-307):   Wop = W^T or |W|^T,  k = input neuron
+//   * McCormick x-side / y-side terms of propagate_dot_product (relax.cpp:533-654):
+//     Wop = per-(sentence, head) coefficient matrices built from the concretized operands.
+// The engine computes the transposed tile C^T[d, n] = sum_k Λ^T[d, k] Wop^T[k, n]:
+//   M = 128 perturbation columns d (TMEM lanes), N = BN output neurons, K loop of 32.
+// So the epilogue writes are coalesced along d and N can be as wide as 256.
 //
-// FP32-class accuracy on the TF32 tensor pipe by error-compensated 3xTF32:
-//   A = A_hi + A_lo (split once at model upload), X = X_hi + X_lo (split per tile in SMEM),
-//   Y = A_hi X_hi + A_hi X_lo + A_lo X_hi   (the dropped A_lo X_lo term is < 2^-22 |A||X|).
+// FP32-class accuracy on the TF32 pipe by error-compensated 3xTF32:
+//   Wop = W_hi + W_lo (split when built), Λ = L_hi + L_lo (split per tile in SMEM),
+//   C = L_hi W_hi + L_lo W_hi + L_hi W_lo   (dropped L_lo W_lo < 2^-22 |L||W|).
 //
-// Kernel structure (persistent, one CTA per SM, 384 threads):
-//   warp 0      TMA producer: A_hi, A_lo (K-major, SWIZZLE_128B) and the X tile
-//               (MN-major, SWIZZLE_128B: BN/32 boxes of 32 columns x 32 rows) per stage
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32, M=128)
-//   warps 4-7   split warps: X tile -> X_hi (in place) + X_lo, fence.proxy.async
-//   warps 8-11  epilogue: tcgen05.ld TMEM -> registers, (+ residual), st.global
-// Pipelines: smem stages full/split/empty, TMEM accumulators double-buffered
-// (tmem_full/tmem_empty) so a tile's epilogue overlaps the next tile's mainloop.
+// Persistent, warp-specialized kernel (one CTA per SM, 384 threads):
+//   warp 0     TMA producer: W_hi, W_lo tiles [BN][32] (K-major SWIZZLE_128B) and the raw
+//              Λ tile [32][128] (no swizzle) per stage
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32, M=128, N=BN)
+//   warps 4-7  split warps: raw Λ [k][d] -> L_hi, L_lo [d][k] K-major SWIZZLE_128B
+//              (transposed: kind::tf32 with an MN-major operand returned zeros on B200,
+//              profiles/r1_umma_major_probe.txt)
+//   warps 8-11 epilogue: tcgen05.ld TMEM -> registers -> coalesced st.global (+acc/+residual)
+// Pipelines: SMEM stages full/split/empty mbarriers; TMEM accumulators double-buffered.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -28,8 +35,8 @@ namespace fg {
 
 namespace {
 
-constexpr int kBM = 128;
-constexpr int kBK = 32;  // 32 fp32 = 128 B rows: one SWIZZLE_128B atom width
+constexpr int kBM = 128;  // d rows per tile (TMEM lanes)
+constexpr int kBK = 32;   // 32 fp32 = 128 B rows: one SWIZZLE_128B atom width
 constexpr int kThreads = 384;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -56,14 +63,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
-          "r"(smem_u32(dst)),
-      "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1,
                                             int c2, int c3) {
   asm volatile(
@@ -73,12 +72,13 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, ui
       : "memory");
 }
 
-// SMEM matrix descriptor, SWIZZLE_128B (layout type 2), Blackwell version bit 46.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// SMEM matrix descriptor, K-major SWIZZLE_128B: LBO 16 B (unused), SBO 1024 B (8-row groups),
+// Blackwell version bit 46, layout type 2.
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
@@ -113,36 +113,31 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-struct UmmaParams {
-  float* C;
-  long long ldc, c_sr, c_plane;
-  const float* R;
-  long long ldr, r_sr, r_plane;
-  int M, N, K;
-  int tiles_m, tiles_n, num_tiles;
-  float alpha;
-};
-
-// Stage = { A_hi, A_lo (K-major SW128, TMA) | X raw [BK][BN] (TMA, no swizzle) |
-//           X_hi, X_lo (K-major SW128: row n = 32 k values, written by the split warps) }.
-// The tensor core reads both operands K-major: with kind::tf32 an MN-major B operand
-// returned zeros on B200 (probe in DESIGN.md), so the split transposes the Λ tile.
 template <int BN, int STAGES>
 struct SmemLayout {
-  static constexpr int kA = kBM * kBK * 4;  // 16 KB per A tile (hi or lo)
-  static constexpr int kB = kBK * BN * 4;   // X tile (raw, hi or lo)
-  static constexpr int kRaw = 2 * kA;       // offset of the raw X tile in a stage
-  static constexpr int kHi = 2 * kA + kB;   // X_hi
-  static constexpr int kLo = 2 * kA + 2 * kB;
-  static constexpr int kStage = 2 * kA + 3 * kB;
+  static constexpr int kW = BN * kBK * 4;    // W tile (hi or lo), K-major
+  static constexpr int kL = kBK * kBM * 4;   // Λ tile (raw, hi or lo): 16 KB
+  static constexpr int kWlo = kW;
+  static constexpr int kRaw = 2 * kW;
+  static constexpr int kHi = 2 * kW + kL;
+  static constexpr int kLo = 2 * kW + 2 * kL;
+  static constexpr int kStage = 2 * kW + 3 * kL;
   static constexpr int kBarOff = STAGES * kStage;
   static constexpr int kBytes = kBarOff + 256 + 1024;  // + barriers/tmem slot + alignment slack
+  static_assert(kBytes <= 227 * 1024, "stage ring exceeds shared memory");
 };
+
+__device__ __forceinline__ int lin5(const int* co, const int* b) {
+  return co[0] * b[0] + co[1] * b[1] + co[2] * b[2] + co[3] * b[3] + co[4];
+}
+__device__ __forceinline__ long long lin5l(const long long* co, const int* b) {
+  return co[0] * b[0] + co[1] * b[1] + co[2] * b[2] + co[3] * b[3] + co[4];
+}
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
-    affine_umma_kernel(const __grid_constant__ CUtensorMap tm_ahi, const __grid_constant__ CUtensorMap tm_alo,
-                       const __grid_constant__ CUtensorMap tm_b, const UmmaParams p) {
+    lam_gemm_kernel(const __grid_constant__ CUtensorMap tm_lam, const __grid_constant__ CUtensorMap tm_whi,
+                    const __grid_constant__ CUtensorMap tm_wlo, const LamGemm p) {
   using SL = SmemLayout<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -167,13 +162,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[a], 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_ahi) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_alo) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_b) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_lam) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_whi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_wlo) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
+                 "r"(2 * BN < 32 ? 32 : 2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -181,13 +176,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto tile_coords = [&](int t, int& sr, int& plane, int& m0, int& n0) {
-    int mt = t % p.tiles_m;
-    int rest = t / p.tiles_m;
-    int nt = rest % p.tiles_n;
-    int batch = rest / p.tiles_n;
-    sr = batch >> 1;
-    plane = batch & 1;
+  // tile t -> (batch b0..b3, m-tile over d, n-tile over output neurons); n fastest so that
+  // CTAs running concurrently share the (HBM-resident) Λ tiles through L2.
+  auto decode = [&](int t, int* b, int& m0, int& n0) {
+    int nt = t % p.tiles_n;
+    int rest = t / p.tiles_n;
+    int mt = rest % p.tiles_m;
+    int batch = rest / p.tiles_m;
+    b[3] = batch % p.nb[3];
+    batch /= p.nb[3];
+    b[2] = batch % p.nb[2];
+    batch /= p.nb[2];
+    b[1] = batch % p.nb[1];
+    b[0] = batch / p.nb[1];
     m0 = mt * kBM;
     n0 = nt * BN;
   };
@@ -197,25 +198,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int g = 0;
       for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        int sr, plane, m0, n0;
-        tile_coords(t, sr, plane, m0, n0);
+        int b[4], m0, n0;
+        decode(t, b, m0, n0);
+        const int lc1 = lin5(p.lam_c[0], b), lc2 = lin5(p.lam_c[1], b), lc3 = lin5(p.lam_c[2], b);
+        const int wc2 = lin5(p.w_c[0], b), wc3 = lin5(p.w_c[1], b);
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = g % STAGES;
           const uint32_t ph = (g / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * SL::kStage;
-          mbar_expect_tx(&full[s], 2 * SL::kA + SL::kB);
-          tma_load_3d(st, &tm_ahi, &full[s], kb * kBK, m0, plane);
-          tma_load_3d(st + SL::kA, &tm_alo, &full[s], kb * kBK, m0, plane);
-          tma_load_4d(st + SL::kRaw, &tm_b, &full[s], n0, kb * kBK, sr, plane);
+          mbar_expect_tx(&full[s], 2 * SL::kW + SL::kL);
+          const int kw = kb * kBK;
+          tma_load_4d(st, &tm_whi, &full[s], kw, n0, wc2, wc3);
+          tma_load_4d(st + SL::kWlo, &tm_wlo, &full[s], kw, n0, wc2, wc3);
+          int kl = kw, plane = 0;
+          if (kl >= p.K0) {  // c/r concatenation along K: second half reads the r plane
+            kl -= p.K0;
+            plane = 1;
+          }
+          tma_load_4d(st + SL::kRaw, &tm_lam, &full[s], m0, lc1 + (p.kdim == 1 ? kl : 0),
+                      lc2 + (p.kdim == 2 ? kl : 0), lc3 + plane);
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    // instruction descriptor: D f32, A/B tf32, both K-major, N=BN, M=128
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+    // D f32, A/B tf32, both K-major, N = BN, M = 128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(kBM >> 4) << 24);
     int g = 0, it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
       const int acc = it & 1;
@@ -230,19 +240,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (lane == 0) {
           uint8_t* st = smem + s * SL::kStage;
-          const uint32_t a_hi = smem_u32(st), a_lo = smem_u32(st + SL::kA);
-          const uint32_t b_hi = smem_u32(st + SL::kHi), b_lo = smem_u32(st + SL::kLo);
+          const uint32_t w_hi = smem_u32(st), w_lo = smem_u32(st + SL::kWlo);
+          const uint32_t l_hi = smem_u32(st + SL::kHi), l_lo = smem_u32(st + SL::kLo);
 #pragma unroll
-          for (int ks = 0; ks < kBK / 8; ++ks) {
-            // K-major SW128 operands (rows of 128 B, 8-row groups 1024 B apart): +32 B per 8 tf32 of K
-            const uint64_t ahi = sw128_desc(a_hi + ks * 32, 16, 1024);
-            const uint64_t alo = sw128_desc(a_lo + ks * 32, 16, 1024);
-            const uint64_t bhi = sw128_desc(b_hi + ks * 32, 16, 1024);
-            const uint64_t blo = sw128_desc(b_lo + ks * 32, 16, 1024);
-            const uint32_t first = (kb | ks) != 0;
-            umma_tf32(d_tmem, ahi, bhi, idesc, first);
-            umma_tf32(d_tmem, ahi, blo, idesc, 1);
+          for (int ks = 0; ks < kBK / 8; ++ks) {  // +32 B per 8 tf32 of K inside the 128 B rows
+            const uint64_t ahi = kmajor_sw128_desc(l_hi + ks * 32), alo = kmajor_sw128_desc(l_lo + ks * 32);
+            const uint64_t bhi = kmajor_sw128_desc(w_hi + ks * 32), blo = kmajor_sw128_desc(w_lo + ks * 32);
+            umma_tf32(d_tmem, ahi, bhi, idesc, (kb | ks) != 0);
             umma_tf32(d_tmem, alo, bhi, idesc, 1);
+            umma_tf32(d_tmem, ahi, blo, idesc, 1);
           }
           umma_commit(&empty[s]);
           if (kb == nkb - 1) umma_commit(&tfull[acc]);
@@ -251,11 +257,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4 && warp < 8) {
-    // ---------------- split + transpose: raw X [k][n] -> X_hi, X_lo (K-major SW128) ----------------
-    // thread t owns row n = t of the K-major tiles: 32 conflict-free column reads of the raw
-    // tile, 8 float4 stores per output tile (the 128B swizzle spreads a warp's rows over all banks).
-    static_assert(BN == 128, "split maps one thread per output row");
-    const int n = threadIdx.x - 128;
+    // ---------------- split + transpose: raw Λ [k][d] -> L_hi, L_lo [d][k] ----------------
+    // thread = output row d: 32 conflict-free column reads, 8 float4 stores per tile
+    // (the 128 B swizzle spreads a warp's rows over all banks).
+    const int d = threadIdx.x - 128;
     int g = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       for (int kb = 0; kb < nkb; ++kb, ++g) {
@@ -269,13 +274,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           float h[4], l[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float v = raw[(4 * j + q) * BN + n];
+            const float v = raw[(4 * j + q) * kBM + d];
             uint32_t hb;
             asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
             h[q] = __uint_as_float(hb);
             l[q] = v - h[q];
           }
-          const int off = n * 128 + ((j ^ (n & 7)) << 4);
+          const int off = d * 128 + ((j ^ (d & 7)) << 4);
           *reinterpret_cast<float4*>(st + SL::kHi + off) = make_float4(h[0], h[1], h[2], h[3]);
           *reinterpret_cast<float4*>(st + SL::kLo + off) = make_float4(l[0], l[1], l[2], l[3]);
         }
@@ -284,33 +289,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 8) {
-    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    // ---------------- epilogue: TMEM -> registers -> global (coalesced along d) ----------------
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
     int it = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      int sr, plane, m0, n0;
-      tile_coords(t, sr, plane, m0, n0);
+      int b[4], m0, n0;
+      decode(t, b, m0, n0);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int m = m0 + q * 32 + lane;
-      float* crow = p.C + sr * p.c_sr + plane * p.c_plane + (long long)m * p.ldc + n0;
-      const float* rrow = p.R ? p.R + sr * p.r_sr + plane * p.r_plane + (long long)m * p.ldr + n0 : nullptr;
+      const int dd = m0 + q * 32 + lane;
+      float* out = p.out + lin5l(p.out_c, b) + (long long)n0 * p.ldn_out + dd;
+      const float* res = p.res ? p.res + lin5l(p.res_c, b) + (long long)n0 * p.ldn_res + dd : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        // all loads of the chunk are issued before its first store (out/res may alias as far
+        // as the compiler knows: interleaving would serialize 32 global round trips)
+        float o[32];
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 o = make_float4(p.alpha * __uint_as_float(v[j]), p.alpha * __uint_as_float(v[j + 1]),
-                                 p.alpha * __uint_as_float(v[j + 2]), p.alpha * __uint_as_float(v[j + 3]));
-          if (rrow) {
-            float4 r = *reinterpret_cast<const float4*>(rrow + c * 32 + j);
-            o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
-          }
-          *reinterpret_cast<float4*>(crow + c * 32 + j) = o;
+        for (int j = 0; j < 32; ++j) o[j] = p.alpha * __uint_as_float(v[j]);
+        float* oc = out + (long long)c * 32 * p.ldn_out;
+        if (p.accumulate) {
+          float old[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) old[j] = oc[j * p.ldn_out];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] += old[j];
         }
+        if (res) {
+          const float* rc = res + (long long)c * 32 * p.ldn_res;
+          float rr[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rr[j] = __ldg(rc + j * p.ldn_res);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] += rr[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) __stcs(oc + j * p.ldn_out, o[j]);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -321,7 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(2 * BN < 32 ? 32 : 2 * BN));
   }
 }
 
@@ -346,70 +365,78 @@ EncodeTiledFn encode_fn() {
 
 int g_num_sms = 0;
 
+template <int BN, int STAGES>
+int launch_bn(const void* tm_lam, const void* tm_whi, const void* tm_wlo, const LamGemm& p, int grid,
+              cudaStream_t st) {
+  using SL = SmemLayout<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lam_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, SL::kBytes);
+    attr = true;
+  }
+  lam_gemm_kernel<BN, STAGES><<<grid, kThreads, SL::kBytes, st>>>(
+      *static_cast<const CUtensorMap*>(tm_lam), *static_cast<const CUtensorMap*>(tm_whi),
+      *static_cast<const CUtensorMap*>(tm_wlo), p);
+  return 1;
+}
+
 }  // namespace
 
-bool umma_tmap_weights(void* tm, const float* a, int C, int O) {
-  EncodeTiledFn enc = encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)O, 2};
-  cuuint64_t strides[2] = {(cuuint64_t)C * 4, (cuuint64_t)C * O * 4};
-  cuuint32_t box[3] = {kBK, kBM, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  return enc(static_cast<CUtensorMap*>(tm), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(a), dims,
-             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+int umma_pick_bn(int N) {
+  return N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : (N % 64 == 0 ? 64 : (N % 32 == 0 ? 32 : 0)));
 }
 
-bool umma_tmap_lambda(void* tm, const float* lam, long long cr, int D, int C, long long rows) {
+bool umma_available() { return encode_fn() != nullptr; }
+
+bool umma_tmap_lam(void* tm, const float* base, const unsigned long long dims[4],
+                   const unsigned long long strides_bytes[3], int kdim) {
   EncodeTiledFn enc = encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)C, (cuuint64_t)rows, 2};
-  cuuint64_t strides[3] = {(cuuint64_t)D * 4, (cuuint64_t)C * D * 4, (cuuint64_t)cr * 4};
-  cuuint32_t box[4] = {128, kBK, 1, 1};
+  if (!enc || (kdim != 1 && kdim != 2)) return false;
+  cuuint64_t dm[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t sd[3] = {strides_bytes[0], strides_bytes[1], strides_bytes[2]};
+  cuuint32_t box[4] = {kBM, kdim == 1 ? (cuuint32_t)kBK : 1u, kdim == 2 ? (cuuint32_t)kBK : 1u, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
-  return enc(static_cast<CUtensorMap*>(tm), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(lam), dims,
-             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  return enc(static_cast<CUtensorMap*>(tm), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dm, sd,
+             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool umma_supported(int M, int N, int K) {
-  return encode_fn() != nullptr && M % kBM == 0 && K % kBK == 0 && N % 128 == 0 && M > 0 && N > 0;
+bool umma_tmap_wop(void* tm, const float* base, int K, int N, int P2, int P3, int bn) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc || bn <= 0 || N % bn != 0 || K % kBK != 0) return false;
+  cuuint64_t dm[4] = {(cuuint64_t)K, (cuuint64_t)N, (cuuint64_t)P2, (cuuint64_t)P3};
+  cuuint64_t sd[3] = {(cuuint64_t)K * 4, (cuuint64_t)K * N * 4, (cuuint64_t)K * N * P2 * 4};
+  cuuint32_t box[4] = {kBK, (cuuint32_t)bn, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(static_cast<CUtensorMap*>(tm), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dm, sd,
+             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int launch_affine_umma(const void* tm_ahi, const void* tm_alo, const void* tm_b, float* C, long long c_sr,
-                       long long c_plane, const float* R, long long r_sr, long long r_plane, int M, int N, int K,
-                       long long rows, float alpha, cudaStream_t st) {
-  if (!umma_supported(M, N, K)) return -1;
+int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, LamGemm p, int bn,
+                    cudaStream_t st) {
+  if (p.M % kBM || p.K % kBK || p.K0 % kBK || bn <= 0 || p.N % bn) return -1;
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  UmmaParams p{};
-  p.C = C; p.ldc = N; p.c_sr = c_sr; p.c_plane = c_plane;
-  p.R = R; p.ldr = N; p.r_sr = r_sr; p.r_plane = r_plane;
-  p.M = M; p.N = N; p.K = K;
-  p.alpha = alpha;
-  p.tiles_m = M / kBM;
-  p.tiles_n = N / 128;
-  long long tiles = (long long)p.tiles_m * p.tiles_n * rows * 2;
-  if (tiles > 0x7fffffff) return -1;
+  p.tiles_m = p.M / kBM;
+  p.tiles_n = p.N / bn;
+  long long tiles = (long long)p.tiles_m * p.tiles_n * p.nb[0] * p.nb[1] * p.nb[2] * p.nb[3];
+  if (tiles <= 0 || tiles > 0x7fffffff) return -1;
   p.num_tiles = (int)tiles;
-  int grid = (int)std::min<long long>(tiles, g_num_sms);
-  const CUtensorMap& a = *static_cast<const CUtensorMap*>(tm_ahi);
-  const CUtensorMap& b = *static_cast<const CUtensorMap*>(tm_alo);
-  const CUtensorMap& x = *static_cast<const CUtensorMap*>(tm_b);
-  using SL = SmemLayout<128, 2>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(affine_umma_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SL::kBytes);
-    attr = true;
+  const int grid = (int)std::min<long long>(tiles, g_num_sms);
+  switch (bn) {
+    case 256: return launch_bn<256, 2>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+    case 128: return launch_bn<128, 2>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+    case 64: return launch_bn<64, 3>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+    case 32: return launch_bn<32, 3>(tm_lam, tm_whi, tm_wlo, p, grid, st);
   }
-  affine_umma_kernel<128, 2><<<grid, kThreads, SL::kBytes, st>>>(a, b, x, p);
-  return 1;
+  return -1;
 }
 
-// f64 reference of the plane GEMM for fg_selftest_affine (test facility, not on the pass).
+// f64 reference of the affine plane GEMM for fg_selftest_affine (test facility, not on the pass).
 __global__ void ref_affine_f64_kernel(const float* A, const float* X, long long x_cr, double* Y, int C, int O,
                                       int D, long long rows) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
