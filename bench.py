@@ -238,14 +238,12 @@ def main():
         return reference_arm(args, w)
 
     import torch
+    from paper_2209_12708_b200 import dist as D
     from paper_2209_12708_b200 import faith_gpu as F
 
     rank, world, local = dist_env()
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+    dist = D.init(backend="nccl", device_index=local)
     B = args.batch or {"c1": 64, "c2": 64, "c3": 32, "c4": 8, "c5": 2}[w.name]
 
     cfg = F.ModelConfig(w.layers, w.heads, w.embed, w.ffn, w.length, w.classes, w.activation)
@@ -253,10 +251,10 @@ def main():
     model = F.Model(ctx, cfg, F.gen_synthetic(cfg, w.model_seed))
 
     def batch(step):
-        # globally unique sentence ids: rank-major blocks, warm-up steps first
-        base = (rank * (args.steps + args.warmup) + step) * B
-        xs = np.stack([F.gen_input(cfg, w.input_seed(base + i)) for i in range(B)])
-        ps = np.stack([F.gen_positions(w.position_seed(base + i), w.length, w.words) for i in range(B)])
+        # globally unique sentence ids: rank-major blocks, warm-up steps first (no data-path collective)
+        ids = D.sentence_block(rank, step, args.steps + args.warmup, B)
+        xs = np.stack([F.gen_input(cfg, w.input_seed(i)) for i in ids])
+        ps = np.stack([F.gen_positions(w.position_seed(i), w.length, w.words) for i in ids])
         return xs, ps
 
     inputs = [batch(s) for s in range(args.warmup + args.steps)]  # host buffers (the user's data)
@@ -288,10 +286,7 @@ def main():
             d2h += st["passes"] * B * (2 * w.classes * 8 + 4)
         barrier()
         wall = time.perf_counter() - t0
-    t = torch.tensor([dev_ms, wall], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms_max, wall_max = float(t[0]), float(t[1])
+    dev_ms_max, wall_max = D.max_over_ranks([dev_ms, wall], dist, device="cuda")
     sentences = B * args.steps * world
     value = sentences / (dev_ms_max / 1e3)
     e2e = sentences / wall_max

@@ -1,0 +1,97 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the sentence-sharding plumbing that
+bench.py and multi-GPU certification use.  The per-sentence work is the C restatement of
+the reference pass (the GPU path is exercised by the -m gpu tests)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2209_12708_b200 import dist as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle.oracle import ModelConfig, Oracle
+    from paper_2209_12708_b200 import dist as Dm
+    dist = Dm.init(backend="gloo")
+    info = Dm.rank_info()
+    # 1) bench sentence blocks: disjoint across ranks and steps
+    ids = [i for step in range(3) for i in Dm.sentence_block(info.rank, step, 3, 4)]
+    allids = [None] * world
+    dist.all_gather_object(allids, ids)
+    # 2) max over ranks of device times
+    mx = Dm.max_over_ranks([1.0 + info.rank, 5.0 - info.rank], dist)
+    # 3) sharded certification of 5 sentences (C restatement of the reference pass)
+    o = Oracle("port")
+    cfg = ModelConfig(1, 2, 16, 32, 8)
+    params = o.gen_model(cfg, 11)
+
+    def work(r):
+        out = []
+        for s in r:
+            x = o.gen_input(cfg, 2000 + s)
+            pos = o.gen_positions(3000 + s, cfg.length, 1)
+            st, lo, hi, _, _ = o.bound_pass(cfg, params, x, pos, "linf", 0.02)
+            out.append((s, st, lo.tolist(), hi.tolist()))
+        return out
+
+    res = Dm.run_sharded(5, work, dist)
+    q.put((info.rank, allids, mx, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_partitions():
+    for n in (0, 1, 5, 8, 17):
+        for w in (1, 2, 3, 8):
+            parts = [list(D.shard(n, r, w)) for r in range(w)]
+            flat = [i for p in parts for i in p]
+            assert flat == list(range(n))
+            assert max(map(len, parts)) - min(map(len, parts)) <= 1
+
+
+def test_world2_gloo_sharding(port_oracle=None):
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        rank, allids, mx, res = q.get(timeout=240)
+        out[rank] = (allids, mx, res)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    allids = out[0][0]
+    flat = [i for ids in allids for i in ids]
+    assert len(flat) == len(set(flat)) == 2 * 3 * 4
+    assert out[0][1] == out[1][1] == [2.0, 5.0]
+    res = out[0][2]
+    assert out[1][2] is None
+    assert [r[0] for r in res] == list(range(5))
+    # results gathered across ranks equal a single-process run
+    from oracle.oracle import ModelConfig, Oracle
+    o = Oracle("port")
+    cfg = ModelConfig(1, 2, 16, 32, 8)
+    params = o.gen_model(cfg, 11)
+    for s, st, lo, hi in res:
+        x = o.gen_input(cfg, 2000 + s)
+        pos = o.gen_positions(3000 + s, cfg.length, 1)
+        st2, lo2, hi2, _, _ = o.bound_pass(cfg, params, x, pos, "linf", 0.02)
+        assert st == st2 and np.array_equal(lo, lo2) and np.array_equal(hi, hi2)
