@@ -637,7 +637,7 @@ struct Workspace {
   TensorMap tm_QKVk, tm_QKVrow, tm_SC;
   DBuf cf_sim_x[2], cf_sim_y[2], cf_wv_x[2], cf_wv_y[2];  // [hi, lo]
   TensorMap tm_sim_x[2], tm_sim_y[2], tm_wv_x[2], tm_wv_y[2];
-  int bn_sim = 0, bn_wvx = 0;
+  int bn_sim = 0, bn_simx = 0, bn_wvx = 0;
   bool dots_ok = false;
   long long crX = 0, crQKV = 0, crF = 0, crSC = 0;
   DBuf X_b, R1_b, QKV_b, SC_b, CTX_b, F_b;  // f64 lb/ub(/lo/hi) blocks
@@ -747,10 +747,11 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot) {
             lam_map(w.tm_CTX, w.CTX.as<float>(), w.crX, D, (int)E, rows, 1) &&
             lam_map(w.tm_F, w.QF.as<float>(), w.crF, D, (int)F, rows, 1);
   // McCormick dot products on tcgen05 (shapes: K multiples of 32, N multiples of 32)
-  w.bn_sim = umma_pick_bn((int)L);
-  w.bn_wvx = umma_pick_bn((int)hd);
+  w.bn_sim = umma_pick_bn((int)L);       // y-side GEMMs: N = L
+  w.bn_simx = umma_pick_bn((int)(2 * L)); // Q.K^T x-side: both output planes in N = 2L
+  w.bn_wvx = umma_pick_bn((int)(2 * hd)); // P.V x-side: N = 2hd
   w.dots_ok = false;
-  if (w.tm_ok && w.bn_sim > 0 && w.bn_wvx > 0 && hd % 32 == 0 && L % 32 == 0) {
+  if (w.tm_ok && w.bn_sim > 0 && w.bn_simx > 0 && w.bn_wvx > 0 && hd % 32 == 0 && L % 32 == 0) {
     const long long SH = (long long)S * H;
     bool ok = lam_map(w.tm_QKVk, w.QF.as<float>(), w.crQKV, D, (int)(3 * E), rows, 1) &&
               lam_map(w.tm_QKVrow, w.QF.as<float>(), w.crQKV, D, (int)(3 * E), rows, 2) &&
@@ -760,9 +761,10 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot) {
       CK(w.cf_sim_y[part].alloc(sizeof(float) * SH * 2 * L * hd));
       CK(w.cf_wv_x[part].alloc(sizeof(float) * SH * 2 * hd * 2 * L));
       CK(w.cf_wv_y[part].alloc(sizeof(float) * SH * 2 * L * L));
-      ok = ok && umma_tmap_wop(w.tm_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), (int)(2 * hd), (int)L, 2, (int)SH, w.bn_sim) &&
+      // x-side coefficient arrays [SH][2 planes][rows][K] are read as [SH][2*rows][K]
+      ok = ok && umma_tmap_wop(w.tm_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), (int)(2 * hd), (int)(2 * L), 1, (int)SH, w.bn_simx) &&
            umma_tmap_wop(w.tm_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), (int)hd, (int)L, 2, (int)SH, w.bn_sim) &&
-           umma_tmap_wop(w.tm_wv_x[part].bytes, w.cf_wv_x[part].as<float>(), (int)(2 * L), (int)hd, 2, (int)SH, w.bn_wvx) &&
+           umma_tmap_wop(w.tm_wv_x[part].bytes, w.cf_wv_x[part].as<float>(), (int)(2 * L), (int)(2 * hd), 1, (int)SH, w.bn_wvx) &&
            umma_tmap_wop(w.tm_wv_y[part].bytes, w.cf_wv_y[part].as<float>(), (int)L, (int)L, 2, (int)SH, w.bn_sim);
     }
     w.dots_ok = ok;
@@ -864,19 +866,20 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
                                    w.cf_sim_y[0].as<float>(), w.cf_sim_y[1].as<float>(), st));
       LAUNCH(launch_sim_bias(q, k, sc, S, H, L, hd, scale, st));
       // x-side: scores[s,h,i,j,:] = sum_k2 Cx[j,k2] (Qc|Qr)[i, h*hd + k2]   (K0 = hd: c|r concat)
+      // (both output planes in one N = 2L range: n -> plane n / L, key j = n % L)
       LamGemm gx{};
-      gx.M = D; gx.N = L; gx.K = 2 * hd; gx.K0 = hd;
-      gx.nb[0] = S; gx.nb[1] = H; gx.nb[2] = L; gx.nb[3] = 2;
+      gx.M = D; gx.N = 2 * L; gx.K = 2 * hd; gx.K0 = hd;
+      gx.nb[0] = S; gx.nb[1] = H; gx.nb[2] = L; gx.nb[3] = 1;
       gx.kdim = 1;
       gx.lam_c[0][1] = hd;                    // neuron h*hd (+k)
       gx.lam_c[1][0] = L; gx.lam_c[1][2] = 1;  // row s*L + i
-      gx.w_c[0][3] = 1;                       // coefficient plane = output plane
       gx.w_c[1][0] = H; gx.w_c[1][1] = 1;      // (s, h)
       gx.out = SC;
       gx.out_c[0] = (long long)H * L * L * D; gx.out_c[1] = (long long)L * L * D; gx.out_c[2] = (long long)L * D;
-      gx.out_c[3] = w.crSC; gx.ldn_out = D;
+      gx.ldn_out = D;
+      gx.n_split = L; gx.split_stride = w.crSC;
       gx.alpha = (float)scale;
-      LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_x[0].bytes, w.tm_sim_x[1].bytes, gx, w.bn_sim, st));
+      LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_x[0].bytes, w.tm_sim_x[1].bytes, gx, w.bn_simx, st));
       // y-side: scores[s,h,i,j,:] += sum_k lx[i,k] K_p[j, E + h*hd + k]   (per plane p)
       LamGemm gy{};
       gy.M = D; gy.N = L; gy.K = hd; gy.K0 = hd;
@@ -915,16 +918,17 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
                                   w.cf_wv_y[0].as<float>(), w.cf_wv_y[1].as<float>(), st));
       LAUNCH(launch_wv_bias(sc, v, cx, S, H, L, hd, st));
       // x-side: ctx[s,i,h*hd+k,:] = sum_j2 Cx[k,j2] (Pc|Pr)[s,h,i,j2]   (K0 = L: c|r concat)
+      // (both output planes in one N = 2hd range: n -> plane n / hd, k = n % hd)
       LamGemm gx{};
-      gx.M = D; gx.N = hd; gx.K = 2 * L; gx.K0 = L;
-      gx.nb[0] = S; gx.nb[1] = H; gx.nb[2] = L; gx.nb[3] = 2;
+      gx.M = D; gx.N = 2 * hd; gx.K = 2 * L; gx.K0 = L;
+      gx.nb[0] = S; gx.nb[1] = H; gx.nb[2] = L; gx.nb[3] = 1;
       gx.kdim = 1;
       gx.lam_c[1][0] = H * L; gx.lam_c[1][1] = L; gx.lam_c[1][2] = 1;  // score row (s, h, i)
-      gx.w_c[0][3] = 1;
       gx.w_c[1][0] = H; gx.w_c[1][1] = 1;
       gx.out = CTX;
       gx.out_c[0] = (long long)L * E * D; gx.out_c[1] = (long long)hd * D; gx.out_c[2] = (long long)E * D;
-      gx.out_c[3] = w.crX; gx.ldn_out = D;
+      gx.ldn_out = D;
+      gx.n_split = hd; gx.split_stride = w.crX;
       gx.alpha = 1.0f;
       LAUNCH(launch_lam_gemm(w.tm_SC.bytes, w.tm_wv_x[0].bytes, w.tm_wv_x[1].bytes, gx, w.bn_wvx, st));
       // y-side: ctx[s,i,h*hd+k,:] += sum_j lx[i,j] V_p[j, 2E + h*hd + k]   (K along token rows)

@@ -149,6 +149,10 @@ struct LamGemm {
   int w_c[2][5];
   long long out_c[5], res_c[5];
   long long ldn_out, ldn_res;
+  // output column n goes to (n / n_split) * split_stride + (n % n_split) * ldn_out
+  // (both Λ planes of a McCormick x-side term in one N range); n_split = 0: no split
+  int n_split;
+  long long split_stride;
   float* out;
   const float* res;
   float alpha;

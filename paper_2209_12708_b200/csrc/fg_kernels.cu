@@ -5,6 +5,7 @@
 // (no FMA contraction), so on identical inputs they are bit-identical to
 // proj/src/relax.cpp.  The dense Λ contractions live in fg_gemm.cu.
 #include <math.h>
+#include <stdlib.h>
 
 #include "fg_internal.cuh"
 
@@ -371,37 +372,63 @@ __global__ void compose_kernel(const float* __restrict__ lin, long long crin, co
 // Affine bias path (relax.cpp:273-299) in f64: one thread per output neuron,
 // i accumulated in the reference's order; optional residual propagate_add(res, y).
 // ---------------------------------------------------------------------------
-__global__ void affine_bias_kernel(const double* __restrict__ lb_in, const double* __restrict__ ub_in,
-                                   const double* __restrict__ w, const double* __restrict__ bias,
-                                   const double* __restrict__ res_lb, const double* __restrict__ res_ub,
-                                   double* __restrict__ lb_out, double* __restrict__ ub_out,
-                                   long long nrows, int C, int O) {
-  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nrows * O) return;
-  long long r = t / O;
-  int j = (int)(t % O);
-  const double* xlb = lb_in + r * C;
-  const double* xub = ub_in + r * C;
-  double ub_pos = 0.0, ub_neg = 0.0, lb_pos = 0.0, lb_neg = 0.0;
-  for (int i = 0; i < C; ++i) {
-    double wv = w[(long long)i * O + j];
-    double wp = (wv < 0.0) ? 0.0 : wv;
-    double wn = (0.0 < wv) ? 0.0 : wv;
-    double xu = xub[i], xl = xlb[i];
-    ub_pos += wp * xu;
-    ub_neg += wn * xl;
-    lb_pos += wp * xl;
-    lb_neg += wn * xu;
+constexpr int kBiasRows = 8;     // token rows per CTA (one weight load feeds all of them)
+constexpr int kBiasCols = 128;   // output neurons per CTA (one per thread)
+constexpr int kBiasChunk = 256;  // input neurons staged in SMEM per step
+
+__global__ void __launch_bounds__(kBiasCols) affine_bias_kernel(
+    const double* __restrict__ lb_in, const double* __restrict__ ub_in, const double* __restrict__ w,
+    const double* __restrict__ bias, const double* __restrict__ res_lb, const double* __restrict__ res_ub,
+    double* __restrict__ lb_out, double* __restrict__ ub_out, long long nrows, int C, int O) {
+  __shared__ double2 xs[kBiasRows][kBiasChunk];  // (lb, ub) of the CTA's rows
+  const int j = blockIdx.x * kBiasCols + threadIdx.x;
+  const long long r0 = (long long)blockIdx.y * kBiasRows;
+  double ub_pos[kBiasRows], ub_neg[kBiasRows], lb_pos[kBiasRows], lb_neg[kBiasRows];
+#pragma unroll
+  for (int r = 0; r < kBiasRows; ++r) ub_pos[r] = ub_neg[r] = lb_pos[r] = lb_neg[r] = 0.0;
+  for (int i0 = 0; i0 < C; i0 += kBiasChunk) {
+    const int n = min(kBiasChunk, C - i0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < kBiasRows * kBiasChunk; t += kBiasCols) {
+      const int r = t / kBiasChunk, i = t % kBiasChunk;
+      double2 v = make_double2(0.0, 0.0);
+      if (i < n && r0 + r < nrows) v = make_double2(lb_in[(r0 + r) * C + i0 + i], ub_in[(r0 + r) * C + i0 + i]);
+      xs[r][i] = v;
+    }
+    __syncthreads();
+    if (j < O) {
+      // i ascending per (row, j): the reference's accumulation order (relax.cpp:280-287)
+      for (int i = 0; i < n; ++i) {
+        const double wv = w[(long long)(i0 + i) * O + j];
+        const double wp = (wv < 0.0) ? 0.0 : wv;
+        const double wn = (0.0 < wv) ? 0.0 : wv;
+#pragma unroll
+        for (int r = 0; r < kBiasRows; ++r) {
+          const double2 x = xs[r][i];
+          ub_pos[r] += wp * x.y;
+          ub_neg[r] += wn * x.x;
+          lb_pos[r] += wp * x.x;
+          lb_neg[r] += wn * x.y;
+        }
+      }
+    }
   }
-  double bv = bias ? bias[j] : 0.0;
-  double yub = ub_pos + ub_neg + bv;
-  double ylb = lb_pos + lb_neg + bv;
-  if (res_lb) {
-    yub = res_ub[t] + yub;
-    ylb = res_lb[t] + ylb;
+  if (j >= O) return;
+  const double bv = bias ? bias[j] : 0.0;
+#pragma unroll
+  for (int r = 0; r < kBiasRows; ++r) {
+    const long long row = r0 + r;
+    if (row >= nrows) break;
+    const long long t = row * O + j;
+    double yub = ub_pos[r] + ub_neg[r] + bv;
+    double ylb = lb_pos[r] + lb_neg[r] + bv;
+    if (res_lb) {  // propagate_add(res, y) (relax.cpp:666-667)
+      yub = res_ub[t] + yub;
+      ylb = res_lb[t] + ylb;
+    }
+    ub_out[t] = yub;
+    lb_out[t] = ylb;
   }
-  ub_out[t] = yub;
-  lb_out[t] = ylb;
 }
 
 // ---------------------------------------------------------------------------
@@ -535,6 +562,180 @@ __device__ __forceinline__ double block_reduce(double v, double* scratch) {
   double r = scratch[0];
   for (int i = 1; i < nw; ++i) r = qcombine<Q>(r, scratch[i]);
   return r;
+}
+
+// Softmax chain, two-read version (the pass uses this one):
+//   phase 1 (warp per key row j): row norms -> exp envelope (ExpVerify) -> e bounds/norms, and the
+//            composed row a*sel(row) accumulated into the warp's Σ slab in SMEM (SumReduce);
+//   phase 2 (column-owned): Σ over the warp slabs -> norms -> recip envelope (RecipVerify) -> r;
+//   phase 3 (warp per key row): McCormick e_j * r (MulBroadcast) written in place, row norms by
+//            warp reduction -> probs lb/ub/lo/hi.
+// Scores Λ is read twice and written once; occupancy is capped so that the second read of a
+// CTA's rows (L*D*8 bytes) is served by L2.
+template <int Q>
+__global__ void __launch_bounds__(512) softmax2_kernel(NView sc, int rows_per_s, int n, int D,
+                                                       const double* __restrict__ eps, int* __restrict__ status,
+                                                       int site_exp, int site_recip) {
+  extern __shared__ double sm2[];
+  const int nw = blockDim.x >> 5;
+  double* a_lo = sm2;
+  double* a_up = a_lo + n;
+  double* e_lb = a_up + n;
+  double* e_ub = e_lb + n;
+  double* e_lo = e_ub + n;
+  double* e_hi = e_lo + n;
+  double* ru = e_hi + n;  // Σ_u, then r_u  [D]
+  double* rl = ru + D;    // Σ_l, then r_l  [D]
+  double* red = rl + D;   // 32
+  double* scal = red + 32;
+  float* part = reinterpret_cast<float*>(scal + 8);  // [nw][2][D]
+
+  const int s = blockIdx.x / rows_per_s;
+  const int row = blockIdx.x % rows_per_s;
+  const long long nb = (long long)s * sc.s_stride + (long long)row * n;
+  float* cb = sc.lam + nb * D;
+  float* rb = cb + sc.cr;
+  const double e = eps[s];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (int t = threadIdx.x; t < nw * 2 * D; t += blockDim.x) part[t] = 0.f;
+  __syncthreads();
+  float* pu = part + (size_t)warp * 2 * D;
+  float* pl = pu + D;
+
+  // ---- phase 1: ExpVerify per key + SumReduce into the warp slab
+  int err_exp = 0;
+  for (int j = warp; j < n; j += nw) {
+    const float* c = cb + (long long)j * D;
+    const float* r = rb + (long long)j * D;
+    NormAcc<Q> acc;
+    for (int d = lane * 4; d < D; d += 128)
+      acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
+    acc.warp_reduce();
+    const double nl = acc.fin(acc.l), nu = acc.fin(acc.u);
+    const double xlb = sc.lb[nb + j], xub = sc.ub[nb + j];
+    Lines ln;
+    const int code = envelope(RELAX_EXP, xlb - e * nl, xub + e * nu, ln);
+    if (code) err_exp = err_exp ? min(err_exp, code) : code;
+    const double au = ln.au, al = ln.al;
+    if (lane == 0) {
+      a_lo[j] = al;
+      a_up[j] = au;
+      const double ub2 = au * (au >= 0.0 ? xub : xlb) + ln.bu;
+      const double lb2 = al * (al >= 0.0 ? xlb : xub) + ln.bl;
+      e_ub[j] = ub2;
+      e_lb[j] = lb2;
+      // ||a v||_q = |a| ||v||_q: norms of the composed rows without re-reading them
+      e_lo[j] = lb2 - e * fabs(al) * (al >= 0.0 ? nl : nu);
+      e_hi[j] = ub2 + e * fabs(au) * (au >= 0.0 ? nu : nl);
+    }
+    for (int d = lane * 4; d < D; d += 128) {  // second touch of the row: L1
+      const float4 cv = *reinterpret_cast<const float4*>(c + d);
+      const float4 rv = *reinterpret_cast<const float4*>(r + d);
+      const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const double u = (double)cc[t] + (double)rr[t], l = (double)cc[t] - (double)rr[t];
+        pu[d + t] += (float)(au * (au >= 0.0 ? u : l));
+        pl[d + t] += (float)(al * (al >= 0.0 ? l : u));
+      }
+    }
+  }
+  if (lane == 0 && err_exp) set_status(status, s, site_exp, err_exp);
+  __syncthreads();
+
+  // ---- phase 2: Σ rows, RecipVerify, r rows
+  double pnu = 0.0, pnl = 0.0;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    double su = 0.0, sl = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      su += part[(size_t)(2 * w) * D + d];
+      sl += part[(size_t)(2 * w + 1) * D + d];
+    }
+    ru[d] = su;
+    rl[d] = sl;
+    if (Q == NORM_L1) { pnu += fabs(su); pnl += fabs(sl); }
+    else if (Q == NORM_L2) { pnu += su * su; pnl += sl * sl; }
+    else { pnu = fmax(pnu, fabs(su)); pnl = fmax(pnl, fabs(sl)); }
+  }
+  const double nsu = block_reduce<Q>(pnu, red);
+  const double nsl = block_reduce<Q>(pnl, red);
+  NormAcc<Q> fin;
+  if (threadIdx.x == 0) {
+    double slb = 0.0, sub = 0.0;  // propagate_sum_axis order (relax.cpp:728-731)
+    for (int j = 0; j < n; ++j) {
+      slb += e_lb[j];
+      sub += e_ub[j];
+    }
+    Lines ln;
+    const int code = envelope(RELAX_RECIP, slb - e * fin.fin(nsl), sub + e * fin.fin(nsu), ln);
+    if (code) set_status(status, s, site_recip, code);
+    scal[0] = ln.al;
+    scal[1] = ln.au;
+    scal[2] = ln.al * (ln.al >= 0.0 ? slb : sub) + ln.bl;
+    scal[3] = ln.au * (ln.au >= 0.0 ? sub : slb) + ln.bu;
+  }
+  __syncthreads();
+  const double r_al = scal[0], r_au = scal[1], r_lb = scal[2], r_ub = scal[3];
+  pnu = pnl = 0.0;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const double u = ru[d], l = rl[d];
+    const double yu = r_au * (r_au >= 0.0 ? u : l), yl = r_al * (r_al >= 0.0 ? l : u);
+    ru[d] = yu;
+    rl[d] = yl;
+    if (Q == NORM_L1) { pnu += fabs(yu); pnl += fabs(yl); }
+    else if (Q == NORM_L2) { pnu += yu * yu; pnl += yl * yl; }
+    else { pnu = fmax(pnu, fabs(yu)); pnl = fmax(pnl, fabs(yl)); }
+  }
+  const double r_lo = r_lb - e * fin.fin(block_reduce<Q>(pnl, red));
+  const double r_hi = r_ub + e * fin.fin(block_reduce<Q>(pnu, red));
+  __syncthreads();
+
+  // ---- phase 3: MulBroadcast per key row (warp per row)
+  for (int j = warp; j < n; j += nw) {
+    float* c = cb + (long long)j * D;
+    float* r = rb + (long long)j * D;
+    const double au = a_up[j], al = a_lo[j];
+    const double lx = e_lo[j], ly = r_lo, uy = r_hi;
+    double gu = 0.0, gl = 0.0;
+    for (int d = lane * 4; d < D; d += 128) {
+      const float4 cv = *reinterpret_cast<const float4*>(c + d);
+      const float4 rv = *reinterpret_cast<const float4*>(r + d);
+      const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+      float oc[4], orr[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const double u = (double)cc[t] + (double)rr[t], l = (double)cc[t] - (double)rr[t];
+        const double eu = au * (au >= 0.0 ? u : l), el = al * (al >= 0.0 ? l : u);
+        const double su = ru[d + t], sl = rl[d + t];
+        double p_l = 0.0, p_u = 0.0;
+        if (ly != 0.0) p_l += ly * (ly >= 0.0 ? el : eu);  // relax.cpp:542-553
+        if (lx != 0.0) p_l += lx * (lx >= 0.0 ? sl : su);
+        if (uy != 0.0) p_u += uy * (uy >= 0.0 ? eu : el);  // relax.cpp:556-567
+        if (lx != 0.0) p_u += lx * (lx >= 0.0 ? su : sl);
+        oc[t] = (float)(0.5 * (p_u + p_l));
+        orr[t] = (float)(0.5 * (p_u - p_l));
+        if (Q == NORM_L1) { gu += fabs(p_u); gl += fabs(p_l); }
+        else if (Q == NORM_L2) { gu += p_u * p_u; gl += p_l * p_l; }
+        else { gu = fmax(gu, fabs(p_u)); gl = fmax(gl, fabs(p_l)); }
+      }
+      *reinterpret_cast<float4*>(c + d) = make_float4(oc[0], oc[1], oc[2], oc[3]);
+      *reinterpret_cast<float4*>(r + d) = make_float4(orr[0], orr[1], orr[2], orr[3]);
+    }
+    if (Q == NORM_LINF) { gu = warp_max(gu); gl = warp_max(gl); }
+    else { gu = warp_sum(gu); gl = warp_sum(gl); }
+    if (lane == 0) {
+      double olb = 0.0, oub = 0.0;
+      term_bias(lx, ly, uy, e_lb[j], e_ub[j], r_lb, r_ub, olb, oub);
+      const long long o = nb + j;
+      sc.lb[o] = olb;
+      sc.ub[o] = oub;
+      if (sc.lo) {
+        sc.lo[o] = olb - e * fin.fin(gl);
+        sc.hi[o] = oub + e * fin.fin(gu);
+      }
+    }
+  }
 }
 
 template <int Q, int CH>
@@ -1076,8 +1277,9 @@ int launch_affine_bias(const double* lb_in, const double* ub_in, const double* w
   long long nrows = (long long)S * rows;
   long long total = nrows * O;
   if (total <= 0) return 0;
-  affine_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(lb_in, ub_in, w64, bias, res_lb,
-                                                             res_ub, lb_out, ub_out, nrows, C, O);
+  dim3 grid(blocks_for(O, kBiasCols), blocks_for(nrows, kBiasRows));
+  affine_bias_kernel<<<grid, kBiasCols, 0, st>>>(lb_in, ub_in, w64, bias, res_lb, res_ub, lb_out, ub_out, nrows,
+                                                 C, O);
   return 1;
 }
 
@@ -1156,6 +1358,28 @@ int launch_dot_weighted(const NView& p, const NView& v, const NView& out, int S,
 int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int norm,
                    const double* eps, int* status, int site_exp, int site_recip,
                    cudaStream_t st) {
+  const char* v1 = getenv("FG_SOFTMAX_V1");
+  if (!(v1 && v1[0] == '1')) {
+    const int nw = D <= 512 ? 16 : 8;
+    size_t smem = (6 * (size_t)n + 2 * (size_t)D + 40) * sizeof(double) + (size_t)nw * 2 * D * sizeof(float);
+    // at most two CTAs per SM: their rows (n*D*8 bytes each) stay in L2 between phases 1 and 3
+    const size_t cap = 110 * 1024;
+    if (smem < cap && (size_t)n * D * 8 > 64 * 1024) smem = cap;
+    if (smem > 227 * 1024) return -1;
+    static size_t attr_set[3] = {0, 0, 0};
+    const int q = dual_norm(norm);
+    auto launch = [&](auto kern) {
+      if (attr_set[q] < smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set[q] = smem;
+      }
+      kern<<<S * rows_per_s, nw * 32, smem, st>>>(sc, rows_per_s, n, D, eps, status, site_exp, site_recip);
+    };
+    if (q == NORM_L1) launch(softmax2_kernel<NORM_L1>);
+    else if (q == NORM_L2) launch(softmax2_kernel<NORM_L2>);
+    else launch(softmax2_kernel<NORM_LINF>);
+    return 1;
+  }
   int threads = D / 4;
   if (threads < 64) threads = 64;
   if (threads > kSmThreads) threads = kSmThreads;

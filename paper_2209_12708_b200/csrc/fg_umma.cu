@@ -300,10 +300,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const int dd = m0 + q * 32 + lane;
-      float* out = p.out + lin5l(p.out_c, b) + (long long)n0 * p.ldn_out + dd;
+      float* out_b = p.out + lin5l(p.out_c, b) + dd;
       const float* res = p.res ? p.res + lin5l(p.res_c, b) + (long long)n0 * p.ldn_res + dd : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
+        const int n = n0 + c * 32;
+        float* out = p.n_split ? out_b + (long long)(n / p.n_split) * p.split_stride +
+                                     (long long)(n % p.n_split) * p.ldn_out - (long long)c * 32 * p.ldn_out
+                               : out_b + (long long)n0 * p.ldn_out;
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
         // all loads of the chunk are issued before its first store (out/res may alias as far
