@@ -5,7 +5,10 @@
 // (no FMA contraction), so on identical inputs they are bit-identical to
 // proj/src/relax.cpp.  The dense Λ contractions live in fg_gemm.cu.
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
+
+#include <cooperative_groups.h>
 
 #include "fg_internal.cuh"
 
@@ -738,6 +741,467 @@ __global__ void __launch_bounds__(512) softmax2_kernel(NView sc, int rows_per_s,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Softmax chain, single-read cluster version (the pass uses this one).
+//
+// Persistent kernel: a thread-block CLUSTER of CS CTAs walks (sentence, head, query) score
+// rows; CTA `rank` owns the perturbation columns [rank*Dc, (rank+1)*Dc) of all n key rows.
+// The chunk of the NEXT row is bulk-loaded (cp.async.bulk + mbarriers, double-buffered)
+// while the current row is processed, so every SM keeps HBM reads in flight through the
+// serial parts of the chain.  Everything that couples columns is a q-norm over D: each CTA
+// reduces its chunk and PUSHES the partials into every CTA's exchange slot for its rank
+// (st.shared::cluster, slots double-buffered by row parity); after one cluster barrier each
+// CTA combines the CS slots in rank order 0..CS-1, so every CTA holds bit-identical norms and
+// takes identical envelope decisions.  Exchanges per row:
+//   x1  exp-input norms per key      -> ExpVerify envelopes (relax.cpp:363-394)
+//   x2  Σ_j e_j row norms             -> RecipVerify envelope (relax.cpp:396-424)
+//   x3  r = recip(Σ) row norms         -> McCormick y-interval of MulBroadcast
+//   x4  output row norms per key (to rank 0) -> probs lb/ub/lo/hi (relax.cpp:744-775)
+// Key rows are reduced by groups of `lpk` lanes (32/lpk keys per warp step).  Element math
+// is f32 (Λ is stored in f32); per-lane partials are combined in f64.
+// Scores Λ is read from HBM once and written once (in place).
+constexpr int kSm3Threads = 256;
+constexpr int kSm3MaxBars = 16;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int Q>
+__device__ __forceinline__ float qacc_f(float acc, float v) {  // f32 q-norm partial
+  return Q == NORM_L2 ? __fmaf_rn(v, v, acc) : (Q == NORM_L1 ? acc + fabsf(v) : fmaxf(acc, fabsf(v)));
+}
+
+template <int Q>
+__device__ __forceinline__ double qpart(double v) {  // one element's contribution to a q-norm
+  return Q == NORM_L2 ? v * v : fabs(v);
+}
+
+// q-combine across the `lpk` lanes of a key group (lanes lpk-aligned within the warp)
+template <int Q>
+__device__ __forceinline__ double group_reduce(double v, int lpk) {
+  for (int o = lpk >> 1; o > 0; o >>= 1) v = qcombine<Q>(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Cluster barrier split into arrive (release) / wait (acquire) halves.
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Asynchronous remote store of two doubles into CTA `rank`'s copy of `slot`, completing
+// `bytes` on that CTA's copy of `bar` (st.async ... mbarrier::complete_tx): the receiver
+// waits on its own mbarrier, so no cluster-wide barrier (and no release fence over the
+// CTA's global stores) is needed for the exchange.
+__device__ __forceinline__ void push2(double* slot, uint64_t* bar, int rank, double a, double b) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(slot)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_addr(bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+               "d"(a), "d"(b), "r"(rb)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_par(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WP_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WP_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
+template <int Q>
+__global__ void __launch_bounds__(kSm3Threads) softmax3_kernel(NView sc, int rows_per_s, int nrows, int n,
+                                                               int D, int CS, int lpk, int nbuf,
+                                                               const double* __restrict__ eps,
+                                                               int* __restrict__ status, int site_exp,
+                                                               int site_recip) {
+  extern __shared__ __align__(16) unsigned char sm3[];
+  const int Dc = D / CS;
+  uint32_t rank_u;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank_u));
+  const int rank = (int)rank_u;
+  const size_t tile = (size_t)n * Dc;
+  float* tbuf = reinterpret_cast<float*>(sm3);           // [nbuf buffers][c|r][n][Dc]
+  float* ru_f = tbuf + 2 * nbuf * tile;                  // [Dc] r_u rows (phase 3 operand)
+  float* rl_f = ru_f + Dc;                               // [Dc] r_l
+  double* su = reinterpret_cast<double*>(rl_f + Dc);     // [Dc] Σ_u
+  double* sl = su + Dc;                                  // [Dc] Σ_l
+  double* a_lo = sl + Dc;                                // per key [n] x 6
+  double* a_up = a_lo + n;
+  double* e_lb = a_up + n;
+  double* e_ub = e_lb + n;
+  double* e_lo = e_ub + n;
+  double* e_hi = e_lo + n;
+  double* xk0 = e_hi + n;                      // [2 parities][CS][n][2] per-key exchange (x1, x4)
+  double* xs0 = xk0 + (size_t)2 * CS * 2 * n;  // [2 parities][2][CS][2] row exchanges x2, x3
+  double* red = xs0 + 8 * CS;                  // [32]
+  double* scal = red + 32;                     // [8]
+  double* hs = scal + 8;                       // [kSm3Threads][8] key-range partial sums
+  uint64_t* bars = reinterpret_cast<uint64_t*>(hs + 8 * kSm3Threads);  // [2][kSm3MaxBars] loads
+  uint64_t* xbar = bars + 2 * kSm3MaxBars;                              // [2 parities][x1..x4]
+  float* a_lo_f = reinterpret_cast<float*>(xbar + 8);                   // [n]
+  float* a_up_f = a_lo_f + n;                                           // [n]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int kpw = 32 / lpk;                  // keys per warp step
+  const int kstep = nw * kpw;                // keys per block step
+  const int nsteps = (n + kstep - 1) / kstep;
+  const int spb = (nsteps + kSm3MaxBars - 1) / kSm3MaxBars;  // block steps per mbarrier
+  const int nbars = (nsteps + spb - 1) / spb;
+  const int kpb = spb * kstep;               // keys per mbarrier
+  const int sub = lane % lpk;                // lane within the key group
+  const int kofs = warp * kpw + lane / lpk;  // key offset within a block step
+  const int D4 = Dc / 4;
+  const int cluster_id = blockIdx.x / CS, nclusters = gridDim.x / CS;
+  NormAcc<Q> fin;
+
+  if (tid == 0) {
+    for (int b = 0; b < 2 * kSm3MaxBars + 8; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bars + b)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cluster_arrive();  // "this CTA has started": waited on before the first DSMEM store
+
+  // issue the bulk loads of row `rid` into buffer `buf` (warp 0)
+  auto issue = [&](int rid, int buf) {
+    if (warp != 0 || rid >= nrows) return;
+    const int s = rid / rows_per_s, row = rid % rows_per_s;
+    const long long nb = (long long)s * sc.s_stride + (long long)row * n;
+    const float* cb = sc.lam + nb * D + (long long)rank * Dc;
+    const float* rb = cb + sc.cr;
+    float* tc = tbuf + (size_t)buf * 2 * tile;
+    float* tr = tc + tile;
+    uint64_t* bb = bars + buf * kSm3MaxBars;
+    const uint32_t row_bytes = (uint32_t)Dc * 4u;
+    if (lane == 0) {
+      // the previous row's generic-proxy reads of this buffer precede the async-proxy writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int b = 0; b < nbars; ++b) {
+        const int j0 = b * kpb, j1 = min(n, j0 + kpb);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bb + b)),
+                     "r"(2u * row_bytes * (uint32_t)(j1 - j0))
+                     : "memory");
+      }
+    }
+    __syncwarp();
+    for (int j = lane; j < n; j += 32) {
+      const uint32_t bar = smem_addr(bb + j / kpb);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(tc + (size_t)j * Dc)),
+          "l"(cb + (long long)j * D), "r"(row_bytes), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(tr + (size_t)j * Dc)),
+          "l"(rb + (long long)j * D), "r"(row_bytes), "r"(bar)
+          : "memory");
+    }
+  };
+
+  issue(cluster_id, 0);
+  bool started = false;
+  int it_row = 0;
+  for (int rid = cluster_id; rid < nrows; rid += nclusters, ++it_row) {
+    const int buf = nbuf == 2 ? (it_row & 1) : 0, par = it_row & 1;
+    const uint32_t use_parity = (uint32_t)((it_row >> 1) & 1);
+    const uint32_t load_parity = nbuf == 2 ? use_parity : (uint32_t)(it_row & 1);
+    if (nbuf == 2) issue(rid + nclusters, buf ^ 1);  // prefetch the next row of this cluster
+    else if (it_row > 0) issue(rid, 0);              // single buffer: load after the last row's reads
+    const int s = rid / rows_per_s, row = rid % rows_per_s;
+    const long long nb = (long long)s * sc.s_stride + (long long)row * n;  // first neuron of the row
+    float* cb = sc.lam + nb * D + (long long)rank * Dc;
+    float* rb = cb + sc.cr;
+    const float* tc = tbuf + (size_t)buf * 2 * tile;
+    const float* tr = tc + tile;
+    uint64_t* bb = bars + buf * kSm3MaxBars;
+    double* xk = xk0 + (size_t)par * CS * 2 * n;
+    double* xs = xs0 + (size_t)par * 4 * CS;
+    uint64_t* xb = xbar + 4 * par;
+    const uint32_t xpar = use_parity;
+    if (tid == 0) {  // bytes each exchange delivers to this CTA (tx-count may run ahead)
+      mbar_expect(xb + 0, (uint32_t)(CS * n * 16));
+      mbar_expect(xb + 1, (uint32_t)(CS * 16));
+      mbar_expect(xb + 2, (uint32_t)(CS * 16));
+      if (rank == 0) mbar_expect(xb + 3, (uint32_t)(CS * n * 16));
+    }
+    const double e = eps[s];
+
+    for (int j = tid; j < n; j += blockDim.x) {  // scores lb/ub, consumed by phase 1b
+      e_lb[j] = sc.lb[nb + j];
+      e_ub[j] = sc.ub[nb + j];
+    }
+    // ---- phase 1a: partial norms of the exp inputs (lpk lanes per key)
+    for (int it = 0; it < nsteps; ++it) {
+      if (it % spb == 0) {
+        const uint32_t bar = smem_addr(bb + it / spb);
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "W3_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra W3_%=;\n}" ::"r"(bar),
+            "r"(load_parity)
+            : "memory");
+      }
+      const int j = it * kstep + kofs;
+      float fu = 0.f, fl = 0.f;
+      if (j < n) {
+        const float4* c = reinterpret_cast<const float4*>(tc + (size_t)j * Dc);
+        const float4* r = reinterpret_cast<const float4*>(tr + (size_t)j * Dc);
+        for (int f = sub; f < D4; f += lpk) {
+          const float4 cv = c[f], rv = r[f];
+          fu = qacc_f<Q>(fu, cv.x + rv.x); fl = qacc_f<Q>(fl, cv.x - rv.x);
+          fu = qacc_f<Q>(fu, cv.y + rv.y); fl = qacc_f<Q>(fl, cv.y - rv.y);
+          fu = qacc_f<Q>(fu, cv.z + rv.z); fl = qacc_f<Q>(fl, cv.z - rv.z);
+          fu = qacc_f<Q>(fu, cv.w + rv.w); fl = qacc_f<Q>(fl, cv.w - rv.w);
+        }
+      }
+      const double gu = group_reduce<Q>((double)fu, lpk), gl = group_reduce<Q>((double)fl, lpk);
+      if (!started) {
+        cluster_wait();
+        started = true;
+      }
+      if (j < n)  // push to every rank's slot [rank]
+        for (int q = sub; q < CS; q += lpk) push2(xk + ((size_t)rank * n + j) * 2, xb + 0, q, gu, gl);
+    }
+    mbar_wait_par(xb + 0, xpar);  // x1 from every rank
+
+    // ---- phase 1b: ExpVerify envelopes per key (every rank computes the same values)
+    int err_exp = 0;
+    for (int j = tid; j < n; j += blockDim.x) {
+      double pu = 0.0, pl = 0.0;
+      for (int q = 0; q < CS; ++q) {
+        pu = qcombine<Q>(pu, xk[((size_t)q * n + j) * 2]);
+        pl = qcombine<Q>(pl, xk[((size_t)q * n + j) * 2 + 1]);
+      }
+      const double nu = fin.fin(pu), nl = fin.fin(pl);
+      const double xlb = e_lb[j], xub = e_ub[j];  // prefetched scores lb/ub
+      Lines ln;
+      const int code = envelope(RELAX_EXP, xlb - e * nl, xub + e * nu, ln);
+      if (code) err_exp = err_exp ? min(err_exp, code) : code;
+      a_lo[j] = ln.al;
+      a_up[j] = ln.au;
+      a_lo_f[j] = (float)ln.al;
+      a_up_f[j] = (float)ln.au;
+      const double ub2 = ln.au * (ln.au >= 0.0 ? xub : xlb) + ln.bu;
+      const double lb2 = ln.al * (ln.al >= 0.0 ? xlb : xub) + ln.bl;
+      e_ub[j] = ub2;
+      e_lb[j] = lb2;
+      // ||a v||_q = |a| ||v||_q: norms of the composed rows without another sweep
+      e_lo[j] = lb2 - e * fabs(ln.al) * (ln.al >= 0.0 ? nl : nu);
+      e_hi[j] = ub2 + e * fabs(ln.au) * (ln.au >= 0.0 ? nu : nl);
+    }
+    if (err_exp && rank == 0) set_status(status, s, site_exp, err_exp);
+    __syncthreads();
+    if (warp == nw - 1) {  // Σ_j e_lb / e_ub (SumReduce bias) while the other warps start phase 2
+      double a = 0.0, b = 0.0;
+      for (int j = lane; j < n; j += 32) {
+        a += e_lb[j];
+        b += e_ub[j];
+      }
+      a = warp_sum(a);
+      b = warp_sum(b);
+      if (lane == 0) {
+        scal[4] = a;
+        scal[5] = b;
+      }
+    }
+
+    // ---- phase 2: SumReduce over keys.  Thread = (float4 column group, key range); 8
+    // independent f64 accumulators per thread (f32 products), key ranges combined in order.
+    const int gpt = D4 <= (int)blockDim.x ? D4 : (int)blockDim.x;  // column groups per sweep
+    const int nh = (int)blockDim.x / gpt;
+    {
+      const int h = tid / gpt;
+      if (h < nh) {
+        const int j0 = (int)((long long)n * h / nh), j1 = (int)((long long)n * (h + 1) / nh);
+        for (int g = tid % gpt; g < D4; g += gpt) {
+          double au_s[4] = {0.0, 0.0, 0.0, 0.0}, al_s[4] = {0.0, 0.0, 0.0, 0.0};
+          for (int j = j0; j < j1; ++j) {
+            const float au = a_up_f[j], al = a_lo_f[j];
+            const float4 cv = reinterpret_cast<const float4*>(tc + (size_t)j * Dc)[g];
+            const float4 rv = reinterpret_cast<const float4*>(tr + (size_t)j * Dc)[g];
+            const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float u = cc[t] + rr[t], l = cc[t] - rr[t];
+              au_s[t] += (double)(au * (au >= 0.f ? u : l));
+              al_s[t] += (double)(al * (al >= 0.f ? l : u));
+            }
+          }
+          double* dst = nh > 1 ? hs + ((size_t)h * D4 + g) * 8 : nullptr;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            if (nh > 1) {
+              dst[t] = au_s[t];
+              dst[4 + t] = al_s[t];
+            } else {
+              su[4 * g + t] = au_s[t];
+              sl[4 * g + t] = al_s[t];
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    double pnu = 0.0, pnl = 0.0;
+    for (int d = tid; d < Dc; d += blockDim.x) {
+      if (nh > 1) {
+        double a = 0.0, b = 0.0;
+        for (int h = 0; h < nh; ++h) {
+          a += hs[((size_t)h * D4 + d / 4) * 8 + (d & 3)];
+          b += hs[((size_t)h * D4 + d / 4) * 8 + 4 + (d & 3)];
+        }
+        su[d] = a;
+        sl[d] = b;
+      }
+      pnu = qcombine<Q>(pnu, qpart<Q>(su[d]));
+      pnl = qcombine<Q>(pnl, qpart<Q>(sl[d]));
+    }
+    pnu = block_reduce<Q>(pnu, red);
+    pnl = block_reduce<Q>(pnl, red);
+    if (tid < CS) push2(xs + 2 * rank, xb + 1, tid, pnu, pnl);
+    mbar_wait_par(xb + 1, xpar);
+    if (tid == 0) {
+      double nsu = 0.0, nsl = 0.0;
+      for (int q = 0; q < CS; ++q) {
+        nsu = qcombine<Q>(nsu, xs[2 * q]);
+        nsl = qcombine<Q>(nsl, xs[2 * q + 1]);
+      }
+      const double slb = scal[4], sub_ = scal[5];  // propagate_sum_axis (relax.cpp:728-731)
+      Lines ln;
+      const int code = envelope(RELAX_RECIP, slb - e * fin.fin(nsl), sub_ + e * fin.fin(nsu), ln);
+      if (code && rank == 0) set_status(status, s, site_recip, code);
+      scal[0] = ln.al;
+      scal[1] = ln.au;
+      scal[2] = ln.al * (ln.al >= 0.0 ? slb : sub_) + ln.bl;
+      scal[3] = ln.au * (ln.au >= 0.0 ? sub_ : slb) + ln.bu;
+    }
+    __syncthreads();
+    const double r_al = scal[0], r_au = scal[1], r_lb = scal[2], r_ub = scal[3];
+    pnu = pnl = 0.0;
+    for (int d = tid; d < Dc; d += blockDim.x) {
+      const double u = su[d], l = sl[d];
+      const double yu = r_au * (r_au >= 0.0 ? u : l), yl = r_al * (r_al >= 0.0 ? l : u);
+      ru_f[d] = (float)yu;
+      rl_f[d] = (float)yl;
+      pnu = qcombine<Q>(pnu, qpart<Q>(yu));
+      pnl = qcombine<Q>(pnl, qpart<Q>(yl));
+    }
+    pnu = block_reduce<Q>(pnu, red);
+    pnl = block_reduce<Q>(pnl, red);
+    if (tid < CS) push2(xs + 2 * CS + 2 * rank, xb + 2, tid, pnu, pnl);
+    mbar_wait_par(xb + 2, xpar);
+    double nru = 0.0, nrl = 0.0;
+    for (int q = 0; q < CS; ++q) {
+      nru = qcombine<Q>(nru, xs[2 * CS + 2 * q]);
+      nrl = qcombine<Q>(nrl, xs[2 * CS + 2 * q + 1]);
+    }
+    const double r_lo = r_lb - e * fin.fin(nrl);
+    const double r_hi = r_ub + e * fin.fin(nru);
+
+    // ---- phase 3: MulBroadcast (McCormick e_j * r) per key, written to HBM
+    const float ly = (float)r_lo, uy = (float)r_hi;
+    const bool ly_p = ly >= 0.f, uy_p = uy >= 0.f;
+    for (int it = 0; it < nsteps; ++it) {
+      const int j = it * kstep + kofs;
+      float fu = 0.f, fl = 0.f;
+      if (j < n) {
+        const float4* c = reinterpret_cast<const float4*>(tc + (size_t)j * Dc);
+        const float4* r = reinterpret_cast<const float4*>(tr + (size_t)j * Dc);
+        float4* gc = reinterpret_cast<float4*>(cb + (long long)j * D);
+        float4* gr = reinterpret_cast<float4*>(rb + (long long)j * D);
+        const float au = a_up_f[j], al = a_lo_f[j], lx = (float)e_lo[j];
+        const bool au_p = au >= 0.f, al_p = al >= 0.f, lx_p = lx >= 0.f;
+        for (int f = sub; f < D4; f += lpk) {
+          const float4 cv = c[f], rv = r[f];
+          const float4 yuv = reinterpret_cast<const float4*>(ru_f)[f];
+          const float4 ylv = reinterpret_cast<const float4*>(rl_f)[f];
+          const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+          const float yuu[4] = {yuv.x, yuv.y, yuv.z, yuv.w}, yll[4] = {ylv.x, ylv.y, ylv.z, ylv.w};
+          float oc[4], orr[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float u = cc[t] + rr[t], l = cc[t] - rr[t];
+            const float eu = au * (au_p ? u : l), el = al * (al_p ? l : u);
+            // relax.cpp:542-567: lower plane (cx = ly, cy = lx), upper plane (cx = uy, cy = lx)
+            const float p_l = __fmaf_rn(ly, ly_p ? el : eu, lx * (lx_p ? yll[t] : yuu[t]));
+            const float p_u = __fmaf_rn(uy, uy_p ? eu : el, lx * (lx_p ? yuu[t] : yll[t]));
+            oc[t] = 0.5f * (p_u + p_l);
+            orr[t] = 0.5f * (p_u - p_l);
+            fu = qacc_f<Q>(fu, p_u);
+            fl = qacc_f<Q>(fl, p_l);
+          }
+          gc[f] = make_float4(oc[0], oc[1], oc[2], oc[3]);
+          gr[f] = make_float4(orr[0], orr[1], orr[2], orr[3]);
+        }
+      }
+      const double gu = group_reduce<Q>((double)fu, lpk), gl = group_reduce<Q>((double)fl, lpk);
+      if (j < n && sub == 0) push2(xk + ((size_t)rank * n + j) * 2, xb + 3, 0, gu, gl);  // to rank 0
+    }
+    if (rank == 0) {
+      mbar_wait_par(xb + 3, xpar);
+      for (int j = tid; j < n; j += blockDim.x) {
+        double gu = 0.0, gl = 0.0;
+        for (int q = 0; q < CS; ++q) {
+          gu = qcombine<Q>(gu, xk[((size_t)q * n + j) * 2]);
+          gl = qcombine<Q>(gl, xk[((size_t)q * n + j) * 2 + 1]);
+        }
+        double olb = 0.0, oub = 0.0;
+        term_bias(e_lo[j], r_lo, r_hi, e_lb[j], e_ub[j], r_lb, r_ub, olb, oub);
+        const long long o = nb + j;
+        sc.lb[o] = olb;
+        sc.ub[o] = oub;
+        if (sc.lo) {
+          sc.lo[o] = olb - e * fin.fin(gl);
+          sc.hi[o] = oub + e * fin.fin(gu);
+        }
+      }
+    }
+    __syncthreads();  // e_* / a_* / buffers are rewritten by the next row
+  }
+  if (!started) cluster_wait();
+  cluster_arrive();  // no CTA leaves while a peer may still address its SMEM
+  cluster_wait();
+}
+
+size_t softmax3_smem(int n, int Dc, int CS, int nbuf) {
+  return (size_t)nbuf * n * Dc * 8 + (size_t)Dc * 8 + (size_t)Dc * 16 + (size_t)n * 6 * 8 +
+         (size_t)2 * CS * 2 * n * 8 + (size_t)8 * CS * 8 + (32 + 8) * 8 + (size_t)8 * kSm3Threads * 8 +
+         (2 * kSm3MaxBars + 8) * 8 + (size_t)n * 8;
+}
+
+// Lanes per key row: about 16 columns per lane, a power of two in [1, 32].
+int softmax3_lpk(int Dc) {
+  int l = 1;
+  while (l < 32 && l * 16 < Dc) l *= 2;
+  return l;
+}
+
+// Cluster size for the single-read softmax: the smallest power of two (<= 16) that divides
+// D/4 and brings the CTA's row tile (n*Dc*8 bytes) to <= `tile_kb`; else the smallest one
+// that fits SMEM at all; 0 when none does.
+int softmax3_cluster(int n, int D, int nbuf, int tile_kb) {
+  if (D % 4) return 0;
+  int best = 0;
+  for (int cs = 1; cs <= 16; cs *= 2) {
+    if ((D / 4) % cs) break;
+    const size_t sm = softmax3_smem(n, D / cs, cs, nbuf);
+    if (sm <= 227 * 1024 && best == 0) best = cs;
+    if ((size_t)n * (D / cs) * 8 <= (size_t)tile_kb * 1024) return sm <= 227 * 1024 ? cs : best;
+  }
+  return best;
+}
+
 template <int Q, int CH>
 __global__ void __launch_bounds__(kSmThreads) softmax_kernel(NView sc, int rows_per_s, int n, int D,
                                                              const double* __restrict__ eps,
@@ -1358,8 +1822,49 @@ int launch_dot_weighted(const NView& p, const NView& v, const NView& out, int S,
 int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int norm,
                    const double* eps, int* status, int site_exp, int site_recip,
                    cudaStream_t st) {
-  const char* v1 = getenv("FG_SOFTMAX_V1");
-  if (!(v1 && v1[0] == '1')) {
+  const char* ver = getenv("FG_SOFTMAX");  // "1" / "2": older multi-read kernels (comparison runs)
+  const char* pe = getenv("FG_SM3_PERSIST");
+  const char* te = getenv("FG_SM3_TILE_KB");
+  const int nbuf = (pe && pe[0] == '1') ? 2 : 1;
+  const int cs = softmax3_cluster(n, D, nbuf, te ? atoi(te) : 64);
+  if (cs > 0 && !(ver && (ver[0] == '1' || ver[0] == '2'))) {
+    const size_t smem = softmax3_smem(n, D / cs, cs, nbuf);
+    const int lpk = softmax3_lpk(D / cs);
+    static size_t attr_set[3] = {0, 0, 0};
+    const int q = dual_norm(norm);
+    auto launch = [&](auto kern) {
+      if (attr_set[q] < smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        attr_set[q] = smem;
+      }
+      const int nrows = S * rows_per_s;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(nrows * cs));
+      cfg.blockDim = dim3(kSm3Threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (nbuf == 2) {  // persistent: as many clusters as fit at once (at most one per row)
+        int mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, (void*)kern, &cfg) != cudaSuccess || mc <= 0) mc = 148 / cs;
+        const int ncl = mc < nrows ? mc : nrows;
+        cfg.gridDim = dim3((unsigned)(ncl * cs));
+      }
+      cudaLaunchKernelEx(&cfg, kern, sc, rows_per_s, nrows, n, D, cs, lpk, nbuf, eps, status, site_exp, site_recip);
+    };
+    if (q == NORM_L1) launch(softmax3_kernel<NORM_L1>);
+    else if (q == NORM_L2) launch(softmax3_kernel<NORM_L2>);
+    else launch(softmax3_kernel<NORM_LINF>);
+    return 1;
+  }
+  if (!(ver && ver[0] == '1')) {
     const int nw = D <= 512 ? 16 : 8;
     size_t smem = (6 * (size_t)n + 2 * (size_t)D + 40) * sizeof(double) + (size_t)nw * 2 * D * sizeof(float);
     // at most two CTAs per SM: their rows (n*D*8 bytes each) stay in L2 between phases 1 and 3
