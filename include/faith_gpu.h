@@ -65,6 +65,18 @@ typedef int fg_status;
 #define FG_DOT_SIMILARITY 0
 #define FG_DOT_WEIGHTED_VALUES 1
 
+/* Operator-level arithmetic of a context (fg_ctx_set_precision):
+ *   FG_PRECISION_F32  Λ in f32 centre/radius planes, O(N) state (biases, concretized
+ *                     bounds, envelope lines) in f64 -- the arithmetic of the fused pass;
+ *                     results agree with the reference within 1e-4*max(1,|ref|).
+ *   FG_PRECISION_F64  every operator in f64 in the reference's operation order (one thread
+ *                     per output element, no FMA contraction): the arithmetic operators are
+ *                     bit-identical to proj/src/relax.cpp / bounds.cpp, the exp/tanh/SiLU
+ *                     envelopes agree to the device libm's last ulp.  The C++ drop-in layer
+ *                     (compat/) uses this mode by default. */
+#define FG_PRECISION_F32 0
+#define FG_PRECISION_F64 1
+
 typedef struct fg_ctx fg_ctx;
 typedef struct fg_model fg_model;
 
@@ -74,6 +86,10 @@ typedef struct fg_model fg_model;
 fg_status fg_ctx_create(int device, fg_ctx** out);
 void fg_ctx_destroy(fg_ctx* ctx);
 const char* fg_last_error(const fg_ctx* ctx);
+/* Operator-level precision of the context (FG_PRECISION_*; default F32).  Model-level
+ * passes (fg_bound_pass / fg_certify / fg_maxeps) always run the F32 fused kernels. */
+fg_status fg_ctx_set_precision(fg_ctx* ctx, int precision);
+int fg_ctx_precision(const fg_ctx* ctx);
 /* Number of kernels this context has launched so far (evidence counter). */
 uint64_t fg_kernel_launches(const fg_ctx* ctx);
 const char* fg_version(void);
@@ -116,6 +132,34 @@ fg_status fg_dot(fg_ctx* ctx, int layout, size_t len, size_t embed, size_t heads
 fg_status fg_softmax(fg_ctx* ctx, size_t rows, size_t n, size_t d, const double* xlw,
                      const double* xlb, const double* xuw, const double* xub, int norm,
                      double eps, double* ylw, double* ylb, double* yuw, double* yub);
+/* propagate_dot_product with a leading batch axis (relax.cpp:573-654): the same as fg_dot
+ * for each of `batch` independent [len, ...] slices, which share the perturbation columns. */
+fg_status fg_dot_batched(fg_ctx* ctx, int layout, size_t batch, size_t len, size_t embed, size_t heads,
+                         size_t d, const double* alw, const double* alb, const double* auw,
+                         const double* aub, const double* blw, const double* blb, const double* buw,
+                         const double* bub, int norm, double eps, double* ylw, double* ylb, double* yuw,
+                         double* yub);
+/* propagate_softmax along the middle axis of [outer, n, inner] (relax.cpp:777-790).  F32
+ * precision runs the fused single-read kernel when inner == 1; every other case runs the f64
+ * operator chain exp -> sum -> recip -> McCormick multiply. */
+fg_status fg_softmax_axis(fg_ctx* ctx, size_t outer, size_t n, size_t inner, size_t d,
+                          const double* xlw, const double* xlb, const double* xuw, const double* xub,
+                          int norm, double eps, double* ylw, double* ylb, double* yuw, double* yub);
+/* propagate_sum_axis (relax.cpp:705-742): [outer, n, inner] -> [outer, 1, inner].  f64. */
+fg_status fg_sum_axis(fg_ctx* ctx, size_t outer, size_t n, size_t inner, size_t d, const double* xlw,
+                      const double* xlb, const double* xuw, const double* xub, double* ylw, double* ylb,
+                      double* yuw, double* yub);
+/* propagate_mul_broadcast (relax.cpp:744-775): x [outer, n, inner] times r [outer, 1, inner]
+ * under McCormick planes of the concretized operands.  f64. */
+fg_status fg_mul_broadcast(fg_ctx* ctx, size_t outer, size_t n, size_t inner, size_t d,
+                           const double* xlw, const double* xlb, const double* xuw, const double* xub,
+                           const double* rlw, const double* rlb, const double* ruw, const double* rub,
+                           int norm, double eps, double* ylw, double* ylb, double* yuw, double* yub);
+/* relax_bilinear (relax.cpp:499-523): McCormick planes of z = x*y on [xlo,xhi] x [ylo,yhi];
+ * FG_EINVAL when lo > hi for either operand (ConcreteBounds::validate).  f64. */
+fg_status fg_bilinear(fg_ctx* ctx, size_t n, const double* xlo, const double* xhi, const double* ylo,
+                      const double* yhi, double* lo_x, double* lo_y, double* lo_c, double* up_x,
+                      double* up_y, double* up_c);
 /* propagate_add (relax.cpp:656-674) and propagate_scale (relax.cpp:676-703) */
 fg_status fg_add(fg_ctx* ctx, size_t n, size_t d, const double* alw, const double* alb,
                  const double* auw, const double* aub, const double* blw, const double* blb,

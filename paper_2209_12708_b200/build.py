@@ -21,7 +21,9 @@ SOURCES = {
     "fg_kernels.cu": ["-fmad=false"],
     "fg_gemm.cu": [],
     "fg_umma.cu": [],
+    "fg_exact.cu": ["-fmad=false"],
     "fg_host.cu": [],
+    "fg_ops64.cu": [],
 }
 
 
@@ -51,6 +53,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
     return LIB
+
+
+REF_INCLUDE = os.environ.get("FAITH_REF_INCLUDE", "/root/reference/proj/include")
+COMPAT_SRC = os.path.join(HERE, "compat", "faith_compat.cpp")
+COMPAT_LIB = os.path.join(LIBDIR, "libfaith_compat.so")
+
+
+def build_compat(force: bool = False) -> str | None:
+    """The C++ drop-in layer (compat/faith_compat.cpp): the faith:: / faith::relax:: operator
+    signatures over the C ABI.  It is compiled against the reference's public headers
+    (proj/include/faith/*.hpp), so it is (re)built only where those headers exist; the built
+    library travels with the repo like libfaith_gpu.so."""
+    if not os.path.isdir(REF_INCLUDE):
+        return COMPAT_LIB if os.path.exists(COMPAT_LIB) else None
+    build(force=force)
+    if force or not os.path.exists(COMPAT_LIB) or os.path.getmtime(COMPAT_LIB) < max(
+            os.path.getmtime(COMPAT_SRC), os.path.getmtime(LIB)):
+        _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + REF_INCLUDE,
+              "-I" + os.path.join(ROOT, "include"), COMPAT_SRC, "-o", COMPAT_LIB, "-L" + LIBDIR, "-lfaith_gpu",
+              "-Wl,-rpath,$ORIGIN"])
+    return COMPAT_LIB
 
 
 if __name__ == "__main__":

@@ -26,32 +26,16 @@
 #include <vector>
 
 #include "../../include/faith_gpu.h"
+#include "fg_host.h"
 #include "fg_internal.cuh"
 
 using namespace fg;
-
-struct fg_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  std::string err;
-  uint64_t launches = 0;
-};
+using fgh::DBuf;
+using fgh::fail;
 
 namespace {
 
-const char* kVersion = "faith-b200 0.1 (sm_100a)";
-
-fg_status fail(fg_ctx* ctx, fg_status code, const std::string& msg) {
-  if (ctx) ctx->err = msg;
-  return code;
-}
-
-#define CK(expr)                                                                       \
-  do {                                                                                 \
-    cudaError_t e_ = (expr);                                                           \
-    if (e_ != cudaSuccess)                                                             \
-      return fail(ctx, FG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));  \
-  } while (0)
+const char* kVersion = "faith-b200 0.2 (sm_100a)";
 
 // Optional per-launch-site profiler (fg_profile_pass): events around each LAUNCH.
 struct Profiler {
@@ -101,41 +85,6 @@ struct ProfScope {
     if (e_ != cudaSuccess)                                               \
       return fail(ctx, FG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
-
-// RAII device allocation
-struct DBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-  DBuf() = default;
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
-  DBuf& operator=(DBuf&& o) noexcept {
-    if (this != &o) {
-      reset();
-      p = o.p;
-      bytes = o.bytes;
-      o.p = nullptr;
-      o.bytes = 0;
-    }
-    return *this;
-  }
-  ~DBuf() { reset(); }
-  void reset() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
-  }
-  cudaError_t alloc(size_t b) {
-    reset();
-    bytes = b ? b : 16;
-    return cudaMalloc(&p, bytes);
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
 
 inline int round4(size_t d) { return (int)((d + 3) / 4 * 4); }
 
@@ -416,6 +365,7 @@ fg_status fg_concretize(fg_ctx* ctx, size_t n, size_t d, const double* lw, const
                         double* hi) {
   if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
   cudaSetDevice(ctx->device);
+  if (ctx->precision == FG_PRECISION_F64) return fgh::x64_concretize(ctx, n, d, lw, lb, uw, ub, norm, eps, lo, hi);
   OpBounds x;
   fg_status s = op_upload(ctx, x, (long long)n, (int)d, lw, lb, uw, ub);
   if (s) return s;
@@ -438,6 +388,8 @@ fg_status fg_affine(fg_ctx* ctx, size_t rows, size_t c, size_t o, size_t d, cons
                     const double* bias, double* ylw, double* ylb, double* yuw, double* yub) {
   cudaSetDevice(ctx->device);
   if (rows == 0 || c == 0 || o == 0) return fail(ctx, FG_EINVAL, "propagate_affine: empty shape");
+  if (ctx->precision == FG_PRECISION_F64)
+    return fgh::x64_affine(ctx, rows, c, o, d, xlw, xlb, xuw, xub, w, bias, ylw, ylb, yuw, yub);
   OpBounds x, y;
   fg_status s = op_upload(ctx, x, (long long)(rows * c), (int)d, xlw, xlb, xuw, xub);
   if (s) return s;
@@ -484,6 +436,8 @@ fg_status fg_compose(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const d
                      const double* b_low, const double* a_up, const double* b_up, double* ylw,
                      double* ylb, double* yuw, double* yub) {
   cudaSetDevice(ctx->device);
+  if (ctx->precision == FG_PRECISION_F64)
+    return fgh::x64_compose(ctx, n, d, xlw, xlb, xuw, xub, a_low, b_low, a_up, b_up, ylw, ylb, yuw, yub);
   OpBounds x, y;
   fg_status s = op_upload(ctx, x, (long long)n, (int)d, xlw, xlb, xuw, xub);
   if (s) return s;
@@ -507,6 +461,9 @@ fg_status fg_elementwise_verify(fg_ctx* ctx, int kind, size_t n, size_t d, const
                                 double* yub) {
   if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
   cudaSetDevice(ctx->device);
+  if (kind < 0 || kind > FG_RELAX_RECIP) return fail(ctx, FG_EINVAL, "elementwise_verify: unknown kind");
+  if (ctx->precision == FG_PRECISION_F64)
+    return fgh::x64_elementwise_verify(ctx, kind, n, d, xlw, xlb, xuw, xub, norm, eps, ylw, ylb, yuw, yub);
   OpBounds x;
   fg_status s = op_upload(ctx, x, (long long)n, (int)d, xlw, xlb, xuw, xub);
   if (s) return s;
@@ -527,6 +484,9 @@ fg_status fg_dot(fg_ctx* ctx, int layout, size_t len, size_t embed, size_t heads
   if (heads == 0 || embed % heads != 0)
     return fail(ctx, FG_EINVAL, "propagate_dot_product: feature dim not divisible by heads");
   cudaSetDevice(ctx->device);
+  if (ctx->precision == FG_PRECISION_F64)
+    return fgh::x64_dot(ctx, layout, 1, len, embed, heads, d, alw, alb, auw, aub, blw, blb, buw, bub, norm, eps,
+                        ylw, ylb, yuw, yub);
   const int L = (int)len, E = (int)embed, H = (int)heads, hd = E / H;
   const bool sim = layout == FG_DOT_SIMILARITY;
   long long na = sim ? (long long)L * E : (long long)H * L * L;
@@ -570,6 +530,8 @@ fg_status fg_softmax(fg_ctx* ctx, size_t rows, size_t n, size_t d, const double*
                      double eps, double* ylw, double* ylb, double* yuw, double* yub) {
   if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
   cudaSetDevice(ctx->device);
+  if (ctx->precision == FG_PRECISION_F64)
+    return fgh::x64_softmax(ctx, rows, n, 1, d, xlw, xlb, xuw, xub, norm, eps, ylw, ylb, yuw, yub);
   OpBounds x;
   long long N = (long long)(rows * n);
   fg_status s = op_upload(ctx, x, N, (int)d, xlw, xlb, xuw, xub);
@@ -592,6 +554,8 @@ fg_status fg_add(fg_ctx* ctx, size_t n, size_t d, const double* alw, const doubl
                  const double* buw, const double* bub, double* ylw, double* ylb, double* yuw,
                  double* yub) {
   cudaSetDevice(ctx->device);
+  if (ctx->precision == FG_PRECISION_F64)
+    return fgh::x64_add(ctx, n, d, alw, alb, auw, aub, blw, blb, buw, bub, ylw, ylb, yuw, yub);
   OpBounds a, b, y;
   fg_status s = op_upload(ctx, a, (long long)n, (int)d, alw, alb, auw, aub);
   if (s) return s;
@@ -607,6 +571,7 @@ fg_status fg_scale(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const dou
                    const double* xuw, const double* xub, double sv, double* ylw, double* ylb,
                    double* yuw, double* yub) {
   cudaSetDevice(ctx->device);
+  if (ctx->precision == FG_PRECISION_F64) return fgh::x64_scale(ctx, n, d, xlw, xlb, xuw, xub, sv, ylw, ylb, yuw, yub);
   OpBounds x, y;
   fg_status s = op_upload(ctx, x, (long long)n, (int)d, xlw, xlb, xuw, xub);
   if (s) return s;
@@ -614,6 +579,39 @@ fg_status fg_scale(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const dou
   LAUNCH(launch_scale(x.c(), x.cr(), x.lb.as<double>(), x.ub.as<double>(), sv, y.c(), y.cr(),
                       y.lb.as<double>(), y.ub.as<double>(), (long long)n, x.Dp, ctx->stream));
   return op_download(ctx, y, ylw, ylb, yuw, yub);
+}
+
+fg_status fg_dot_batched(fg_ctx* ctx, int layout, size_t batch, size_t len, size_t embed, size_t heads,
+                         size_t d, const double* alw, const double* alb, const double* auw, const double* aub,
+                         const double* blw, const double* blb, const double* buw, const double* bub, int norm,
+                         double eps, double* ylw, double* ylb, double* yuw, double* yub) {
+  if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  if (heads == 0 || embed % heads != 0)
+    return fail(ctx, FG_EINVAL, "propagate_dot_product: feature dim not divisible by heads");
+  cudaSetDevice(ctx->device);
+  if (ctx->precision == FG_PRECISION_F64)
+    return fgh::x64_dot(ctx, layout, batch, len, embed, heads, d, alw, alb, auw, aub, blw, blb, buw, bub, norm,
+                        eps, ylw, ylb, yuw, yub);
+  const bool sim = layout == FG_DOT_SIMILARITY;
+  const size_t na = sim ? len * embed : heads * len * len, nb = len * embed;
+  const size_t ny = sim ? heads * len * len : len * embed;
+  for (size_t bi = 0; bi < batch; ++bi) {  // batch slices are independent problems
+    fg_status s = fg_dot(ctx, layout, len, embed, heads, d, alw + bi * na * d, alb + bi * na, auw + bi * na * d,
+                         aub + bi * na, blw + bi * nb * d, blb + bi * nb, buw + bi * nb * d, bub + bi * nb, norm,
+                         eps, ylw + bi * ny * d, ylb + bi * ny, yuw + bi * ny * d, yub + bi * ny);
+    if (s) return s;
+  }
+  return FG_OK;
+}
+
+fg_status fg_softmax_axis(fg_ctx* ctx, size_t outer, size_t n, size_t inner, size_t d, const double* xlw,
+                          const double* xlb, const double* xuw, const double* xub, int norm, double eps,
+                          double* ylw, double* ylb, double* yuw, double* yub) {
+  if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  cudaSetDevice(ctx->device);
+  if (inner == 1 && ctx->precision == FG_PRECISION_F32)
+    return fg_softmax(ctx, outer, n, d, xlw, xlb, xuw, xub, norm, eps, ylw, ylb, yuw, yub);
+  return fgh::x64_softmax(ctx, outer, n, inner, d, xlw, xlb, xuw, xub, norm, eps, ylw, ylb, yuw, yub);
 }
 
 }  // extern "C"

@@ -1,0 +1,98 @@
+// fg_host.h -- host-side internals shared by the C-ABI translation units (fg_host.cu,
+// fg_ops64.cu): the context object, error plumbing and an RAII device buffer.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/faith_gpu.h"
+
+struct fg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+  int precision = FG_PRECISION_F32;  // operator-level arithmetic (fg_ctx_set_precision)
+};
+
+namespace fgh {
+
+inline fg_status fail(fg_ctx* ctx, fg_status code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+// RAII device allocation
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t alloc(size_t b) {
+    reset();
+    bytes = b ? b : 16;
+    return cudaMalloc(&p, bytes);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+// f64 operator level of the exact precision mode (fg_ops64.cu); same contracts as the
+// extern "C" entries that dispatch to them.
+fg_status x64_concretize(fg_ctx* ctx, size_t n, size_t d, const double* lw, const double* lb, const double* uw,
+                         const double* ub, int norm, double eps, double* lo, double* hi);
+fg_status x64_affine(fg_ctx* ctx, size_t rows, size_t c, size_t o, size_t d, const double* xlw, const double* xlb,
+                     const double* xuw, const double* xub, const double* w, const double* bias, double* ylw,
+                     double* ylb, double* yuw, double* yub);
+fg_status x64_compose(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const double* xlb, const double* xuw,
+                      const double* xub, const double* a_low, const double* b_low, const double* a_up,
+                      const double* b_up, double* ylw, double* ylb, double* yuw, double* yub);
+fg_status x64_elementwise_verify(fg_ctx* ctx, int kind, size_t n, size_t d, const double* xlw, const double* xlb,
+                                 const double* xuw, const double* xub, int norm, double eps, double* ylw,
+                                 double* ylb, double* yuw, double* yub);
+fg_status x64_dot(fg_ctx* ctx, int layout, size_t batch, size_t len, size_t embed, size_t heads, size_t d,
+                  const double* alw, const double* alb, const double* auw, const double* aub, const double* blw,
+                  const double* blb, const double* buw, const double* bub, int norm, double eps, double* ylw,
+                  double* ylb, double* yuw, double* yub);
+fg_status x64_softmax(fg_ctx* ctx, size_t outer, size_t n, size_t inner, size_t d, const double* xlw,
+                      const double* xlb, const double* xuw, const double* xub, int norm, double eps, double* ylw,
+                      double* ylb, double* yuw, double* yub);
+fg_status x64_add(fg_ctx* ctx, size_t n, size_t d, const double* alw, const double* alb, const double* auw,
+                  const double* aub, const double* blw, const double* blb, const double* buw, const double* bub,
+                  double* ylw, double* ylb, double* yuw, double* yub);
+fg_status x64_scale(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const double* xlb, const double* xuw,
+                    const double* xub, double s, double* ylw, double* ylb, double* yuw, double* yub);
+
+}  // namespace fgh
+
+#define CK(expr)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fgh::fail(ctx, FG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));   \
+  } while (0)

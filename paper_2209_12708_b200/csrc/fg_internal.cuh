@@ -183,4 +183,35 @@ int launch_sim_bias(const NView& q, const NView& k, const NView& out, int S, int
 int launch_wv_bias(const NView& p, const NView& v, const NView& out, int S, int H, int L, int hd,
                    cudaStream_t st);
 
+// ---- exact f64 operator kernels (fg_exact.cu; FG_PRECISION_F64 mode of the operator ABI) ----
+// Reference layout: lw/uw [n, d] row-major f64, lb/ub [n] f64; reference operation order.
+struct XDotArgs {
+  const double *alw, *alb, *auw, *aub, *alo;        // operand a (+ concretized lo)
+  const double *blw, *blb, *buw, *bub, *blo, *bhi;  // operand b (+ concretized lo, hi)
+  double *ylw, *ylb, *yuw, *yub;
+  int layout;  // 0 = pairwise similarity, 1 = weighted values
+  long long batch;
+  int len, e, heads, d;
+};
+int launch_x_affine(const double* xlw, const double* xlb, const double* xuw, const double* xub, const double* w,
+                    const double* bias, double* ylw, double* ylb, double* yuw, double* yub, long long rows, int c,
+                    int o, int d, cudaStream_t st);
+int launch_x_concretize(const double* lw, const double* lb, const double* uw, const double* ub, long long n,
+                        int d, int norm, double eps, double* lo, double* hi, cudaStream_t st);
+int launch_x_compose(const double* xlw, const double* xlb, const double* xuw, const double* xub,
+                     const double* a_low, const double* b_low, const double* a_up, const double* b_up, double* ylw,
+                     double* ylb, double* yuw, double* yub, long long n, int d, cudaStream_t st);
+int launch_x_dot(const XDotArgs& a, cudaStream_t st);
+// x = operand a [outer, n, inner], r = operand b [outer, 1, inner]
+int launch_x_mul_broadcast(const XDotArgs& a, long long outer, int n, long long inner, cudaStream_t st);
+int launch_x_sum_axis(const double* xlw, const double* xlb, const double* xuw, const double* xub, double* ylw,
+                      double* ylb, double* yuw, double* yub, long long outer, int n, long long inner, int d,
+                      cudaStream_t st);
+int launch_x_add(const double* a, const double* b, double* y, long long n, cudaStream_t st);
+int launch_x_scale(const double* xl, const double* xu, double s, double* yl, double* yu, long long n,
+                   cudaStream_t st);
+// out6 = lo_x, lo_y, lo_c, up_x, up_y, up_c (each n); status <- kCodeInval if lo > hi
+int launch_x_bilinear(const double* xlo, const double* xhi, const double* ylo, const double* yhi, double* out6,
+                      long long n, int* status, cudaStream_t st);
+
 }  // namespace fg

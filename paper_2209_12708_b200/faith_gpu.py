@@ -136,6 +136,13 @@ def load_library():
     L.fg_gen_positions.argtypes = [C.c_uint64, C.c_int, C.c_int, _ip]
     L.fg_profile_pass.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_char_p, _dp, _ip, _ip]
     L.fg_selftest_affine.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _dp, _dp, _dp, _dp]
+    L.fg_ctx_set_precision.argtypes = [vp, C.c_int]
+    L.fg_ctx_precision.argtypes = [vp]
+    L.fg_dot_batched.argtypes = [vp, C.c_int, sz, sz, sz, sz, sz] + [_dp] * 8 + [C.c_int, C.c_double] + [_dp] * 4
+    L.fg_softmax_axis.argtypes = [vp, sz, sz, sz, sz] + [_dp] * 4 + [C.c_int, C.c_double] + [_dp] * 4
+    L.fg_sum_axis.argtypes = [vp, sz, sz, sz, sz] + [_dp] * 8
+    L.fg_mul_broadcast.argtypes = [vp, sz, sz, sz, sz] + [_dp] * 8 + [C.c_int, C.c_double] + [_dp] * 4
+    L.fg_bilinear.argtypes = [vp, sz] + [_dp] * 10
     _lib = L
     return L
 
@@ -154,6 +161,9 @@ def _f64(a) -> np.ndarray:
 
 def _bounds(b) -> LinearBounds:
     return LinearBounds(*(_f64(t) for t in b))
+
+
+PRECISION = {"f32": 0, "f64": 1}
 
 
 class Context:
@@ -178,6 +188,15 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    @property
+    def precision(self) -> str:
+        return {0: "f32", 1: "f64"}[int(self.lib.fg_ctx_precision(self.handle))]
+
+    def set_precision(self, precision: str):
+        """Operator-level arithmetic: "f32" (f32 Λ planes + f64 O(N) state, the fused pass's
+        arithmetic) or "f64" (reference operation order, bit-identical arithmetic operators)."""
+        self._check(self.lib.fg_ctx_set_precision(self.handle, PRECISION[precision]), "set_precision")
 
     @property
     def kernel_launches(self) -> int:
@@ -299,6 +318,70 @@ class Context:
         self._check(self.lib.fg_softmax(self.handle, rows, n, d, *map(_d, x), NORM[norm], eps, *map(_d, y)),
                     "propagate_softmax")
         return LinearBounds(*y)
+
+    def propagate_dot_product_batched(self, a, b, norm: str, eps: float, layout: str,
+                                      num_heads: int = 1) -> LinearBounds:
+        """propagate_dot_product with a leading batch axis B (relax.cpp:573-654)."""
+        a, b = _bounds(a), _bounds(b)
+        d = a.lw.shape[-1]
+        if b.lw.shape[-1] != d:
+            raise InvalidArgument("propagate_dot_product: perturbation dims differ")
+        batch, length, embed = b.lb.shape
+        yshape = (batch, num_heads, length, length) if layout == "similarity" else (batch, length, embed)
+        y = [np.zeros(yshape + (d,)), np.zeros(yshape), np.zeros(yshape + (d,)), np.zeros(yshape)]
+        self._check(self.lib.fg_dot_batched(self.handle, DOT[layout], batch, length, embed, num_heads, d,
+                                            *map(_d, a), *map(_d, b), NORM[norm], eps, *map(_d, y)),
+                    "propagate_dot_product")
+        return LinearBounds(*y)
+
+    @staticmethod
+    def _axis_split(shape, axis):
+        n = shape[axis]
+        inner = int(np.prod(shape[axis + 1:], dtype=np.int64))
+        outer = int(np.prod(shape[:axis], dtype=np.int64))
+        return outer, n, inner
+
+    def propagate_softmax_axis(self, x, axis: int, norm: str, eps: float) -> LinearBounds:
+        """faith::relax::propagate_softmax along `axis` of the neuron shape (relax.cpp:777-790)."""
+        x = _bounds(x)
+        outer, n, inner = self._axis_split(x.lb.shape, axis)
+        d = x.lw.shape[-1]
+        y = [np.zeros(x.lw.shape), np.zeros(x.lb.shape), np.zeros(x.lw.shape), np.zeros(x.lb.shape)]
+        self._check(self.lib.fg_softmax_axis(self.handle, outer, n, inner, d, *map(_d, x), NORM[norm], eps,
+                                             *map(_d, y)), "propagate_softmax")
+        return LinearBounds(*y)
+
+    def propagate_sum_axis(self, x, axis: int) -> LinearBounds:
+        """faith::relax::propagate_sum_axis (relax.cpp:705-742); the reduced axis keeps extent 1."""
+        x = _bounds(x)
+        outer, n, inner = self._axis_split(x.lb.shape, axis)
+        d = x.lw.shape[-1]
+        oshape = x.lb.shape[:axis] + (1,) + x.lb.shape[axis + 1:]
+        y = [np.zeros(oshape + (d,)), np.zeros(oshape), np.zeros(oshape + (d,)), np.zeros(oshape)]
+        self._check(self.lib.fg_sum_axis(self.handle, outer, n, inner, d, *map(_d, x), *map(_d, y)),
+                    "propagate_sum_axis")
+        return LinearBounds(*y)
+
+    def propagate_mul_broadcast(self, x, r, axis: int, norm: str, eps: float) -> LinearBounds:
+        """faith::relax::propagate_mul_broadcast (relax.cpp:744-775)."""
+        x, r = _bounds(x), _bounds(r)
+        outer, n, inner = self._axis_split(x.lb.shape, axis)
+        if r.lb.ndim != x.lb.ndim or r.lb.shape[axis] != 1:
+            raise InvalidArgument("propagate_mul_broadcast: operand shapes incompatible")
+        d = x.lw.shape[-1]
+        y = [np.zeros(x.lw.shape), np.zeros(x.lb.shape), np.zeros(x.lw.shape), np.zeros(x.lb.shape)]
+        self._check(self.lib.fg_mul_broadcast(self.handle, outer, n, inner, d, *map(_d, x), *map(_d, r),
+                                              NORM[norm], eps, *map(_d, y)), "propagate_mul_broadcast")
+        return LinearBounds(*y)
+
+    def relax_bilinear(self, xlo, xhi, ylo, yhi) -> tuple:
+        """faith::relax::relax_bilinear (relax.cpp:499-523) -> (lo_x, lo_y, lo_c, up_x, up_y, up_c)."""
+        xlo, xhi, ylo, yhi = (_f64(t) for t in (xlo, xhi, ylo, yhi))
+        shape, n = xlo.shape, xlo.size
+        out = [np.zeros(n) for _ in range(6)]
+        self._check(self.lib.fg_bilinear(self.handle, n, _d(xlo.ravel()), _d(xhi.ravel()), _d(ylo.ravel()),
+                                         _d(yhi.ravel()), *map(_d, out)), "relax_bilinear")
+        return tuple(o.reshape(shape) for o in out)
 
     def propagate_add(self, a, b) -> LinearBounds:
         a, b = _bounds(a), _bounds(b)
