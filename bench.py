@@ -230,6 +230,10 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="sentences per step per GPU (default: per config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--shard", default="sentences", choices=["sentences", "columns"],
+                    help="sentences: independent sentences per GPU (weak scaling, no collective); columns: "
+                         "perturbation columns of every sentence split over the GPUs, concretization partials "
+                         "all-reduced with NCCL inside the pass (strong scaling; SURVEY 8(e) c5)")
     args = ap.parse_args()
     w = CONFIGS[args.config]
     if args.warmup < 3 and args.impl == "ours":
@@ -249,10 +253,14 @@ def main():
     cfg = F.ModelConfig(w.layers, w.heads, w.embed, w.ffn, w.length, w.classes, w.activation)
     ctx = F.Context(local)
     model = F.Model(ctx, cfg, F.gen_synthetic(cfg, w.model_seed))
+    columns = args.shard == "columns"
+    if columns:
+        D.shard_model_columns(model, dist)
 
     def batch(step):
-        # globally unique sentence ids: rank-major blocks, warm-up steps first (no data-path collective)
-        ids = D.sentence_block(rank, step, args.steps + args.warmup, B)
+        # globally unique sentence ids: rank-major blocks, warm-up steps first (no data-path collective);
+        # column sharding: every rank works on the same sentences (its own slice of their columns)
+        ids = D.sentence_block(0 if columns else rank, step, args.steps + args.warmup, B)
         xs = np.stack([F.gen_input(cfg, w.input_seed(i)) for i in ids])
         ps = np.stack([F.gen_positions(w.position_seed(i), w.length, w.words) for i in ids])
         return xs, ps
@@ -287,7 +295,7 @@ def main():
         barrier()
         wall = time.perf_counter() - t0
     dev_ms_max, wall_max = D.max_over_ranks([dev_ms, wall], dist, device="cuda")
-    sentences = B * args.steps * world
+    sentences = B * args.steps * (1 if columns else world)
     value = sentences / (dev_ms_max / 1e3)
     e2e = sentences / wall_max
     ms_pass_batched = statistics.mean(pass_ms)
@@ -296,11 +304,13 @@ def main():
     line = {
         "metric": "certified sentences/sec (eps binary search)", "value": value, "unit": "sentences/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+        "higher_is_better": True, "scaling": "strong" if columns else "weak", "vs_baseline": None,
+        "dtype": "f32+f64",
         "data": f"synthetic: gen_synthetic(seed {w.model_seed}) weights, gen_synthetic_input(2000+s), "
                 f"{w.words} perturbed word(s) at Rng(3000+s) positions",
-        "config": {**w.as_dict(), "global_batch": B * world, "sentences_per_step_per_gpu": B,
-                   "parallelism": f"sentence-sharded dp{world}",
+        "config": {**w.as_dict(), "global_batch": B * (1 if columns else world), "sentences_per_step_per_gpu": B,
+                   "parallelism": (f"column-sharded cp{world} (NCCL all-reduce of concretization partials)"
+                                   if columns else f"sentence-sharded dp{world}"),
                    "l2_flush": "not needed: inputs larger than L2 (Λ working set "
                                f"{B * 0.45:.1f} GB per GPU >> 126 MB L2)"},
         "ms_per_bound_pass": {"batched_pass_ms": ms_pass_batched, "per_sentence_ms": ms_pass_sentence,
@@ -312,12 +322,14 @@ def main():
         "clocks": clocks.summary(),
     }
 
-    if rank == 0 and not args.no_profile:
-        pk, pk_kind = peaks()
+    prof = None
+    if not args.no_profile and (rank == 0 or columns):  # column shards all-reduce inside the pass
         prof = model.profile_pass(w.norm, w.eps)
+    if rank == 0 and prof is not None:
+        pk, pk_kind = peaks()
         total = sum(ms for ms, _ in prof.values())
         gemm_ms, gemm_k = prof.get("affine_gemm", (0.0, 0))
-        flops = affine_flops(w) * B
+        flops = affine_flops(w) * B / (world if columns else 1)
         ach = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
         traffic = None
         try:
@@ -336,7 +348,7 @@ def main():
         mem = {}
         for site, nbytes in site_bytes(w).items():
             if site in prof and prof[site][0] > 0:
-                gbs = nbytes * B / (prof[site][0] / 1e3) / 1e9
+                gbs = nbytes * B / (world if columns else 1) / (prof[site][0] / 1e3) / 1e9
                 mem[site] = {"GB/s": gbs, "frac_hbm": gbs / pk["hbm_gbs"], "ms": prof[site][0]}
         line["kernels"] = {k: {"ms_per_pass": v[0], "launches": v[1]} for k, v in sorted(prof.items())}
         line["hbm_sites"] = mem

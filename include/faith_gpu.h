@@ -215,6 +215,34 @@ fg_status fg_maxeps(fg_model* model, int S, const double* x, const int* position
                     int norm, double eps_max, double tol, int slots, double* eps_out,
                     int* calls_out, int* predicted_out, int* status);
 
+/* ---- column sharding -------------------------------------------------
+ * The perturbation columns D = words*E of every Λ are split across `nranks` ranks (one GPU
+ * each): rank r owns columns [r*D/nranks, (r+1)*D/nranks).  Every operator of the pass is
+ * column-separable except concretization, whose partial q-norms (raw sums / sums of squares /
+ * maxima) are all-reduced across the ranks at every concretization site: Q/K/V, the four
+ * concretizations of the softmax chain, the FFN activation, the logits.  All O(N) state is
+ * replicated, so every rank takes identical envelope decisions and returns identical results.
+ * All ranks must call fg_bound_pass / fg_certify / fg_maxeps with the same arguments.
+ * D must be a multiple of 4*nranks.  fg_bound_pass_dump is not available on a sharded model. */
+#define FG_REDUCE_SUM 0
+#define FG_REDUCE_MAX 1
+/* In-place all-reduce of `count` doubles on device memory, stream-ordered on `cuda_stream`
+ * (a cudaStream_t); returns 0 on success. */
+typedef int (*fg_allreduce_fn)(void* user, double* buf, size_t count, int op, void* cuda_stream);
+fg_status fg_model_set_column_shard(fg_model* model, int rank, int nranks, fg_allreduce_fn fn, void* user,
+                                    int graph_capturable);
+/* Built-in exchange over NCCL (ncclAllReduce, loaded at run time from libnccl.so.2): rank 0
+ * creates the id, every rank passes the same 128 bytes (e.g. through torch.distributed). */
+fg_status fg_nccl_unique_id(unsigned char id[128]);
+fg_status fg_model_shard_nccl(fg_model* model, int rank, int nranks, const unsigned char id[128]);
+/* Built-in in-process exchange: `nranks` models on ONE device, driven by one host thread each
+ * (a deterministic rank-ordered reduction kernel between CUDA events); used to exercise the
+ * sharded pass on a single GPU. */
+typedef struct fg_loopback fg_loopback;
+fg_status fg_loopback_create(int nranks, fg_loopback** out);
+void fg_loopback_destroy(fg_loopback* group);
+fg_status fg_model_shard_loopback(fg_model* model, fg_loopback* group, int rank);
+
 /* Synthetic model / inputs with the reference's seeded recipe (model.cpp:87-141):
  * gen_synthetic weights U(+-0.5/sqrt(fan_in)) rounded to f32, gen_synthetic_input
  * U(-0.5, 0.5); word positions = `words` distinct Rng(seed).uniform_index(length) draws,

@@ -24,6 +24,7 @@ SOURCES = {
     "fg_exact.cu": ["-fmad=false"],
     "fg_host.cu": [],
     "fg_ops64.cu": [],
+    "fg_shard.cu": [],
 }
 
 
@@ -51,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose:
                 sys.stderr.write(r.stderr)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"])
     return LIB
 
 

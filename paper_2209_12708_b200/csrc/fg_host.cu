@@ -642,6 +642,9 @@ struct Workspace {
   DBuf pooled, pooled_b, coef;
   DBuf eps, status, logits, slot_map, x_all, pos_all;
   DBuf dump_lo, dump_hi;
+  // column-sharded pass: concretization partials and the softmax chain's phase buffers
+  int col0 = 0;
+  DBuf part, sm_ex, sm_sig, sm_rows, head_part;
   double* h_eps = nullptr;  // pinned
   int* h_slot = nullptr;
   double* h_logits = nullptr;
@@ -685,6 +688,7 @@ struct fg_model {
   DBuf wc64, bc64;
   Workspace ws;
   fg_run_stats stats{};
+  fgh::ShardState shard;  // column sharding of the perturbation dimension (fg_model_set_column_shard)
   // offsets of the layers in params (gen_synthetic order)
   size_t layer_off(int l) const {
     size_t e = cfg.embed, f = cfg.ffn;
@@ -698,8 +702,12 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot) {
   fg_ctx* ctx = m->ctx;
   Workspace& w = m->ws;
   const fg_config& c = m->cfg;
-  const int D = W * c.embed;
+  const int Dg = W * c.embed;  // global perturbation columns
+  const int nr = m->shard.active() ? m->shard.nranks : 1;
+  if (Dg % (4 * nr) != 0) return fail(ctx, FG_EINVAL, "column shard: words*embed must be a multiple of 4*nranks");
+  const int D = Dg / nr;  // columns of this rank
   if (w.S == S && w.D == D && w.W == W && w.Ntot >= Ntot) return FG_OK;
+  w.col0 = (m->shard.active() ? m->shard.rank : 0) * D;
   w.release_host();
   const long long L = c.length, E = c.embed, F = c.ffn, H = c.heads, hd = E / H;
   const long long nX = S * L * E, nQKV = S * L * 3 * E, nF = S * L * F, nSC = S * H * L * L;
@@ -730,6 +738,14 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot) {
   size_t dmax = std::max({(size_t)nQKV, (size_t)nF, (size_t)nSC});
   CK(w.dump_lo.alloc(sizeof(double) * dmax));
   CK(w.dump_hi.alloc(sizeof(double) * dmax));
+  if (m->shard.active()) {
+    const long long rows = (long long)S * H * L;
+    CK(w.part.alloc(sizeof(double) * 2 * std::max({nQKV, nF, nSC})));
+    CK(w.sm_ex.alloc(sizeof(double) * 5 * nSC));
+    CK(w.sm_sig.alloc(sizeof(double) * 2 * rows * D));
+    CK(w.sm_rows.alloc(sizeof(double) * 14 * rows));  // p_row, p_row2, sb (2 each), rb (6)
+    CK(w.head_part.alloc(sizeof(double) * 4 * S * c.classes));
+  }
   CK(cudaMallocHost(&w.h_eps, sizeof(double) * S));
   CK(cudaMallocHost(&w.h_slot, sizeof(int) * S));
   CK(cudaMallocHost(&w.h_logits, sizeof(double) * 2 * S * c.classes));
@@ -799,6 +815,35 @@ struct Dumper {
   }
 };
 
+// All-reduce of concretization partials across the column shards (stream-ordered).
+fg_status shard_allreduce(fg_model* m, double* buf, size_t count, int norm) {
+  fg_ctx* ctx = m->ctx;
+  if (m->shard.nranks <= 1 && !m->shard.fn) return FG_OK;
+  const int op = reduce_op_for_norm(norm) ? FG_REDUCE_MAX : FG_REDUCE_SUM;
+  if (m->shard.fn(m->shard.user, buf, count, op, (void*)ctx->stream) != 0)
+    return fail(ctx, FG_ECUDA, "column shard: all-reduce failed");
+  ++ctx->launches;
+  return FG_OK;
+}
+
+// Concretization of `nrows` rows of a Λ: fused kernel when unsharded; partial norms ->
+// all-reduce -> finish when the perturbation columns are sharded.
+fg_status concretize_site(fg_model* m, const float* lam, long long cr, const double* lb, const double* ub,
+                          long long rows_per_s, long long nrows, int D, int norm, const double* eps, double* lo,
+                          double* hi) {
+  fg_ctx* ctx = m->ctx;
+  cudaStream_t st = ctx->stream;
+  if (!m->shard.active()) {
+    LAUNCH(launch_concretize(lam, cr, lb, ub, rows_per_s, nrows, D, norm, eps, lo, hi, st));
+    return FG_OK;
+  }
+  double* part = m->ws.part.as<double>();
+  LAUNCH(launch_partial_norms(lam, cr, nrows, D, norm, part, st));
+  if (fg_status s = shard_allreduce(m, part, 2 * (size_t)nrows, norm)) return s;
+  LAUNCH(launch_finish_concretize(part, lb, ub, rows_per_s, nrows, norm, eps, lo, hi, st));
+  return FG_OK;
+}
+
 // One batched bound pass over the resident slots (graph.cpp:531-673 node order).
 // Reads ws.eps / ws.slot_map; writes ws.logits / ws.status.
 fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
@@ -833,7 +878,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
   g_tag = "init";
   LAUNCH(launch_fill_int(status, kStatusClear, S, st));
   LAUNCH(launch_init_input(X, w.crX, X_lb, X_ub, w.x_all.as<double>(), w.pos_all.as<int>(),
-                           w.slot_map.as<int>(), S, L, E, w.W, st));
+                           w.slot_map.as<int>(), S, L, E, w.W, st, D, w.col0));
+  const bool sharded = m->shard.active();
   for (int l = 0; l < c.layers; ++l) {
     const DevLayer& lw = m->layers[l];
     const size_t base = (size_t)l * per_layer;
@@ -845,8 +891,9 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     LAUNCH(launch_affine_bias(X_lb, X_ub, lw.qkv.w64.as<double>(), lw.qkv.b64.as<double>(), nullptr,
                               nullptr, Q_lb, Q_ub, S, L, E, 3 * E, st));
     g_tag = "concretize";
-    LAUNCH(launch_concretize(QKV, w.crQKV, Q_lb, Q_ub, (long long)L * 3 * E, nQKV, D, norm, eps, Q_lo,
-                             Q_hi, st));
+    if (fg_status s = concretize_site(m, QKV, w.crQKV, Q_lb, Q_ub, (long long)L * 3 * E, nQKV, D, norm, eps,
+                                      Q_lo, Q_hi))
+      return s;
     if (dump) {
       for (int t = 0; t < 3; ++t)
         if (fg_status s = dump->copy(base + (size_t)t * L * E, Q_lo, Q_hi, 0, 3 * E, E, (size_t)t * E, L)) return s;
@@ -903,7 +950,21 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     }
     // softmax: exp -> sum -> recip -> mul (graph.cpp:237-240), in place
     g_tag = "softmax";
-    LAUNCH(launch_softmax(sc, S, H * L, L, D, norm, eps, status, site(l, 0), site(l, 1), st));
+    if (!sharded) {
+      LAUNCH(launch_softmax(sc, S, H * L, L, D, norm, eps, status, site(l, 0), site(l, 1), st));
+    } else {  // exp -> sum -> recip -> multiply around four all-reduces of the partial norms
+      const long long rows = (long long)S * H * L;
+      double* pr = w.sm_rows.as<double>();
+      SmShardBufs b{w.part.as<double>(), pr, pr + 2 * rows, w.sm_ex.as<double>(), w.sm_sig.as<double>(),
+                    pr + 4 * rows, pr + 6 * rows};
+      const size_t counts[4] = {2 * (size_t)nSC, 2 * (size_t)rows, 2 * (size_t)rows, 2 * (size_t)nSC};
+      double* bufs[4] = {b.p_key, b.p_row, b.p_row2, b.p_key};
+      for (int ph = 0; ph < 5; ++ph) {
+        LAUNCH(launch_sm_shard(ph, sc, S, H * L, L, D, norm, eps, status, site(l, 0), site(l, 1), b, st));
+        if (ph < 4)
+          if (fg_status s = shard_allreduce(m, bufs[ph], counts[ph], norm)) return s;
+      }
+    }
     if (dump) {
       if (fg_status s = dump->copy(base + 3ull * L * E + 3ull * H * L * L + 2ull * H * L, S_lo, S_hi,
                                    (size_t)H * L * L)) return s;
@@ -972,9 +1033,16 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     LAUNCH(launch_affine_bias(R1_lb, R1_ub, lw.w1.w64.as<double>(), lw.w1.b64.as<double>(), nullptr,
                               nullptr, F_lb, F_ub, S, L, E, F, st));
     g_tag = "act_verify";
-    LAUNCH(launch_elementwise_verify(c.activation, Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm,
-                                     eps, status, site(l, 2), dump ? F_lo : nullptr,
-                                     dump ? F_hi : nullptr, st));
+    if (!sharded) {
+      LAUNCH(launch_elementwise_verify(c.activation, Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm,
+                                       eps, status, site(l, 2), dump ? F_lo : nullptr,
+                                       dump ? F_hi : nullptr, st));
+    } else {
+      if (fg_status s = concretize_site(m, Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm, eps, F_lo, F_hi))
+        return s;
+      LAUNCH(launch_elementwise_verify(c.activation, Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm, eps,
+                                       status, site(l, 2), nullptr, nullptr, st, F_lo, F_hi));
+    }
     const size_t off_f1 = off_ctx + 3ull * L * E;
     if (dump) {
       if (fg_status s = dump->copy(base + off_f1, F_lo, F_hi, (size_t)L * F)) return s;
@@ -1003,9 +1071,18 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
   g_tag = "head";
   LAUNCH(launch_meanpool(X, w.crX, X_lb, X_ub, pc, pr, plb, pub, S, L, E, D, st));
   double* lg = w.logits.as<double>();
-  LAUNCH(launch_head(pc, pr, plb, pub, m->wc64.as<double>(), m->bc64.as<double>(), S, E, C, D, norm,
-                     eps, lg, lg + (long long)S * C, status, c.layers * 8, dump ? plo : nullptr,
-                     dump ? phi : nullptr, st));
+  if (!sharded) {
+    LAUNCH(launch_head(pc, pr, plb, pub, m->wc64.as<double>(), m->bc64.as<double>(), S, E, C, D, norm,
+                       eps, lg, lg + (long long)S * C, status, c.layers * 8, dump ? plo : nullptr,
+                       dump ? phi : nullptr, st));
+  } else {
+    double* hp = w.head_part.as<double>();
+    LAUNCH(launch_head_partial(pc, pr, plb, pub, m->wc64.as<double>(), m->bc64.as<double>(), S, E, C, D, norm, hp,
+                               hp + 2 * S * C, st));
+    if (fg_status s = shard_allreduce(m, hp, 2 * (size_t)S * C, norm)) return s;
+    LAUNCH(launch_head_finish(hp, hp + 2 * S * C, S, C, norm, eps, lg, lg + (long long)S * C, status,
+                              c.layers * 8, st));
+  }
   if (dump) {
     size_t off = (size_t)c.layers * per_layer;
     if (fg_status s = dump->copy(off, plo, phi, (size_t)E)) return s;
@@ -1029,7 +1106,7 @@ fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, floa
   CK(cudaMemcpyAsync(w.eps.p, w.h_eps, sizeof(double) * S, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(w.slot_map.p, w.h_slot, sizeof(int) * S, cudaMemcpyHostToDevice, st));
   if (ev0) CK(cudaEventRecord(ev0, st));
-  if (use_graphs()) {
+  if (use_graphs() && m->shard.capturable) {
     if (!w.graph || w.graph_norm != norm) {
       if (w.graph) cudaGraphExecDestroy(w.graph);
       w.graph = nullptr;
@@ -1173,8 +1250,10 @@ std::vector<int> predict_all(const fg_model* m, int S, const double* x) {
 int default_slots(const fg_model* m, int S, int D) {
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  size_t per = bytes_per_sentence(m->cfg, D);
+  size_t per = bytes_per_sentence(m->cfg, m->shard.active() ? D / m->shard.nranks : D);
   size_t cap = (size_t)(0.8 * (double)free_b) / std::max<size_t>(per, 1);
+  if (m->shard.active())  // every rank must batch identically: plan from total HBM, not free HBM
+    cap = (size_t)(0.6 * (double)total_b / m->shard.ranks_per_device) / std::max<size_t>(per, 1);
   if (const char* e = std::getenv("FG_SLOTS")) cap = std::min<size_t>(cap, (size_t)std::atoi(e));
   int slots = (int)std::min<size_t>({cap, (size_t)S, (size_t)64});
   int maxb = 65535 / (2 * m->cfg.length);  // GEMM batch-grid limit
@@ -1299,6 +1378,7 @@ fg_status fg_bound_pass_dump(fg_model* m, const double* x, const int* positions,
   fg_ctx* ctx = m->ctx;
   cudaSetDevice(ctx->device);
   if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  if (m->shard.active()) return fail(ctx, FG_EINVAL, "fg_bound_pass_dump: not available on a column-sharded model");
   fg_status st = ensure_workspace(m, 1, words, 1);
   if (st) return st;
   if ((st = stage_inputs(m, 1, x, positions, words))) return st;
@@ -1632,6 +1712,41 @@ fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_
   *err_simt = e1s / std::max(mx, 1e-300);
   *err_umma = umma ? e2s / std::max(mx, 1e-300) : -1.0;
   return FG_OK;
+}
+
+static fg_status set_shard(fg_model* m, fgh::ShardState sh) {
+  if (sh.nranks < 1 || sh.rank < 0 || sh.rank >= sh.nranks)
+    return fail(m->ctx, FG_EINVAL, "column shard: bad rank / nranks");
+  m->shard = std::move(sh);
+  m->ws.release_host();  // drop the captured graph; buffers are re-planned for the local columns
+  m->ws.S = 0;
+  return FG_OK;
+}
+
+fg_status fg_model_set_column_shard(fg_model* m, int rank, int nranks, fg_allreduce_fn fn, void* user,
+                                    int graph_capturable) {
+  fgh::ShardState sh;
+  sh.rank = rank;
+  sh.nranks = nranks;
+  sh.fn = fn;
+  sh.user = user;
+  sh.capturable = graph_capturable != 0;
+  if (!fn && nranks != 1) return fail(m->ctx, FG_EINVAL, "column shard: an all-reduce is required for nranks > 1");
+  return set_shard(m, std::move(sh));
+}
+
+fg_status fg_model_shard_nccl(fg_model* m, int rank, int nranks, const unsigned char id[128]) {
+  cudaSetDevice(m->ctx->device);
+  fgh::ShardState sh;
+  std::string err;
+  if (fg_status s = fgh::nccl_exchange(rank, nranks, id, sh, err)) return fail(m->ctx, s, err);
+  return set_shard(m, std::move(sh));
+}
+
+fg_status fg_model_shard_loopback(fg_model* m, fg_loopback* g, int rank) {
+  fgh::ShardState sh;
+  if (fg_status s = fgh::loopback_exchange(g, rank, sh)) return fail(m->ctx, s, "column shard: bad loopback rank");
+  return set_shard(m, std::move(sh));
 }
 
 fg_status fg_last_run_stats(const fg_model* m, fg_run_stats* out) {

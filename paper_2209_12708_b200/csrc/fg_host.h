@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <string>
 
 #include "../../include/faith_gpu.h"
@@ -18,6 +19,24 @@ struct fg_ctx {
 };
 
 namespace fgh {
+
+// Column (perturbation-dimension) sharding of a model's passes (fg_model_set_column_shard):
+// this rank owns columns [rank*D/nranks, (rank+1)*D/nranks) of every Λ; concretization
+// partials are all-reduced through `fn` (stream-ordered on the pass stream).
+struct ShardState {
+  int rank = 0, nranks = 1;
+  fg_allreduce_fn fn = nullptr;
+  void* user = nullptr;
+  bool capturable = true;       // fn may be captured into a CUDA graph (NCCL: yes)
+  int ranks_per_device = 1;     // loopback: all ranks share one device's HBM
+  std::shared_ptr<void> owned;  // communicator / loopback endpoint kept alive with the model
+  bool active() const { return fn != nullptr; }
+};
+
+// built-in exchanges (fg_shard.cu)
+fg_status nccl_exchange(int rank, int nranks, const unsigned char id[128], ShardState& out, std::string& err);
+fg_status nccl_unique_id(unsigned char id[128], std::string& err);
+fg_status loopback_exchange(fg_loopback* group, int rank, ShardState& out);
 
 inline fg_status fail(fg_ctx* ctx, fg_status code, const std::string& msg) {
   if (ctx) ctx->err = msg;

@@ -71,7 +71,8 @@ int launch_concretize(const float* lam, long long cr, const double* lb, const do
 int launch_elementwise_verify(int kind, float* lam, long long cr, double* lb, double* ub,
                               long long rows_per_s, long long nrows, int D, int norm,
                               const double* eps, int* status, int site, double* lo_out,
-                              double* hi_out, cudaStream_t st);
+                              double* hi_out, cudaStream_t st, const double* lo_in = nullptr,
+                              const double* hi_in = nullptr);
 
 // Standalone envelope / compose (operator-level API).
 int launch_relax(int kind, const double* lo, const double* hi, long long n, double* a_low,
@@ -106,7 +107,7 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
 // Word-level input binding: lb = ub = x, Λ rows of perturbed positions one-hot.
 int launch_init_input(float* lam, long long cr, double* lb, double* ub, const double* x,
                       const int* positions, const int* slot_map, int S, int L, int E, int W,
-                      cudaStream_t st);
+                      cudaStream_t st, int D = 0, int col0 = 0);
 // MeanPool (graph.cpp:628-634) -> pooled f64 planes [S, E, D] (+ lb/ub [S, E]).
 int launch_meanpool(const float* lam, long long cr, const double* lb, const double* ub,
                     double* pooled_c, double* pooled_r, double* plb, double* pub, int S, int L,
@@ -213,5 +214,29 @@ int launch_x_scale(const double* xl, const double* xu, double s, double* yl, dou
 // out6 = lo_x, lo_y, lo_c, up_x, up_y, up_c (each n); status <- kCodeInval if lo > hi
 int launch_x_bilinear(const double* xlo, const double* xhi, const double* ylo, const double* yhi, double* out6,
                       long long n, int* status, cudaStream_t st);
+
+// ---- column-sharded pass (fg_kernels.cu): partial norms / finish, softmax in 5 phases ----
+int launch_partial_norms(const float* lam, long long cr, long long nrows, int D, int norm, double* part,
+                         cudaStream_t st);
+int launch_finish_concretize(const double* part, const double* lb, const double* ub, long long rows_per_s,
+                             long long nrows, int norm, const double* eps, double* lo, double* hi, cudaStream_t st);
+int reduce_op_for_norm(int norm);  // all-reduce op of the partials: 0 SUM, 1 MAX
+struct SmShardBufs {
+  double* p_key;   // [2][nSC] per-key partial norms (exp input, later outputs)
+  double* p_row;   // [2][rows] Σ partial norms
+  double* p_row2;  // [2][rows] r partial norms
+  double* ex;      // [5][nSC] a_lo, a_up, e_lb, e_ub, e_lo
+  double* sig;     // [rows][2][D] Σ rows, then r rows
+  double* sb;      // [2][rows] Σ_j e_lb, Σ_j e_ub
+  double* rb;      // [6][rows] r_al, r_au, r_lb, r_ub, r_lo, r_hi
+};
+// phase 0: key partials -> (all-reduce p_key) -> 1 -> (p_row) -> 2 -> (p_row2) -> 3 -> (p_key) -> 4
+int launch_sm_shard(int phase, const NView& sc, int S, int rows_per_s, int n, int D, int norm, const double* eps,
+                    int* status, int site_exp, int site_recip, SmShardBufs b, cudaStream_t st);
+int launch_head_partial(const double* pc, const double* pr, const double* plb, const double* pub, const double* wc,
+                        const double* bc, int S, int E, int C, int D, int norm, double* part, double* bias,
+                        cudaStream_t st);
+int launch_head_finish(const double* part, const double* bias, int S, int C, int norm, const double* eps,
+                       double* out_lo, double* out_hi, int* status, int site, cudaStream_t st);
 
 }  // namespace fg

@@ -304,21 +304,28 @@ template <int Q>
 __global__ void __launch_bounds__(256) elementwise_verify_kernel(
     int kind, float* __restrict__ lam, long long cr, double* __restrict__ lb, double* __restrict__ ub,
     long long rows_per_s, long long nrows, int D, const double* __restrict__ eps,
-    int* __restrict__ status, int site, double* __restrict__ lo_out, double* __restrict__ hi_out) {
+    int* __restrict__ status, int site, double* __restrict__ lo_out, double* __restrict__ hi_out,
+    const double* __restrict__ lo_in, const double* __restrict__ hi_in) {
   long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
   int lane = threadIdx.x & (kWarp - 1);
   if (row >= nrows) return;
   float* c = lam + row * D;
   float* r = c + cr;
-  NormAcc<Q> acc;
-  for (int d = lane * 4; d < D; d += 4 * kWarp)
-    acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
-  acc.warp_reduce();
   long long s = row / rows_per_s;
-  double e = eps[s];
   double xlb = lb[row], xub = ub[row];
-  double lo = xlb - e * acc.fin(acc.l);
-  double hi = xub + e * acc.fin(acc.u);
+  double lo, hi;
+  if (lo_in) {  // concretized elsewhere (column-sharded pass: norms all-reduced across ranks)
+    lo = lo_in[row];
+    hi = hi_in[row];
+  } else {
+    NormAcc<Q> acc;
+    for (int d = lane * 4; d < D; d += 4 * kWarp)
+      acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
+    acc.warp_reduce();
+    double e = eps[s];
+    lo = xlb - e * acc.fin(acc.l);
+    hi = xub + e * acc.fin(acc.u);
+  }
   Lines ln;
   int code = envelope(kind, lo, hi, ln, lane, kind == RELAX_SILU ? kWarp : 1);
   if (lane == 0) {
@@ -1427,12 +1434,11 @@ __global__ void __launch_bounds__(kSmThreads) softmax_kernel(NView sc, int rows_
 // W perturbed positions are one-hot into columns w*E + e, all other rows zero.
 __global__ void init_input_kernel(float* lam, long long cr, double* lb, double* ub, const double* x,
                                   const int* positions, const int* slot_map, int S, int L, int E,
-                                  int W) {
+                                  int W, int D, int col0) {
   long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
   int lane = threadIdx.x & (kWarp - 1);
   long long nrows = (long long)S * L * E;
   if (row >= nrows) return;
-  int D = W * E;
   int e = (int)(row % E);
   int tok = (int)((row / E) % L);
   int s = (int)(row / ((long long)L * E));
@@ -1441,7 +1447,7 @@ __global__ void init_input_kernel(float* lam, long long cr, double* lb, double* 
   float* r = c + cr;
   int hot = -1;
   for (int w = 0; w < W; ++w)
-    if (positions[src * W + w] == tok) hot = w * E + e;
+    if (positions[src * W + w] == tok) hot = w * E + e - col0;  // local column of this shard
   for (int d = lane * 4; d < D; d += 4 * kWarp) {
     float v[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -1707,12 +1713,12 @@ int launch_concretize(const float* lam, long long cr, const double* lb, const do
 int launch_elementwise_verify(int kind, float* lam, long long cr, double* lb, double* ub,
                               long long rows_per_s, long long nrows, int D, int norm,
                               const double* eps, int* status, int site, double* lo_out,
-                              double* hi_out, cudaStream_t st) {
+                              double* hi_out, cudaStream_t st, const double* lo_in, const double* hi_in) {
   if (nrows <= 0) return 0;
   dim3 grid(blocks_for(nrows, 8)), block(256);
   DISPATCH_Q(dual_norm(norm), elementwise_verify_kernel,
              <<<grid, block, 0, st>>>(kind, lam, cr, lb, ub, rows_per_s, nrows, D, eps, status,
-                                      site, lo_out, hi_out));
+                                      site, lo_out, hi_out, lo_in, hi_in));
   return 1;
 }
 
@@ -1911,10 +1917,11 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
 
 int launch_init_input(float* lam, long long cr, double* lb, double* ub, const double* x,
                       const int* positions, const int* slot_map, int S, int L, int E, int W,
-                      cudaStream_t st) {
+                      cudaStream_t st, int D, int col0) {
   long long nrows = (long long)S * L * E;
+  if (D <= 0) D = W * E;
   init_input_kernel<<<blocks_for(nrows, 8), 256, 0, st>>>(lam, cr, lb, ub, x, positions, slot_map, S,
-                                                          L, E, W);
+                                                          L, E, W, D, col0);
   return 1;
 }
 
@@ -2006,6 +2013,363 @@ int launch_wv_bias(const NView& p, const NView& v, const NView& out, int S, int 
 
 int launch_fill_int(int* p, int v, long long n, cudaStream_t st) {
   fill_int_kernel<<<blocks_for(n, 256), 256, 0, st>>>(p, v, n);
+  return 1;
+}
+
+// ===========================================================================
+// Column-sharded pass: rank r owns perturbation columns [col0, col0 + D)
+// of every Λ.  Every column-separable op is unchanged; each concretization becomes
+//   local partial q-norm  ->  all-reduce across ranks (SUM; MAX for the l-inf dual)  ->  finish,
+// "partial" meaning the raw accumulation before the l2 square root.  The softmax chain, which
+// holds four dependent concretizations, runs as five kernels around four all-reduces.
+// ===========================================================================
+namespace {
+
+// raw q-norm partials of the upper / lower rows: pu[row], pl[row] (pl = pu + nrows)
+template <int Q>
+__global__ void __launch_bounds__(256) partial_norm_kernel(const float* __restrict__ lam, long long cr,
+                                                           long long nrows, int D, double* __restrict__ part) {
+  long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+  int lane = threadIdx.x & (kWarp - 1);
+  if (row >= nrows) return;
+  const float* c = lam + row * D;
+  const float* r = c + cr;
+  NormAcc<Q> acc;
+  for (int d = lane * 4; d < D; d += 4 * kWarp)
+    acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
+  acc.warp_reduce();
+  if (lane == 0) {
+    part[row] = acc.u;
+    part[nrows + row] = acc.l;
+  }
+}
+
+template <int Q>
+__global__ void finish_concretize_kernel(const double* __restrict__ part, const double* __restrict__ lb,
+                                         const double* __restrict__ ub, long long rows_per_s, long long nrows,
+                                         const double* __restrict__ eps, double* __restrict__ lo,
+                                         double* __restrict__ hi) {
+  long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nrows) return;
+  NormAcc<Q> fin;
+  const double e = eps[row / rows_per_s];
+  lo[row] = lb[row] - e * fin.fin(part[nrows + row]);
+  hi[row] = ub[row] + e * fin.fin(part[row]);
+}
+
+// softmax chain, phase B: one CTA per score row (s, h, i).  Exp envelopes per key from the
+// all-reduced input norms; Σ_j e_j rows (local columns, f64) and their partial norms; Σ_j e_lb,
+// Σ_j e_ub.  ex: [5][nSC] a_lo, a_up, e_lb, e_ub, e_lo; sig: [rows][2][D]; p2: [2][rows];
+// sb: [2][rows].
+template <int Q>
+__global__ void __launch_bounds__(256) sm_shard_b_kernel(NView sc, int rows_per_s, int n, int D,
+                                                         const double* __restrict__ p1, long long nsc,
+                                                         const double* __restrict__ eps, int* __restrict__ status,
+                                                         int site_exp, double* __restrict__ ex,
+                                                         double* __restrict__ sig, double* __restrict__ p2,
+                                                         double* __restrict__ sb, long long nrows) {
+  extern __shared__ double smb[];
+  double* a_lo = smb;
+  double* a_up = smb + n;
+  double* red = smb + 2 * n;
+  const long long rid = blockIdx.x;
+  const int s = (int)(rid / rows_per_s);
+  const long long nb = (long long)s * sc.s_stride + (rid % rows_per_s) * n;  // first key neuron
+  const double e = eps[s];
+  NormAcc<Q> fin;
+  int err = 0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const long long o = nb + j;
+    const double nu = fin.fin(p1[o]), nl = fin.fin(p1[nsc + o]);
+    const double xlb = sc.lb[o], xub = sc.ub[o];
+    Lines ln;
+    const int code = envelope(RELAX_EXP, xlb - e * nl, xub + e * nu, ln);
+    if (code) err = err ? min(err, code) : code;
+    a_lo[j] = ln.al;
+    a_up[j] = ln.au;
+    const double ub2 = ln.au * (ln.au >= 0.0 ? xub : xlb) + ln.bu;
+    const double lb2 = ln.al * (ln.al >= 0.0 ? xlb : xub) + ln.bl;
+    ex[o] = ln.al;
+    ex[nsc + o] = ln.au;
+    ex[2 * nsc + o] = lb2;
+    ex[3 * nsc + o] = ub2;
+    ex[4 * nsc + o] = lb2 - e * fabs(ln.al) * (ln.al >= 0.0 ? nl : nu);
+  }
+  if (err) set_status(status, s, site_exp, err);
+  __syncthreads();
+  const float* cb = sc.lam + nb * D;
+  const float* rb = cb + sc.cr;
+  double* sg = sig + rid * 2 * D;
+  double pnu = 0.0, pnl = 0.0;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    double su = 0.0, sl = 0.0;
+    for (int j = 0; j < n; ++j) {
+      const double c = cb[(long long)j * D + d], r = rb[(long long)j * D + d];
+      const double u = c + r, l = c - r;
+      su += a_up[j] * (a_up[j] >= 0.0 ? u : l);
+      sl += a_lo[j] * (a_lo[j] >= 0.0 ? l : u);
+    }
+    sg[d] = su;
+    sg[D + d] = sl;
+    pnu = qcombine<Q>(pnu, Q == NORM_L2 ? su * su : fabs(su));
+    pnl = qcombine<Q>(pnl, Q == NORM_L2 ? sl * sl : fabs(sl));
+  }
+  pnu = block_reduce<Q>(pnu, red);
+  pnl = block_reduce<Q>(pnl, red);
+  if (threadIdx.x == 0) {
+    p2[rid] = pnu;
+    p2[nrows + rid] = pnl;
+    double slb = 0.0, sub = 0.0;  // propagate_sum_axis order (relax.cpp:728-731)
+    for (int j = 0; j < n; ++j) {
+      slb += ex[2 * nsc + nb + j];
+      sub += ex[3 * nsc + nb + j];
+    }
+    sb[rid] = slb;
+    sb[nrows + rid] = sub;
+  }
+}
+
+// phase C: RecipVerify of the all-reduced Σ norms; r rows (in place in sig) and partial norms.
+// rb4: [4][rows] r_al, r_au, r_lb, r_ub.
+template <int Q>
+__global__ void __launch_bounds__(256) sm_shard_c_kernel(int rows_per_s, int D, const double* __restrict__ p2,
+                                                         const double* __restrict__ sb, long long nrows,
+                                                         const double* __restrict__ eps, int* __restrict__ status,
+                                                         int site_recip, double* __restrict__ sig,
+                                                         double* __restrict__ p3, double* __restrict__ rb4) {
+  __shared__ double red[40];
+  const long long rid = blockIdx.x;
+  const int s = (int)(rid / rows_per_s);
+  const double e = eps[s];
+  NormAcc<Q> fin;
+  if (threadIdx.x == 0) {
+    const double slb = sb[rid], sub = sb[nrows + rid];
+    Lines ln;
+    const int code = envelope(RELAX_RECIP, slb - e * fin.fin(p2[nrows + rid]), sub + e * fin.fin(p2[rid]), ln);
+    if (code) set_status(status, s, site_recip, code);
+    red[32] = ln.al;
+    red[33] = ln.au;
+    red[34] = ln.al * (ln.al >= 0.0 ? slb : sub) + ln.bl;
+    red[35] = ln.au * (ln.au >= 0.0 ? sub : slb) + ln.bu;
+  }
+  __syncthreads();
+  const double r_al = red[32], r_au = red[33];
+  if (threadIdx.x == 0) {
+    rb4[rid] = r_al;
+    rb4[nrows + rid] = r_au;
+    rb4[2 * nrows + rid] = red[34];
+    rb4[3 * nrows + rid] = red[35];
+  }
+  double* sg = sig + rid * 2 * D;
+  double pnu = 0.0, pnl = 0.0;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const double u = sg[d], l = sg[D + d];
+    const double yu = r_au * (r_au >= 0.0 ? u : l), yl = r_al * (r_al >= 0.0 ? l : u);
+    sg[d] = yu;
+    sg[D + d] = yl;
+    pnu = qcombine<Q>(pnu, Q == NORM_L2 ? yu * yu : fabs(yu));
+    pnl = qcombine<Q>(pnl, Q == NORM_L2 ? yl * yl : fabs(yl));
+  }
+  pnu = block_reduce<Q>(pnu, red);
+  pnl = block_reduce<Q>(pnl, red);
+  if (threadIdx.x == 0) {
+    p3[rid] = pnu;
+    p3[nrows + rid] = pnl;
+  }
+}
+
+// phase D: McCormick e_j * r per key (warp per key), in place, with per-key partial norms
+// (p4 [2][nSC]); r_lo / r_hi per row appended to rb4 rows 4, 5.
+template <int Q>
+__global__ void __launch_bounds__(256) sm_shard_d_kernel(NView sc, int rows_per_s, int n, int D,
+                                                         const double* __restrict__ p3, long long nrows,
+                                                         const double* __restrict__ eps,
+                                                         const double* __restrict__ ex, long long nsc,
+                                                         const double* __restrict__ sig, double* __restrict__ rb4,
+                                                         double* __restrict__ p4) {
+  const long long rid = blockIdx.x;
+  const int s = (int)(rid / rows_per_s);
+  const long long nb = (long long)s * sc.s_stride + (rid % rows_per_s) * n;
+  const double e = eps[s];
+  NormAcc<Q> fin;
+  const double r_lo = rb4[2 * nrows + rid] - e * fin.fin(p3[nrows + rid]);
+  const double r_hi = rb4[3 * nrows + rid] + e * fin.fin(p3[rid]);
+  if (threadIdx.x == 0) {
+    rb4[4 * nrows + rid] = r_lo;
+    rb4[5 * nrows + rid] = r_hi;
+  }
+  const double* sg = sig + rid * 2 * D;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < n; j += nw) {
+    const long long o = nb + j;
+    float* c = sc.lam + o * D;
+    float* r = c + sc.cr;
+    const double al = ex[o], au = ex[nsc + o], lx = ex[4 * nsc + o], ly = r_lo, uy = r_hi;
+    double gu = 0.0, gl = 0.0;
+    for (int d = lane; d < D; d += 32) {
+      const double cv = c[d], rv = r[d];
+      const double u = cv + rv, l = cv - rv;
+      const double eu = au * (au >= 0.0 ? u : l), el = al * (al >= 0.0 ? l : u);
+      const double yu = sg[d], yl = sg[D + d];
+      double p_l = 0.0, p_u = 0.0;
+      if (ly != 0.0) p_l += ly * (ly >= 0.0 ? el : eu);  // relax.cpp:542-553
+      if (lx != 0.0) p_l += lx * (lx >= 0.0 ? yl : yu);
+      if (uy != 0.0) p_u += uy * (uy >= 0.0 ? eu : el);  // relax.cpp:556-567
+      if (lx != 0.0) p_u += lx * (lx >= 0.0 ? yu : yl);
+      c[d] = (float)(0.5 * (p_u + p_l));
+      r[d] = (float)(0.5 * (p_u - p_l));
+      gu = qcombine<Q>(gu, Q == NORM_L2 ? p_u * p_u : fabs(p_u));
+      gl = qcombine<Q>(gl, Q == NORM_L2 ? p_l * p_l : fabs(p_l));
+    }
+    if (Q == NORM_LINF) { gu = warp_max(gu); gl = warp_max(gl); }
+    else { gu = warp_sum(gu); gl = warp_sum(gl); }
+    if (lane == 0) {
+      p4[o] = gu;
+      p4[nsc + o] = gl;
+    }
+  }
+}
+
+// phase E: probs lb/ub (term_bias) and lo/hi per key from the all-reduced output norms.
+template <int Q>
+__global__ void sm_shard_e_kernel(NView sc, int rows_per_s, int n, long long nrows_total,
+                                  const double* __restrict__ ex, long long nsc, const double* __restrict__ rb4,
+                                  long long nrows, const double* __restrict__ p4, const double* __restrict__ eps) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows_total * n) return;
+  const long long rid = t / n;
+  const int j = (int)(t % n);
+  const int s = (int)(rid / rows_per_s);
+  const long long o = (long long)s * sc.s_stride + (rid % rows_per_s) * n + j;
+  double olb = 0.0, oub = 0.0;
+  term_bias(ex[4 * nsc + o], rb4[4 * nrows + rid], rb4[5 * nrows + rid], ex[2 * nsc + o], ex[3 * nsc + o],
+            rb4[2 * nrows + rid], rb4[3 * nrows + rid], olb, oub);
+  sc.lb[o] = olb;
+  sc.ub[o] = oub;
+  if (sc.lo) {
+    NormAcc<Q> fin;
+    const double e = eps[s];
+    sc.lo[o] = olb - e * fin.fin(p4[nsc + o]);
+    sc.hi[o] = oub + e * fin.fin(p4[o]);
+  }
+}
+
+// classifier head, partial: logits Λ over the local columns, raw norms + f64 biases.
+// part: [2][S*C] (u, l raw partials; +inf when a local element is non-finite); bias: [2][S*C]
+template <int Q>
+__global__ void head_partial_kernel(const double* pc, const double* pr, const double* plb, const double* pub,
+                                    const double* wc, const double* bc, int S, int E, int C, int D, double* part,
+                                    double* bias) {
+  __shared__ double red[32];
+  const int s = blockIdx.x / C, cls = blockIdx.x % C;
+  double nu = 0.0, nl = 0.0;
+  int finite = 1;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    double ac = 0.0, ar = 0.0;
+    for (int e = 0; e < E; ++e) {
+      const double w = wc[e * C + cls];
+      ac += w * pc[((long long)s * E + e) * D + d];
+      ar += fabs(w) * pr[((long long)s * E + e) * D + d];
+    }
+    const double u = ac + ar, l = ac - ar;
+    finite &= (isfinite(u) && isfinite(l));
+    nu = qcombine<Q>(nu, Q == NORM_L2 ? u * u : fabs(u));
+    nl = qcombine<Q>(nl, Q == NORM_L2 ? l * l : fabs(l));
+  }
+  finite = __syncthreads_and(finite);
+  nu = block_reduce<Q>(nu, red);
+  nl = block_reduce<Q>(nl, red);
+  if (threadIdx.x == 0) {
+    double ub_pos = 0.0, ub_neg = 0.0, lb_pos = 0.0, lb_neg = 0.0;  // relax.cpp:280-299
+    for (int i = 0; i < E; ++i) {
+      const double wv = wc[i * C + cls];
+      const double wp = (wv < 0.0) ? 0.0 : wv, wn = (0.0 < wv) ? 0.0 : wv;
+      const double xu = pub[(long long)s * E + i], xl = plb[(long long)s * E + i];
+      ub_pos += wp * xu;
+      ub_neg += wn * xl;
+      lb_pos += wp * xl;
+      lb_neg += wn * xu;
+    }
+    const int k = s * C + cls, SC = S * C;
+    part[k] = finite ? nu : HUGE_VAL;
+    part[SC + k] = finite ? nl : HUGE_VAL;
+    bias[k] = ub_pos + ub_neg + bc[cls];
+    bias[SC + k] = lb_pos + lb_neg + bc[cls];
+  }
+}
+
+template <int Q>
+__global__ void head_finish_kernel(const double* part, const double* bias, int S, int C, const double* eps,
+                                   double* out_lo, double* out_hi, int* status, int site) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= S * C) return;
+  const int s = k / C, SC = S * C;
+  const double yub = bias[k], ylb = bias[SC + k], nu = part[k], nl = part[SC + k];
+  if (!isfinite(yub) || !isfinite(ylb) || !isfinite(nu) || !isfinite(nl))  // graph.cpp:663-671
+    set_status(status, s, site, kCodeDomain);
+  NormAcc<Q> fin;
+  const double e = eps[s];
+  out_lo[k] = ylb - e * fin.fin(nl);
+  out_hi[k] = yub + e * fin.fin(nu);
+}
+
+}  // namespace
+
+int launch_partial_norms(const float* lam, long long cr, long long nrows, int D, int norm, double* part,
+                         cudaStream_t st) {
+  if (nrows <= 0) return 0;
+  DISPATCH_Q(dual_norm(norm), partial_norm_kernel, <<<blocks_for(nrows, 8), 256, 0, st>>>(lam, cr, nrows, D, part));
+  return 1;
+}
+
+int launch_finish_concretize(const double* part, const double* lb, const double* ub, long long rows_per_s,
+                             long long nrows, int norm, const double* eps, double* lo, double* hi, cudaStream_t st) {
+  if (nrows <= 0) return 0;
+  DISPATCH_Q(dual_norm(norm), finish_concretize_kernel,
+             <<<blocks_for(nrows, 256), 256, 0, st>>>(part, lb, ub, rows_per_s, nrows, eps, lo, hi));
+  return 1;
+}
+
+int reduce_op_for_norm(int norm) { return dual_norm(norm) == NORM_LINF ? 1 : 0; }  // 0 SUM, 1 MAX
+
+int launch_sm_shard(int phase, const NView& sc, int S, int rows_per_s, int n, int D, int norm, const double* eps,
+                    int* status, int site_exp, int site_recip, SmShardBufs b, cudaStream_t st) {
+  const long long nrows = (long long)S * rows_per_s, nsc = nrows * n;
+  const int q = dual_norm(norm);
+  switch (phase) {
+    case 0:  // exp-input partial norms per key
+      return launch_partial_norms(sc.lam, sc.cr, nsc, D, norm, b.p_key, st);
+    case 1:
+      DISPATCH_Q(q, sm_shard_b_kernel, <<<(unsigned)nrows, 256, (2 * n + 32) * sizeof(double), st>>>(
+          sc, rows_per_s, n, D, b.p_key, nsc, eps, status, site_exp, b.ex, b.sig, b.p_row, b.sb, nrows));
+      return 1;
+    case 2:
+      DISPATCH_Q(q, sm_shard_c_kernel, <<<(unsigned)nrows, 256, 0, st>>>(
+          rows_per_s, D, b.p_row, b.sb, nrows, eps, status, site_recip, b.sig, b.p_row2, b.rb));
+      return 1;
+    case 3:
+      DISPATCH_Q(q, sm_shard_d_kernel, <<<(unsigned)nrows, 256, 0, st>>>(
+          sc, rows_per_s, n, D, b.p_row2, nrows, eps, b.ex, nsc, b.sig, b.rb, b.p_key));
+      return 1;
+    default:
+      DISPATCH_Q(q, sm_shard_e_kernel, <<<blocks_for(nsc, 256), 256, 0, st>>>(
+          sc, rows_per_s, n, nrows, b.ex, nsc, b.rb, nrows, b.p_key, eps));
+      return 1;
+  }
+}
+
+int launch_head_partial(const double* pc, const double* pr, const double* plb, const double* pub, const double* wc,
+                        const double* bc, int S, int E, int C, int D, int norm, double* part, double* bias,
+                        cudaStream_t st) {
+  DISPATCH_Q(dual_norm(norm), head_partial_kernel,
+             <<<S * C, 256, 0, st>>>(pc, pr, plb, pub, wc, bc, S, E, C, D, part, bias));
+  return 1;
+}
+
+int launch_head_finish(const double* part, const double* bias, int S, int C, int norm, const double* eps,
+                       double* out_lo, double* out_hi, int* status, int site, cudaStream_t st) {
+  DISPATCH_Q(dual_norm(norm), head_finish_kernel,
+             <<<blocks_for((long long)S * C, 128), 128, 0, st>>>(part, bias, S, C, eps, out_lo, out_hi, status, site));
   return 1;
 }
 

@@ -143,6 +143,12 @@ def load_library():
     L.fg_sum_axis.argtypes = [vp, sz, sz, sz, sz] + [_dp] * 8
     L.fg_mul_broadcast.argtypes = [vp, sz, sz, sz, sz] + [_dp] * 8 + [C.c_int, C.c_double] + [_dp] * 4
     L.fg_bilinear.argtypes = [vp, sz] + [_dp] * 10
+    L.fg_nccl_unique_id.argtypes = [C.c_char_p]
+    L.fg_model_shard_nccl.argtypes = [vp, C.c_int, C.c_int, C.c_char_p]
+    L.fg_loopback_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.fg_loopback_destroy.argtypes = [vp]
+    L.fg_model_shard_loopback.argtypes = [vp, vp, C.c_int]
+    L.fg_model_set_column_shard.argtypes = [vp, C.c_int, C.c_int, vp, vp, C.c_int]
     _lib = L
     return L
 
@@ -441,8 +447,49 @@ def gen_positions(seed: int, length: int, words: int) -> np.ndarray:
     return p
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for fg_model_shard_nccl (create on rank 0, share with all ranks)."""
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    if lib.fg_nccl_unique_id(buf) != FG_OK:
+        raise CudaError("fg_nccl_unique_id: libnccl.so.2 unavailable")
+    return buf.raw
+
+
+class LoopbackGroup:
+    """fg_loopback: `nranks` column-sharded models on ONE device, one host thread per rank."""
+
+    def __init__(self, nranks: int):
+        self.lib = load_library()
+        h = C.c_void_p()
+        if self.lib.fg_loopback_create(nranks, C.byref(h)) != FG_OK:
+            raise CudaError("fg_loopback_create failed")
+        self.handle, self.nranks = h, nranks
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.fg_loopback_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Model:
     """fg_model: weights resident in HBM; batched bound passes, certify and max-epsilon."""
+
+    def shard_columns_nccl(self, rank: int, nranks: int, uid: bytes):
+        """Column-shard the perturbation dimension over `nranks` GPUs; partial norms all-reduced
+        with NCCL.  Every rank must then call the same passes."""
+        self.ctx._check(self.lib.fg_model_shard_nccl(self.handle, rank, nranks, uid), "fg_model_shard_nccl")
+
+    def shard_columns_loopback(self, group: LoopbackGroup, rank: int):
+        """Column-shard over a LoopbackGroup (virtual ranks on one device, one thread each)."""
+        self._loop = group  # keep the group alive as long as the model
+        self.ctx._check(self.lib.fg_model_shard_loopback(self.handle, group.handle, rank), "fg_model_shard_loopback")
 
     def __init__(self, ctx: Context, cfg: ModelConfig, params: np.ndarray):
         self.ctx, self.cfg, self.lib = ctx, cfg, ctx.lib

@@ -95,3 +95,71 @@ def test_world2_gloo_sharding(port_oracle=None):
         pos = o.gen_positions(3000 + s, cfg.length, 1)
         st2, lo2, hi2, _, _ = o.bound_pass(cfg, params, x, pos, "linf", 0.02)
         assert st == st2 and np.array_equal(lo, lo2) and np.array_equal(hi, hi2)
+
+
+def _col_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import numpy as np
+    import torch
+    from oracle.oracle import Oracle
+    from paper_2209_12708_b200 import dist as Dm
+    from paper_2209_12708_b200 import faith_gpu as F
+    dist = Dm.init(backend="gloo")
+    info = Dm.rank_info()
+    o = Oracle("port")
+    out = {}
+    # 1) concretization of column-split Λ with all-reduced partials == full concretization
+    rng = np.random.default_rng(5)
+    n, d = 37, 64
+    lw, uw = rng.uniform(-1, 1, (n, d)), rng.uniform(-1, 1, (n, d))
+    lb, ub = rng.uniform(-1, 0, n), rng.uniform(0, 1, n)
+    cols = Dm.column_range(d, info.rank, info.world)
+    for norm in ("l1", "l2", "linf"):
+        pl = torch.tensor(Dm.partial_norms(lw[:, cols.start:cols.stop], norm))
+        pu = torch.tensor(Dm.partial_norms(uw[:, cols.start:cols.stop], norm))
+        op = dist.ReduceOp.MAX if Dm.reduce_op(norm) == "max" else dist.ReduceOp.SUM
+        dist.all_reduce(pl, op=op)
+        dist.all_reduce(pu, op=op)
+        lo = lb - 0.3 * Dm.finish_norms(pl.numpy(), norm)
+        hi = ub + 0.3 * Dm.finish_norms(pu.numpy(), norm)
+        out[norm] = (lo, hi, o.concretize(lw, lb, uw, ub, norm, 0.3))
+    # 2) the NCCL unique-id handshake of shard_model_columns (broadcast from rank 0)
+    box = [F.nccl_unique_id() if info.rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    out["uid"] = box[0]
+    q.put((info.rank, out, list(cols)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_world2_gloo_column_shard_host_logic():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_col_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, out, cols = q.get(timeout=240)
+        res[rank] = (out, cols)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] + res[1][1] == list(range(64))
+    assert res[0][0]["uid"] == res[1][0]["uid"] and len(res[0][0]["uid"]) == 128
+    for norm in ("l1", "l2", "linf"):
+        for r in range(world):
+            lo, hi, (plo, phi) = res[r][0][norm]
+            assert np.allclose(lo, plo, rtol=0, atol=1e-12) and np.allclose(hi, phi, rtol=0, atol=1e-12)
+
+
+def test_column_range_rules():
+    assert list(D.column_range(16, 1, 2)) == list(range(8, 16))
+    with pytest.raises(ValueError):
+        D.column_range(1536, 0, 16 * 7)
+    assert D.reduce_op("l1") == "max" and D.reduce_op("l2") == "sum" and D.reduce_op("linf") == "sum"
