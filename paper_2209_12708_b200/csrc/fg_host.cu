@@ -194,7 +194,8 @@ struct DevAffine {
   DBuf w32, w64, b64;
   DBuf a_hi, a_lo;        // [2][O][C] f32: (W^T, |W|^T) split for 3xTF32 (tcgen05 path)
   TensorMap tm_hi, tm_lo;
-  bool umma = false;
+  TensorMap tm2_hi, tm2_lo;  // box height bn/2: one CTA's half of a W tile (CTA-pair kernel)
+  bool umma = false, umma2 = false;
   int bn = 0;
   int C = 0, O = 0;
 };
@@ -220,6 +221,10 @@ fg_status upload_affine(fg_ctx* ctx, DevAffine& a, int C, int O, const std::vect
   }
   // tcgen05 operands: transposed (K-major) and split into TF32 hi/lo parts once.
   a.bn = umma_pick_bn(O);
+  if (const char* e = std::getenv("FG_AFFINE_BN")) {  // tuning knob: N tile of the affine GEMM
+    const int want = std::atoi(e);
+    if (want >= 32 && want <= a.bn && O % want == 0) a.bn = want;
+  }
   if (umma_available() && a.bn > 0 && C % 32 == 0) {
     std::vector<float> hi(2 * (size_t)C * O), lo(2 * (size_t)C * O);
     for (int plane = 0; plane < 2; ++plane)
@@ -237,6 +242,8 @@ fg_status upload_affine(fg_ctx* ctx, DevAffine& a, int C, int O, const std::vect
     CK(cudaMemcpy(a.a_lo.p, lo.data(), sizeof(float) * lo.size(), cudaMemcpyHostToDevice));
     a.umma = umma_tmap_wop(a.tm_hi.bytes, a.a_hi.as<float>(), C, O, 2, 1, a.bn) &&
              umma_tmap_wop(a.tm_lo.bytes, a.a_lo.as<float>(), C, O, 2, 1, a.bn);
+    a.umma2 = a.umma && a.bn >= 64 && umma_tmap_wop(a.tm2_hi.bytes, a.a_hi.as<float>(), C, O, 2, 1, a.bn / 2) &&
+              umma_tmap_wop(a.tm2_lo.bytes, a.a_lo.as<float>(), C, O, 2, 1, a.bn / 2);
   }
   return FG_OK;
 }
@@ -247,6 +254,14 @@ GemmArgs affine_gemm(const DevAffine& a, const float* in, long long in_cr, float
 bool umma_enabled() {
   const char* e = std::getenv("FG_NO_UMMA");
   return !(e && e[0] == '1');
+}
+bool umma_dots_enabled() {
+  const char* e = std::getenv("FG_NO_UMMA_DOTS");
+  return umma_enabled() && !(e && e[0] == '1');
+}
+bool umma_affine_enabled() {
+  const char* e = std::getenv("FG_NO_UMMA_AFFINE");
+  return umma_enabled() && !(e && e[0] == '1');
 }
 
 // Λ bound GEMM of one affine over `rows` token rows: tcgen05 3xTF32 when the shape and
@@ -272,9 +287,10 @@ LamGemm affine_lam(const DevAffine& a, float* out, long long out_cr, const float
 int launch_affine_lambda(const DevAffine& a, const TensorMap* tm_in, const float* in, long long in_cr,
                          float* out, long long out_cr, const float* res, long long res_cr, long long rows,
                          int D, cudaStream_t st) {
-  if (a.umma && tm_in && umma_enabled() && D % 128 == 0) {
+  if (a.umma && tm_in && umma_affine_enabled() && D % 128 == 0) {
     return launch_lam_gemm(tm_in->bytes, a.tm_hi.bytes, a.tm_lo.bytes,
-                           affine_lam(a, out, out_cr, res, res_cr, rows, D), a.bn, st);
+                           affine_lam(a, out, out_cr, res, res_cr, rows, D), a.bn, st,
+                           a.umma2 ? a.tm2_hi.bytes : nullptr, a.umma2 ? a.tm2_lo.bytes : nullptr);
   }
   return launch_gemm(affine_gemm(a, in, in_cr, out, out_cr, res, res_cr, rows, D), st);
 }
@@ -635,6 +651,8 @@ struct Workspace {
   TensorMap tm_QKVk, tm_QKVrow, tm_SC;
   DBuf cf_sim_x[2], cf_sim_y[2], cf_wv_x[2], cf_wv_y[2];  // [hi, lo]
   TensorMap tm_sim_x[2], tm_sim_y[2], tm_wv_x[2], tm_wv_y[2];
+  TensorMap tm2_sim_x[2], tm2_sim_y[2], tm2_wv_x[2], tm2_wv_y[2];  // half-height boxes (CTA pairs)
+  bool dots2_ok = false;
   int bn_sim = 0, bn_simx = 0, bn_wvx = 0;
   bool dots_ok = false;
   long long crX = 0, crQKV = 0, crF = 0, crSC = 0;
@@ -782,6 +800,13 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot) {
            umma_tmap_wop(w.tm_wv_y[part].bytes, w.cf_wv_y[part].as<float>(), (int)L, (int)L, 2, (int)SH, w.bn_sim);
     }
     w.dots_ok = ok;
+    bool ok2 = ok && w.bn_sim >= 64 && w.bn_simx >= 64 && w.bn_wvx >= 64;
+    for (int part = 0; part < 2 && ok2; ++part)
+      ok2 = umma_tmap_wop(w.tm2_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), (int)(2 * hd), (int)(2 * L), 1, (int)SH, w.bn_simx / 2) &&
+            umma_tmap_wop(w.tm2_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), (int)hd, (int)L, 2, (int)SH, w.bn_sim / 2) &&
+            umma_tmap_wop(w.tm2_wv_x[part].bytes, w.cf_wv_x[part].as<float>(), (int)(2 * L), (int)(2 * hd), 1, (int)SH, w.bn_wvx / 2) &&
+            umma_tmap_wop(w.tm2_wv_y[part].bytes, w.cf_wv_y[part].as<float>(), (int)L, (int)L, 2, (int)SH, w.bn_sim / 2);
+    w.dots2_ok = ok2;
   }
   return FG_OK;
 }
@@ -906,7 +931,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     // scores = DotProduct(q, k); scaled = Scale(scores, 1/sqrt(hd))   (model.cpp:410-418)
     const double scale = 1.0 / std::sqrt((double)hd);
     g_tag = "dot_similarity";
-    if (w.dots_ok && umma_enabled()) {
+    if (w.dots_ok && umma_dots_enabled()) {
       LAUNCH(launch_sim_coef_split(q, k, S, H, L, hd, w.cf_sim_x[0].as<float>(), w.cf_sim_x[1].as<float>(),
                                    w.cf_sim_y[0].as<float>(), w.cf_sim_y[1].as<float>(), st));
       LAUNCH(launch_sim_bias(q, k, sc, S, H, L, hd, scale, st));
@@ -924,7 +949,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
       gx.ldn_out = D;
       gx.n_split = L; gx.split_stride = w.crSC;
       gx.alpha = (float)scale;
-      LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_x[0].bytes, w.tm_sim_x[1].bytes, gx, w.bn_simx, st));
+      LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_x[0].bytes, w.tm_sim_x[1].bytes, gx, w.bn_simx, st,
+                             w.dots2_ok ? w.tm2_sim_x[0].bytes : nullptr, w.dots2_ok ? w.tm2_sim_x[1].bytes : nullptr));
       // y-side: scores[s,h,i,j,:] += sum_k lx[i,k] K_p[j, E + h*hd + k]   (per plane p)
       LamGemm gy{};
       gy.M = D; gy.N = L; gy.K = hd; gy.K0 = hd;
@@ -940,7 +966,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
       gy.out_c[3] = w.crSC; gy.ldn_out = (long long)L * D;
       gy.alpha = (float)scale;
       gy.accumulate = 1;
-      LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_y[0].bytes, w.tm_sim_y[1].bytes, gy, w.bn_sim, st));
+      LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_y[0].bytes, w.tm_sim_y[1].bytes, gy, w.bn_sim, st,
+                             w.dots2_ok ? w.tm2_sim_y[0].bytes : nullptr, w.dots2_ok ? w.tm2_sim_y[1].bytes : nullptr));
     } else {
       LAUNCH(launch_dot_similarity(q, k, sc, S, L, H, hd, D, w.coef.as<float>(), (float)scale, st));
     }
@@ -972,7 +999,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     // ctx = DotProduct(probs, v)
     NView cx{CTX, w.crX, CTX_lb, CTX_ub, nullptr, nullptr, (long long)L * E, E, 0};
     g_tag = "dot_weighted";
-    if (w.dots_ok && umma_enabled()) {
+    if (w.dots_ok && umma_dots_enabled()) {
       LAUNCH(launch_wv_coef_split(sc, v, S, H, L, hd, w.cf_wv_x[0].as<float>(), w.cf_wv_x[1].as<float>(),
                                   w.cf_wv_y[0].as<float>(), w.cf_wv_y[1].as<float>(), st));
       LAUNCH(launch_wv_bias(sc, v, cx, S, H, L, hd, st));
@@ -989,7 +1016,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
       gx.ldn_out = D;
       gx.n_split = hd; gx.split_stride = w.crX;
       gx.alpha = 1.0f;
-      LAUNCH(launch_lam_gemm(w.tm_SC.bytes, w.tm_wv_x[0].bytes, w.tm_wv_x[1].bytes, gx, w.bn_wvx, st));
+      LAUNCH(launch_lam_gemm(w.tm_SC.bytes, w.tm_wv_x[0].bytes, w.tm_wv_x[1].bytes, gx, w.bn_wvx, st,
+                             w.dots2_ok ? w.tm2_wv_x[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_x[1].bytes : nullptr));
       // y-side: ctx[s,i,h*hd+k,:] += sum_j lx[i,j] V_p[j, 2E + h*hd + k]   (K along token rows)
       LamGemm gy{};
       gy.M = D; gy.N = L; gy.K = L; gy.K0 = L;
@@ -1005,7 +1033,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
       gy.out_c[3] = w.crX; gy.ldn_out = (long long)E * D;
       gy.alpha = 1.0f;
       gy.accumulate = 1;
-      LAUNCH(launch_lam_gemm(w.tm_QKVrow.bytes, w.tm_wv_y[0].bytes, w.tm_wv_y[1].bytes, gy, w.bn_sim, st));
+      LAUNCH(launch_lam_gemm(w.tm_QKVrow.bytes, w.tm_wv_y[0].bytes, w.tm_wv_y[1].bytes, gy, w.bn_sim, st,
+                             w.dots2_ok ? w.tm2_wv_y[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_y[1].bytes : nullptr));
     } else {
       LAUNCH(launch_dot_weighted(sc, v, cx, S, L, H, hd, D, w.coef.as<float>(), st));
     }
@@ -1682,7 +1711,8 @@ fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_
   if (umma) {
     CK(cudaEventRecord(e0, ctx->stream));
     LAUNCH(launch_lam_gemm(tm.bytes, a.tm_hi.bytes, a.tm_lo.bytes, affine_lam(a, Y2.as<float>(), nout, nullptr, 0, rows, D),
-                           a.bn, ctx->stream));
+                           a.bn, ctx->stream, a.umma2 ? a.tm2_hi.bytes : nullptr,
+                           a.umma2 ? a.tm2_lo.bytes : nullptr));
     CK(cudaEventRecord(e1, ctx->stream));
     CK(cudaEventSynchronize(e1));
     cudaEventElapsedTime(&t, e0, e1);

@@ -165,8 +165,10 @@ int umma_pick_bn(int N);  // 256 / 128 / 64, or 0 when N is not a multiple of 64
 bool umma_tmap_lam(void* tm, const float* base, const unsigned long long dims[4],
                    const unsigned long long strides_bytes[3], int kdim);
 bool umma_tmap_wop(void* tm, const float* base, int K, int N, int P2, int P3, int bn);
+// tm2_whi / tm2_wlo: the same operands mapped with box height bn/2 (one CTA's half of a W tile);
+// when given and M % 256 == 0 the CTA-pair (cta_group::2, M = 256) kernel runs.
 int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, LamGemm p, int bn,
-                    cudaStream_t st);
+                    cudaStream_t st, const void* tm2_whi = nullptr, const void* tm2_wlo = nullptr);
 int launch_ref_affine_f64(const float* W, const float* X, long long x_cr, double* Y, int C, int O, int D,
                           long long rows, cudaStream_t st);
 

@@ -28,6 +28,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fg_internal.cuh"
 
@@ -97,6 +98,22 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void umma2_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// commit of the pair's MMAs, arriving on `bar` in both CTAs of the cluster
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -113,20 +130,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN, int STAGES>
-struct SmemLayout {
-  static constexpr int kW = BN * kBK * 4;    // W tile (hi or lo), K-major
-  static constexpr int kL = kBK * kBM * 4;   // Λ tile (raw, hi or lo): 16 KB
-  static constexpr int kWlo = kW;
-  static constexpr int kRaw = 2 * kW;
-  static constexpr int kHi = 2 * kW + kL;
-  static constexpr int kLo = 2 * kW + 2 * kL;
-  static constexpr int kStage = 2 * kW + 3 * kL;
-  static constexpr int kBarOff = STAGES * kStage;
-  static constexpr int kBytes = kBarOff + 256 + 1024;  // + barriers/tmem slot + alignment slack
-  static_assert(kBytes <= 227 * 1024, "stage ring exceeds shared memory");
-};
-
 __device__ __forceinline__ int lin5(const int* co, const int* b) {
   return co[0] * b[0] + co[1] * b[1] + co[2] * b[2] + co[3] * b[3] + co[4];
 }
@@ -134,32 +137,77 @@ __device__ __forceinline__ long long lin5l(const long long* co, const int* b) {
   return co[0] * b[0] + co[1] * b[1] + co[2] * b[2] + co[3] * b[3] + co[4];
 }
 
-template <int BN, int STAGES>
+// Arrive on the pair leader's (CTA rank 0) copy of a barrier.
+__device__ __forceinline__ void mbar_arrive_cta0(uint64_t* local_bar) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(a) : "r"(smem_u32(local_bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+// SMEM plan: an operand ring of S stages {W_hi, W_lo, L_hi, L_lo} feeding the MMA and a raw
+// ring of R Λ tiles feeding the split warps, so Λ loads run ahead of the operand stages.
+template <int BN, int S, int R, bool PAIR>
+struct Ring {
+  static constexpr int kWT = (PAIR ? BN / 2 : BN) * kBK * 4;  // this CTA's W tile, hi or lo
+  static constexpr int kL = kBK * kBM * 4;                    // Λ tile: 16 KB
+  static constexpr int kWlo = kWT;
+  static constexpr int kLhi = 2 * kWT;
+  static constexpr int kLlo = 2 * kWT + kL;
+  static constexpr int kOp = 2 * kWT + 2 * kL;
+  static constexpr int kRawOff = S * kOp;
+  static constexpr int kBarOff = kRawOff + R * kL;
+  static constexpr int kBytes = kBarOff + 256 + 1024;  // + barriers / TMEM slot + alignment slack
+  static_assert(kBytes <= 227 * 1024, "rings exceed shared memory");
+  static_assert(3 * S + 2 * R + 4 <= 31, "barrier area");
+};
+
+// Persistent warp-specialized tcgen05 3xTF32 engine (see the file header).  PAIR = CTA-pair
+// variant (2-CTA cluster, cta_group::2, M = 256): CTA r holds d-rows m0 + 128r.. of Λ and W
+// rows n0 + r*BN/2.. of the weight operand; the leader issues the MMA over both CTAs' SMEM and
+// commits multicast; operand readiness of both CTAs is collected on the leader's `split`
+// barrier (split warps wait for their CTA's W tile before arriving), accumulator drain on the
+// leader's `tempty`.
+//   warp 0: W producer    warp 1: TMEM alloc + MMA issuer    warp 2: Λ producer
+//   warps 4-7: split/transpose Λ -> L_hi/L_lo    warps 8-11: epilogue
+template <int BN, int S, int R, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     lam_gemm_kernel(const __grid_constant__ CUtensorMap tm_lam, const __grid_constant__ CUtensorMap tm_whi,
                     const __grid_constant__ CUtensorMap tm_wlo, const LamGemm p) {
-  using SL = SmemLayout<BN, STAGES>;
+  using RL = Ring<BN, S, R, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SL::kBarOff);
-  uint64_t* split = full + STAGES;
-  uint64_t* empty = split + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + RL::kBarOff);
+  uint64_t* split = wfull + S;
+  uint64_t* opempty = split + S;
+  uint64_t* rawfull = opempty + S;
+  uint64_t* rawfree = rawfull + R;
+  uint64_t* tfull = rawfree + R;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = p.K / kBK;
+  uint32_t rank = 0;
+  if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int tiles_m = PAIR ? p.tiles_m / 2 : p.tiles_m;
+  const int num_tiles = PAIR ? p.num_tiles / 2 : p.num_tiles;
+  constexpr int kGather = PAIR ? 256 : 128;  // split / epilogue threads reporting to the (leader) CTA
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&split[s], 128);
-      mbar_init(&empty[s], 1);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&wfull[i], 1);
+      mbar_init(&split[i], kGather);
+      mbar_init(&opempty[i], 1);
+    }
+    for (int i = 0; i < R; ++i) {
+      mbar_init(&rawfull[i], 1);
+      mbar_init(&rawfree[i], 128);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], kGather);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_lam) : "memory");
@@ -167,93 +215,124 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_wlo) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN < 32 ? 32 : 2 * BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN < 32 ? 32 : 2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN < 32 ? 32 : 2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   // tile t -> (batch b0..b3, m-tile over d, n-tile over output neurons); n fastest so that
-  // CTAs running concurrently share the (HBM-resident) Λ tiles through L2.
+  // units running concurrently share the (HBM-resident) Λ tiles through L2.
   auto decode = [&](int t, int* b, int& m0, int& n0) {
     int nt = t % p.tiles_n;
     int rest = t / p.tiles_n;
-    int mt = rest % p.tiles_m;
-    int batch = rest / p.tiles_m;
+    int mt = rest % tiles_m;
+    int batch = rest / tiles_m;
     b[3] = batch % p.nb[3];
     batch /= p.nb[3];
     b[2] = batch % p.nb[2];
     batch /= p.nb[2];
     b[1] = batch % p.nb[1];
     b[0] = batch / p.nb[1];
-    m0 = mt * kBM;
+    m0 = mt * (PAIR ? 2 : 1) * kBM + (int)rank * kBM;  // this CTA's first d-row
     n0 = nt * BN;
   };
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- W producer ----------------
     if (lane == 0) {
       int g = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = unit; t < num_tiles; t += nunits) {
+        int b[4], m0, n0;
+        decode(t, b, m0, n0);
+        const int wc2 = lin5(p.w_c[0], b), wc3 = lin5(p.w_c[1], b);
+        const int nw0 = n0 + (PAIR ? (int)rank * (BN / 2) : 0);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % S;
+          mbar_wait(&opempty[s], ((g / S) & 1) ^ 1);
+          uint8_t* st = smem + s * RL::kOp;
+          mbar_expect_tx(&wfull[s], 2 * RL::kWT);
+          tma_load_4d(st, &tm_whi, &wfull[s], kb * kBK, nw0, wc2, wc3);
+          tma_load_4d(st + RL::kWlo, &tm_wlo, &wfull[s], kb * kBK, nw0, wc2, wc3);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    // ---------------- Λ producer (raw ring) ----------------
+    if (lane == 0) {
+      int g = 0;
+      for (int t = unit; t < num_tiles; t += nunits) {
         int b[4], m0, n0;
         decode(t, b, m0, n0);
         const int lc1 = lin5(p.lam_c[0], b), lc2 = lin5(p.lam_c[1], b), lc3 = lin5(p.lam_c[2], b);
-        const int wc2 = lin5(p.w_c[0], b), wc3 = lin5(p.w_c[1], b);
         for (int kb = 0; kb < nkb; ++kb, ++g) {
-          const int s = g % STAGES;
-          const uint32_t ph = (g / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * SL::kStage;
-          mbar_expect_tx(&full[s], 2 * SL::kW + SL::kL);
-          const int kw = kb * kBK;
-          tma_load_4d(st, &tm_whi, &full[s], kw, n0, wc2, wc3);
-          tma_load_4d(st + SL::kWlo, &tm_wlo, &full[s], kw, n0, wc2, wc3);
-          int kl = kw, plane = 0;
+          const int r = g % R;
+          mbar_wait(&rawfree[r], ((g / R) & 1) ^ 1);
+          mbar_expect_tx(&rawfull[r], RL::kL);
+          int kl = kb * kBK, plane = 0;
           if (kl >= p.K0) {  // c/r concatenation along K: second half reads the r plane
             kl -= p.K0;
             plane = 1;
           }
-          tma_load_4d(st + SL::kRaw, &tm_lam, &full[s], m0, lc1 + (p.kdim == 1 ? kl : 0),
+          tma_load_4d(smem + RL::kRawOff + r * RL::kL, &tm_lam, &rawfull[r], m0, lc1 + (p.kdim == 1 ? kl : 0),
                       lc2 + (p.kdim == 2 ? kl : 0), lc3 + plane);
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    // D f32, A/B tf32, both K-major, N = BN, M = 128
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(kBM >> 4) << 24);
-    int g = 0, it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      mbar_wait(&tempty[acc], aph ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < nkb; ++kb, ++g) {
-        const int s = g % STAGES;
-        const uint32_t ph = (g / STAGES) & 1;
-        mbar_wait(&split[s], ph);
+    // ---------------- MMA issuer (the leader CTA of a pair) ----------------
+    if (!PAIR || rank == 0) {
+      // D f32, A/B tf32, both K-major, N = BN, M = 128 (256 for a pair)
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)((PAIR ? 2 : 1) * kBM >> 4) << 24);
+      int g = 0, it = 0;
+      for (int t = unit; t < num_tiles; t += nunits, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          uint8_t* st = smem + s * SL::kStage;
-          const uint32_t w_hi = smem_u32(st), w_lo = smem_u32(st + SL::kWlo);
-          const uint32_t l_hi = smem_u32(st + SL::kHi), l_lo = smem_u32(st + SL::kLo);
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % S;
+          mbar_wait(&split[s], (g / S) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            uint8_t* st = smem + s * RL::kOp;
+            const uint32_t w_hi = smem_u32(st), w_lo = smem_u32(st + RL::kWlo);
+            const uint32_t l_hi = smem_u32(st + RL::kLhi), l_lo = smem_u32(st + RL::kLlo);
 #pragma unroll
-          for (int ks = 0; ks < kBK / 8; ++ks) {  // +32 B per 8 tf32 of K inside the 128 B rows
-            const uint64_t ahi = kmajor_sw128_desc(l_hi + ks * 32), alo = kmajor_sw128_desc(l_lo + ks * 32);
-            const uint64_t bhi = kmajor_sw128_desc(w_hi + ks * 32), blo = kmajor_sw128_desc(w_lo + ks * 32);
-            umma_tf32(d_tmem, ahi, bhi, idesc, (kb | ks) != 0);
-            umma_tf32(d_tmem, alo, bhi, idesc, 1);
-            umma_tf32(d_tmem, ahi, blo, idesc, 1);
+            for (int ks = 0; ks < kBK / 8; ++ks) {  // +32 B per 8 tf32 of K inside the 128 B rows
+              const uint64_t ahi = kmajor_sw128_desc(l_hi + ks * 32), alo = kmajor_sw128_desc(l_lo + ks * 32);
+              const uint64_t bhi = kmajor_sw128_desc(w_hi + ks * 32), blo = kmajor_sw128_desc(w_lo + ks * 32);
+              if (PAIR) {
+                umma2_tf32(d_tmem, ahi, bhi, idesc, (kb | ks) != 0);
+                umma2_tf32(d_tmem, alo, bhi, idesc, 1);
+                umma2_tf32(d_tmem, ahi, blo, idesc, 1);
+              } else {
+                umma_tf32(d_tmem, ahi, bhi, idesc, (kb | ks) != 0);
+                umma_tf32(d_tmem, alo, bhi, idesc, 1);
+                umma_tf32(d_tmem, ahi, blo, idesc, 1);
+              }
+            }
+            if (PAIR) {
+              umma2_commit_both(&opempty[s]);
+              if (kb == nkb - 1) umma2_commit_both(&tfull[acc]);
+            } else {
+              umma_commit(&opempty[s]);
+              if (kb == nkb - 1) umma_commit(&tfull[acc]);
+            }
           }
-          umma_commit(&empty[s]);
-          if (kb == nkb - 1) umma_commit(&tfull[acc]);
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -262,42 +341,49 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (the 128 B swizzle spreads a warp's rows over all banks).
     const int d = threadIdx.x - 128;
     int g = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int t = unit; t < num_tiles; t += nunits) {
       for (int kb = 0; kb < nkb; ++kb, ++g) {
-        const int s = g % STAGES;
-        const uint32_t ph = (g / STAGES) & 1;
-        mbar_wait(&full[s], ph);
-        uint8_t* st = smem + s * SL::kStage;
-        const float* raw = reinterpret_cast<const float*>(st + SL::kRaw);
+        const int s = g % S, r = g % R;
+        mbar_wait(&rawfull[r], (g / R) & 1);
+        mbar_wait(&opempty[s], ((g / S) & 1) ^ 1);  // the MMAs of this stage's previous use are done
+        uint8_t* st = smem + s * RL::kOp;
+        const float* raw = reinterpret_cast<const float*>(smem + RL::kRawOff + r * RL::kL);
+        float v[kBK];
+#pragma unroll
+        for (int k = 0; k < kBK; ++k) v[k] = raw[k * kBM + d];
+        // raw tile consumed: order these generic-proxy reads before the Λ producer's next TMA
+        // (async-proxy) write into the same buffer, then release it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&rawfree[r]);
 #pragma unroll
         for (int j = 0; j < kBK / 4; ++j) {
           float h[4], l[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float v = raw[(4 * j + q) * kBM + d];
             uint32_t hb;
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v));
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v[4 * j + q]));
             h[q] = __uint_as_float(hb);
-            l[q] = v - h[q];
+            l[q] = v[4 * j + q] - h[q];
           }
           const int off = d * 128 + ((j ^ (d & 7)) << 4);
-          *reinterpret_cast<float4*>(st + SL::kHi + off) = make_float4(h[0], h[1], h[2], h[3]);
-          *reinterpret_cast<float4*>(st + SL::kLo + off) = make_float4(l[0], l[1], l[2], l[3]);
+          *reinterpret_cast<float4*>(st + RL::kLhi + off) = make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(st + RL::kLlo + off) = make_float4(l[0], l[1], l[2], l[3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&split[s]);
+        mbar_wait(&wfull[s], (g / S) & 1);  // this CTA's W tile landed too
+        if (PAIR) mbar_arrive_cta0(&split[s]);
+        else mbar_arrive(&split[s]);
       }
     }
   } else if (warp >= 8) {
     // ---------------- epilogue: TMEM -> registers -> global (coalesced along d) ----------------
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
     int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    for (int t = unit; t < num_tiles; t += nunits, ++it) {
       int b[4], m0, n0;
       decode(t, b, m0, n0);
       const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], aph);
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const int dd = m0 + q * 32 + lane;
       float* out_b = p.out + lin5l(p.out_c, b) + dd;
@@ -335,16 +421,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < 32; ++j) __stcs(oc + j * p.ldn_out, o[j]);
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (PAIR) mbar_arrive_cta0(&tempty[acc]);
+      else mbar_arrive(&tempty[acc]);
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(2 * BN < 32 ? 32 : 2 * BN));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(2 * BN < 32 ? 32 : 2 * BN));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(2 * BN < 32 ? 32 : 2 * BN));
   }
 }
 
@@ -369,18 +461,30 @@ EncodeTiledFn encode_fn() {
 
 int g_num_sms = 0;
 
-template <int BN, int STAGES>
-int launch_bn(const void* tm_lam, const void* tm_whi, const void* tm_wlo, const LamGemm& p, int grid,
-              cudaStream_t st) {
-  using SL = SmemLayout<BN, STAGES>;
+template <int BN, int S, int R, bool PAIR>
+int launch_ring(const void* tm_lam, const void* tm_whi, const void* tm_wlo, const LamGemm& p, int grid,
+                cudaStream_t st) {
+  using RL = Ring<BN, S, R, PAIR>;
+  auto kern = lam_gemm_kernel<BN, S, R, PAIR>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(lam_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, SL::kBytes);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RL::kBytes);
     attr = true;
   }
-  lam_gemm_kernel<BN, STAGES><<<grid, kThreads, SL::kBytes, st>>>(
-      *static_cast<const CUtensorMap*>(tm_lam), *static_cast<const CUtensorMap*>(tm_whi),
-      *static_cast<const CUtensorMap*>(tm_wlo), p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = RL::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr2[1];
+  attr2[0].id = cudaLaunchAttributeClusterDimension;
+  attr2[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr2[0].val.clusterDim.y = 1;
+  attr2[0].val.clusterDim.z = 1;
+  cfg.attrs = attr2;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, *static_cast<const CUtensorMap*>(tm_lam), *static_cast<const CUtensorMap*>(tm_whi),
+                     *static_cast<const CUtensorMap*>(tm_wlo), p);
   return 1;
 }
 
@@ -417,9 +521,36 @@ bool umma_tmap_wop(void* tm, const float* base, int K, int N, int P2, int P3, in
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool umma_pair_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("FG_2CTA");  // CTA-pair kernel: opt-in (slower than one CTA so far)
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, LamGemm p, int bn,
-                    cudaStream_t st) {
+                    cudaStream_t st, const void* tm2_whi, const void* tm2_wlo) {
   if (p.M % kBM || p.K % kBK || p.K0 % kBK || bn <= 0 || p.N % bn) return -1;
+  if (tm2_whi && tm2_wlo && p.M % (2 * kBM) == 0 && bn >= 64 && umma_pair_enabled()) {
+    if (!g_num_sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    p.tiles_m = p.M / kBM;
+    p.tiles_n = p.N / bn;
+    long long tiles = (long long)p.tiles_m * p.tiles_n * p.nb[0] * p.nb[1] * p.nb[2] * p.nb[3];
+    if (tiles <= 0 || tiles > 0x7fffffff) return -1;
+    p.num_tiles = (int)tiles;  // single-CTA tiles; the pair kernel walks tiles / 2 pair tiles
+    const int grid = 2 * (int)std::min<long long>(tiles / 2, g_num_sms / 2);
+    switch (bn) {
+      case 256: return launch_ring<256, 3, 2, true>(tm_lam, tm2_whi, tm2_wlo, p, grid, st);
+      case 128: return launch_ring<128, 4, 2, true>(tm_lam, tm2_whi, tm2_wlo, p, grid, st);
+      case 64: return launch_ring<64, 4, 3, true>(tm_lam, tm2_whi, tm2_wlo, p, grid, st);
+    }
+  }
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -432,10 +563,10 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
   p.num_tiles = (int)tiles;
   const int grid = (int)std::min<long long>(tiles, g_num_sms);
   switch (bn) {
-    case 256: return launch_bn<256, 2>(tm_lam, tm_whi, tm_wlo, p, grid, st);
-    case 128: return launch_bn<128, 2>(tm_lam, tm_whi, tm_wlo, p, grid, st);
-    case 64: return launch_bn<64, 3>(tm_lam, tm_whi, tm_wlo, p, grid, st);
-    case 32: return launch_bn<32, 3>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+    case 256: return launch_ring<256, 2, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+    case 128: return launch_ring<128, 3, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+    case 64: return launch_ring<64, 4, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+    case 32: return launch_ring<32, 4, 3, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
   }
   return -1;
 }
