@@ -234,6 +234,9 @@ def main():
                     help="sentences: independent sentences per GPU (weak scaling, no collective); columns: "
                          "perturbation columns of every sentence split over the GPUs, concretization partials "
                          "all-reduced with NCCL inside the pass (strong scaling; SURVEY 8(e) c5)")
+    ap.add_argument("--speculative", type=int, default=0, metavar="DEPTH",
+                    help="speculative eps bisection: DEPTH levels per batched round, the probes of a round "
+                         "split over the GPUs (latency mode for few sentences, e.g. c1; SURVEY 8(e))")
     args = ap.parse_args()
     w = CONFIGS[args.config]
     if args.warmup < 3 and args.impl == "ours":
@@ -254,13 +257,14 @@ def main():
     ctx = F.Context(local)
     model = F.Model(ctx, cfg, F.gen_synthetic(cfg, w.model_seed))
     columns = args.shard == "columns"
+    spec = args.speculative > 0
     if columns:
         D.shard_model_columns(model, dist)
 
     def batch(step):
         # globally unique sentence ids: rank-major blocks, warm-up steps first (no data-path collective);
         # column sharding: every rank works on the same sentences (its own slice of their columns)
-        ids = D.sentence_block(0 if columns else rank, step, args.steps + args.warmup, B)
+        ids = D.sentence_block(0 if (columns or spec) else rank, step, args.steps + args.warmup, B)
         xs = np.stack([F.gen_input(cfg, w.input_seed(i)) for i in ids])
         ps = np.stack([F.gen_positions(w.position_seed(i), w.length, w.words) for i in ids])
         return xs, ps
@@ -272,8 +276,13 @@ def main():
         if dist:
             dist.barrier()
 
+    def search(xs, ps):
+        if spec:
+            return model.maxeps_speculative(xs, ps, w.norm, w.eps_max, w.tol, depth=args.speculative, dist=dist)
+        return model.maxeps(xs, ps, w.norm, w.eps_max, w.tol, slots=B)
+
     for s in range(args.warmup):
-        model.maxeps(*inputs[s], w.norm, w.eps_max, w.tol, slots=B)
+        search(*inputs[s])
     barrier()
     dev_ms, calls, launches, passes, pass_ms = 0.0, [], 0, 0, []
     h2d = B * (w.length * w.embed * 8 + w.words * 4)
@@ -282,7 +291,7 @@ def main():
         barrier()
         t0 = time.perf_counter()
         for s in range(args.warmup, args.warmup + args.steps):
-            r = model.maxeps(*inputs[s], w.norm, w.eps_max, w.tol, slots=B)
+            r = search(*inputs[s])
             st = model.last_stats()
             dev_ms += st["device_ms"]
             launches += st["launches"]
@@ -295,7 +304,7 @@ def main():
         barrier()
         wall = time.perf_counter() - t0
     dev_ms_max, wall_max = D.max_over_ranks([dev_ms, wall], dist, device="cuda")
-    sentences = B * args.steps * (1 if columns else world)
+    sentences = B * args.steps * (1 if (columns or spec) else world)
     value = sentences / (dev_ms_max / 1e3)
     e2e = sentences / wall_max
     ms_pass_batched = statistics.mean(pass_ms)
@@ -304,13 +313,16 @@ def main():
     line = {
         "metric": "certified sentences/sec (eps binary search)", "value": value, "unit": "sentences/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
-        "higher_is_better": True, "scaling": "strong" if columns else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if (columns or spec) else "weak", "vs_baseline": None,
         "dtype": "f32+f64",
         "data": f"synthetic: gen_synthetic(seed {w.model_seed}) weights, gen_synthetic_input(2000+s), "
                 f"{w.words} perturbed word(s) at Rng(3000+s) positions",
-        "config": {**w.as_dict(), "global_batch": B * (1 if columns else world), "sentences_per_step_per_gpu": B,
+        "config": {**w.as_dict(), "global_batch": B * (1 if (columns or spec) else world),
+                   "sentences_per_step_per_gpu": B,
                    "parallelism": (f"column-sharded cp{world} (NCCL all-reduce of concretization partials)"
-                                   if columns else f"sentence-sharded dp{world}"),
+                                   if columns else
+                                   f"speculative bisection depth {args.speculative} over {world} GPU(s)" if spec
+                                   else f"sentence-sharded dp{world}"),
                    "l2_flush": "not needed: inputs larger than L2 (Λ working set "
                                f"{B * 0.45:.1f} GB per GPU >> 126 MB L2)"},
         "ms_per_bound_pass": {"batched_pass_ms": ms_pass_batched, "per_sentence_ms": ms_pass_sentence,

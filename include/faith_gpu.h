@@ -243,6 +243,22 @@ fg_status fg_loopback_create(int nranks, fg_loopback** out);
 void fg_loopback_destroy(fg_loopback* group);
 fg_status fg_model_shard_loopback(fg_model* model, fg_loopback* group, int rank);
 
+/* Speculative ε bisection: the same decision path as fg_maxeps /
+ * cmd_maxeps (cli.cpp:144-177), but each round evaluates a whole subtree of the next `depth`
+ * bisection levels (2^depth - 1 midpoints, computed with the sequential algorithm's own
+ * expressions) in one batched pass, then walks it -- the first round also carries the ε = 0
+ * and ε = eps_max probes.  Latency per sentence drops from 2 + n passes to about 1 + n/depth
+ * rounds for about 2^depth / depth times the work.  Multi-GPU: rank `rank` of `nranks`
+ * evaluates the probes whose index % nranks == rank and `exchange` combines the per-probe
+ * verdict words across ranks (element-wise MAX over ranks, in place; NULL when nranks == 1).
+ * calls_out = verification calls on the decision path (what cmd_maxeps reports),
+ * rounds_out = batched rounds used.  All ranks return identical results. */
+typedef int (*fg_exchange_fn)(void* user, int* verdicts, size_t count);
+fg_status fg_maxeps_spec(fg_model* model, int S, const double* x, const int* positions, int words, int norm,
+                         double eps_max, double tol, int depth, int rank, int nranks, fg_exchange_fn exchange,
+                         void* user, double* eps_out, int* calls_out, int* rounds_out, int* predicted_out,
+                         int* status_out);
+
 /* Synthetic model / inputs with the reference's seeded recipe (model.cpp:87-141):
  * gen_synthetic weights U(+-0.5/sqrt(fan_in)) rounded to f32, gen_synthetic_input
  * U(-0.5, 0.5); word positions = `words` distinct Rng(seed).uniform_index(length) draws,

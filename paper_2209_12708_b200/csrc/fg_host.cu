@@ -1561,6 +1561,178 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
 }
 
 
+// Speculative bisection (see faith_gpu.h).  Probe list per round and sentence:
+//   first round: eps = 0, eps = eps_max, then the subtree under [0, eps_max];
+//   later rounds: the subtree under the current [lo, hi].
+// Subtree nodes are enumerated level by level; a node (lo, hi) is a probe iff hi - lo > tol
+// (the sequential loop's condition), its midpoint is 0.5 * (lo + hi) exactly as in cli.cpp:168.
+namespace {
+struct SpecProbe {
+  int sent;
+  double eps;
+};
+struct SpecNode {
+  double lo, hi;
+};
+}  // namespace
+
+fg_status fg_maxeps_spec(fg_model* m, int S, const double* x, const int* positions, int words, int norm,
+                         double eps_max, double tol, int depth, int rank, int nranks, fg_exchange_fn exchange,
+                         void* user, double* eps_out, int* calls_out, int* rounds_out, int* predicted_out,
+                         int* status_out) {
+  fg_ctx* ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  if (S < 1 || words < 1 || words > m->cfg.length || depth < 1 || depth > 10 || nranks < 1 || rank < 0 ||
+      rank >= nranks || (nranks > 1 && !exchange))
+    return fail(ctx, FG_EINVAL, "fg_maxeps_spec: bad arguments");
+  if (!eps_ok(eps_max)) return fail(ctx, FG_EINVAL, "fg_maxeps_spec: eps_max must be finite and >= 0");
+  const int C = m->cfg.classes;
+  const int per_sent = 2 + (1 << depth) - 1;
+  const int total_max = S * per_sent;
+  const int mine_max = (total_max + nranks - 1) / nranks;
+  int slots = std::min(mine_max, default_slots(m, mine_max, words * m->cfg.embed));
+  slots = std::max(1, slots);
+  fg_status st = ensure_workspace(m, slots, words, S);
+  if (st) return st;
+  if ((st = stage_inputs(m, S, x, positions, words))) return st;
+  Workspace& w = m->ws;
+  std::vector<int> pred = predict_all(m, S, x);
+  enum { P_FIRST = 0, P_BISECT = 1, P_DONE = 2 };
+  std::vector<int> phase(S, P_FIRST);
+  std::vector<double> lo(S, 0.0), hi(S, eps_max);
+  std::vector<int> calls(S, 0);
+  for (int s = 0; s < S; ++s) status_out[s] = FG_OK;
+  int rounds = 0, done = 0;
+  uint64_t launches0 = ctx->launches;
+  double dev_ms = 0.0, sentence_passes = 0.0;
+  int passes = 0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  while (done < S) {
+    // ---- probes of this round
+    std::vector<SpecProbe> probes;
+    std::vector<std::vector<SpecNode>> trees(S);
+    std::vector<int> first_probe(S, -1), tree_base(S, -1);
+    for (int s = 0; s < S; ++s) {
+      if (phase[s] == P_DONE) continue;
+      first_probe[s] = (int)probes.size();
+      if (phase[s] == P_FIRST) {
+        probes.push_back({s, 0.0});
+        probes.push_back({s, eps_max});
+      }
+      tree_base[s] = (int)probes.size();
+      std::vector<SpecNode> level{{lo[s], hi[s]}};  // BFS: nodes of the next `depth` levels
+      for (int d = 0; d < depth && !level.empty(); ++d) {
+        std::vector<SpecNode> next;
+        for (const SpecNode& nd : level) {
+          if (!(nd.hi - nd.lo > tol)) continue;
+          const double mid = 0.5 * (nd.lo + nd.hi);
+          trees[s].push_back(nd);
+          probes.push_back({s, mid});
+          next.push_back({nd.lo, mid});
+          next.push_back({mid, nd.hi});
+        }
+        level.swap(next);
+      }
+    }
+    // ---- evaluate this rank's share in batched passes of `slots` probes
+    std::vector<int> verdict(probes.size(), 0);
+    std::vector<int> mine;
+    for (int i = rank; i < (int)probes.size(); i += nranks) mine.push_back(i);
+    for (size_t b0 = 0; b0 < mine.size(); b0 += slots) {
+      const size_t nb = std::min(mine.size() - b0, (size_t)slots);
+      for (int i = 0; i < slots; ++i) {
+        const SpecProbe& pr = probes[mine[b0 + std::min((size_t)i, nb - 1)]];
+        w.h_slot[i] = pr.sent;
+        w.h_eps[i] = pr.eps;
+      }
+      float ms = 0.f;
+      if ((st = run_pass(m, norm, e0, e1, &ms))) break;
+      dev_ms += ms;
+      ++passes;
+      sentence_passes += (double)nb;
+      for (size_t i = 0; i < nb; ++i) {
+        const int pi = mine[b0 + i];
+        const fg_status ps = decode_status(w.h_status[i]);
+        int ok = 0;
+        if (ps == FG_OK)
+          fg_check_robust((size_t)C, w.h_logits + i * C, w.h_logits + (size_t)slots * C + i * C,
+                          (size_t)pred[probes[pi].sent], 0.0, &ok);
+        verdict[pi] = ps != FG_OK ? 10 + ps : (ok ? 2 : 1);
+      }
+    }
+    if (st) break;
+    if (nranks > 1 && exchange(user, verdict.data(), verdict.size()) != 0) {
+      st = fail(ctx, FG_ERUNTIME, "fg_maxeps_spec: verdict exchange failed");
+      break;
+    }
+    ++rounds;
+    // ---- walk each sentence's probes along the sequential decision path
+    for (int s = 0; s < S; ++s) {
+      if (phase[s] == P_DONE) continue;
+      const int pi = first_probe[s];
+      bool finished = false;
+      if (phase[s] == P_FIRST) {
+        const int v0 = verdict[pi], vmax = verdict[pi + 1];
+        calls[s] = 1;
+        if (v0 >= 10) {  // verified_at(0, tolerate = false) rethrows (cli.cpp:146-156)
+          status_out[s] = v0 - 10;
+          finished = true;
+        } else if (v0 != 2) {
+          status_out[s] = FG_ERUNTIME;  // misclassified input (cli.cpp:159-161)
+          finished = true;
+        } else {
+          calls[s] = 2;
+          if (vmax == 2) {
+            lo[s] = eps_max;
+            finished = true;
+          } else {
+            lo[s] = 0.0;
+            hi[s] = eps_max;
+            phase[s] = P_BISECT;
+          }
+        }
+      }
+      if (!finished) {
+        // follow the decision path through this round's subtree (nodes matched by interval)
+        const std::vector<SpecNode>& tr = trees[s];
+        double l = lo[s], h = hi[s];
+        for (int d = 0; d < depth; ++d) {
+          if (!(h - l > tol)) break;
+          int k = -1;
+          for (size_t i = 0; i < tr.size(); ++i)
+            if (tr[i].lo == l && tr[i].hi == h) {
+              k = (int)i;
+              break;
+            }
+          if (k < 0) break;
+          const double mid = 0.5 * (l + h);
+          ++calls[s];
+          if (verdict[tree_base[s] + k] == 2) l = mid;
+          else h = mid;
+        }
+        lo[s] = l;
+        hi[s] = h;
+        if (!(h - l > tol)) finished = true;
+      }
+      if (finished) {
+        phase[s] = P_DONE;
+        eps_out[s] = status_out[s] == FG_OK ? lo[s] : std::numeric_limits<double>::quiet_NaN();
+        calls_out[s] = calls[s];
+        ++done;
+      }
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  for (int s = 0; s < S; ++s) predicted_out[s] = pred[s];
+  *rounds_out = rounds;
+  m->stats = fg_run_stats{dev_ms, passes ? dev_ms / passes : 0.0, passes, slots, ctx->launches - launches0,
+                          sentence_passes};
+  return st;
+}
+
 }  // extern "C"
 
 // ---- synthetic model / inputs: the reference's seeded generators (model.cpp:87-141,

@@ -149,6 +149,8 @@ def load_library():
     L.fg_loopback_destroy.argtypes = [vp]
     L.fg_model_shard_loopback.argtypes = [vp, vp, C.c_int]
     L.fg_model_set_column_shard.argtypes = [vp, C.c_int, C.c_int, vp, vp, C.c_int]
+    L.fg_maxeps_spec.argtypes = [vp, C.c_int, _dp, _ip, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
+                                 C.c_int, C.c_int, EXCHANGE_FN, vp, _dp, _ip, _ip, _ip, _ip]
     _lib = L
     return L
 
@@ -170,6 +172,8 @@ def _bounds(b) -> LinearBounds:
 
 
 PRECISION = {"f32": 0, "f64": 1}
+# int (*fg_exchange_fn)(void* user, int* verdicts, size_t count): element-wise MAX over ranks, in place
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int), C.c_size_t)
 
 
 class Context:
@@ -569,6 +573,36 @@ class Model:
         self.ctx._check(self.lib.fg_maxeps(self.handle, S, _d(x), _i(pos), pos.shape[1], NORM[norm], eps_max, tol,
                                            slots, _d(eps), _i(calls), _i(pred), _i(st)), "fg_maxeps")
         return {"eps": eps, "calls": calls, "predicted": pred, "status": st}
+
+    def maxeps_speculative(self, x, positions, norm: str, eps_max: float = 1.0, tol: float = 1e-3, depth: int = 3,
+                           dist=None):
+        """fg_maxeps_spec: cmd_maxeps's decision path, `depth` bisection levels per batched round.
+        With a torch.distributed group `dist`, the probes of each round are split across ranks and
+        the verdicts combined with an all-reduce(MAX) -> dict(eps, calls, rounds, predicted, status)."""
+        x, pos = self._inputs(x, positions)
+        S = x.shape[0]
+        eps = np.zeros(S)
+        calls, pred, st = (np.zeros(S, dtype=np.int32) for _ in range(3))
+        rounds = np.zeros(1, dtype=np.int32)
+        rank, world, cb = 0, 1, EXCHANGE_FN()
+        if dist is not None and dist.get_world_size() > 1:
+            import torch
+            rank, world = dist.get_rank(), dist.get_world_size()
+
+            def _exchange(user, buf, count):
+                t = torch.from_numpy(np.ctypeslib.as_array(buf, shape=(count,)).copy())
+                if dist.get_backend() == "nccl":
+                    t = t.cuda()
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                np.ctypeslib.as_array(buf, shape=(count,))[:] = t.cpu().numpy()
+                return 0
+
+            cb = EXCHANGE_FN(_exchange)
+        self._spec_cb = cb  # keep the callback alive during the call
+        self.ctx._check(self.lib.fg_maxeps_spec(self.handle, S, _d(x), _i(pos), pos.shape[1], NORM[norm], eps_max,
+                                                tol, depth, rank, world, cb, None, _d(eps), _i(calls), _i(rounds),
+                                                _i(pred), _i(st)), "fg_maxeps_spec")
+        return {"eps": eps, "calls": calls, "rounds": int(rounds[0]), "predicted": pred, "status": st}
 
     def profile_pass(self, norm: str, eps: float) -> dict:
         """One eager pass with CUDA events around every launch site -> {site: (ms, kernels)}."""
