@@ -9,6 +9,9 @@
 //             --seed S --model OUT.json [--input-seed S2 --input OUT2.json]
 //   verify    --model M --input X --eps E --norm l1|l2|linf [--margin m] [--naive] [--out R.json]
 //   maxeps    --model M --input X --norm N [--tol t] [--eps-max e] [--out R.json]
+// and, in the GPU build (-DFAITH_FUSED), the pass-level fast path on the same files:
+//   verify-fused / maxeps-fused   same options, faith::gpu::FusedVerifier (whole bound passes on
+//                                 the B200, f32 Λ + f64 O(N) state), same output lines
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -17,6 +20,9 @@
 
 #include "faith/cli.hpp"
 #include "faith/model.hpp"
+#ifdef FAITH_FUSED
+#include "faith_fused.hpp"
+#endif
 
 using namespace faith;
 
@@ -72,6 +78,25 @@ int main(int argc, char** argv) {
       o.eps_max = std::stod(get("eps-max", "1.0"));
       return cli::cmd_maxeps(o);
     }
+#ifdef FAITH_FUSED
+    if (cmd == "verify-fused" || cmd == "maxeps-fused") {
+      model::TransformerSpec spec = model::load_model(get("model", ""));
+      Tensor x = model::load_embedding(get("input", ""));
+      gpu::FusedVerifier fv(spec);
+      const Norm p = norm_from_name(get("norm", "linf"));
+      if (cmd == "verify-fused") {
+        const double eps = std::stod(get("eps", "0"));
+        bool bounded = true;
+        std::size_t cls = 0;
+        const bool ok = fv.certify(x, p, eps, std::stod(get("margin", "0")), &cls, nullptr, &bounded);
+        std::printf("%s eps=%g norm=%s class=%zu\n", ok ? "verified" : "not verified", eps, norm_name(p).c_str(), cls);
+        return ok ? 0 : 1;
+      }
+      auto r = fv.max_epsilon({x}, p, std::stod(get("eps-max", "1.0")), std::stod(get("tol", "1e-3")));
+      std::printf("max verified epsilon = %g (%zu calls)\n", r[0].epsilon, r[0].calls);
+      return 0;
+    }
+#endif
   } catch (const std::exception& e) {
     std::fprintf(stderr, "%s: %s\n", cmd.c_str(), e.what());
     return 2;

@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 REF_INCLUDE = os.environ.get("FAITH_REF_INCLUDE", "/root/reference/proj/include")
-COMPAT_SRC = os.path.join(HERE, "compat", "faith_compat.cpp")
+COMPAT_SRCS = [os.path.join(HERE, "compat", f) for f in ("faith_compat.cpp", "faith_fused.cpp")]
+COMPAT_HDRS = [os.path.join(HERE, "compat", "faith_fused.hpp")]
 COMPAT_LIB = os.path.join(LIBDIR, "libfaith_compat.so")
 
 
@@ -70,9 +71,9 @@ def build_compat(force: bool = False) -> str | None:
         return COMPAT_LIB if os.path.exists(COMPAT_LIB) else None
     build(force=force)
     if force or not os.path.exists(COMPAT_LIB) or os.path.getmtime(COMPAT_LIB) < max(
-            os.path.getmtime(COMPAT_SRC), os.path.getmtime(LIB)):
+            [os.path.getmtime(f) for f in COMPAT_SRCS + COMPAT_HDRS] + [os.path.getmtime(LIB)]):
         _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra", "-I" + REF_INCLUDE,
-              "-I" + os.path.join(ROOT, "include"), COMPAT_SRC, "-o", COMPAT_LIB, "-L" + LIBDIR, "-lfaith_gpu",
+              "-I" + os.path.join(ROOT, "include"), *COMPAT_SRCS, "-o", COMPAT_LIB, "-L" + LIBDIR, "-lfaith_gpu",
               "-Wl,-rpath,$ORIGIN"])
     return COMPAT_LIB
 

@@ -91,3 +91,25 @@ def test_cmd_maxeps_f32_mode_within_tolerance(tmp_path):
     ea = float(re.search(r"= ([0-9.e+-]+)", a.stdout).group(1))
     eb = float(re.search(r"= ([0-9.e+-]+)", b.stdout).group(1))
     assert abs(ea - eb) <= 1e-3 * ea + 1e-5, (ea, eb)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_fused_pass_on_reference_models(tmp_path, case):
+    """The pass-level fast path (faith::gpu::FusedVerifier: whole fused bound passes, f32 Λ) on the
+    reference's own model/embedding files and whole-embedding ε-ball: same verdicts as the CPU
+    reference's cmd_verify and max ε within 1e-3 relative (+ tol) of its cmd_maxeps."""
+    _need(CLI_GPU, CLI_REF)
+    name, layers, heads, embed, ffn, length, act, norm, eps = case
+    m, x = _gen(str(tmp_path), name, layers, heads, embed, ffn, length, act, 4242)
+    for e in (0.0, eps, 10 * eps):
+        a = _run([CLI_REF, "verify", "--model", m, "--input", x, "--eps", str(e), "--norm", norm])
+        b = _run([CLI_GPU, "verify-fused", "--model", m, "--input", x, "--eps", str(e), "--norm", norm])
+        assert a.returncode == b.returncode and a.stdout.split()[0] == b.stdout.split()[0], (a.stdout, b.stdout,
+                                                                                              b.stderr)
+    args = ["--model", m, "--input", x, "--norm", norm, "--tol", "1e-5", "--eps-max", "1.0"]
+    a = _run([CLI_REF, "maxeps"] + args)
+    b = _run([CLI_GPU, "maxeps-fused"] + args)
+    assert a.returncode == b.returncode == 0, (a.stderr, b.stderr)
+    ea = float(re.search(r"= ([0-9.e+-]+)", a.stdout).group(1))
+    eb = float(re.search(r"= ([0-9.e+-]+)", b.stdout).group(1))
+    assert abs(ea - eb) <= 1e-3 * ea + 1e-5, (a.stdout, b.stdout)
