@@ -159,6 +159,7 @@ struct LamGemm {
   float alpha;
   int accumulate;
   int tiles_m, tiles_n, num_tiles;  // set by launch_lam_gemm
+  int epi_groups;                   // epilogue warp groups draining tiles (1 or 2; launch_lam_gemm)
 };
 bool umma_available();
 int umma_pick_bn(int N);  // 256 / 128 / 64, or 0 when N is not a multiple of 64

@@ -21,7 +21,8 @@
 //   warps 4-7  split warps: raw Λ [k][d] -> L_hi, L_lo [d][k] K-major SWIZZLE_128B
 //              (transposed: kind::tf32 with an MN-major operand returned zeros on B200,
 //              profiles/r1_umma_major_probe.txt)
-//   warps 8-11 epilogue: tcgen05.ld TMEM -> registers -> coalesced st.global (+acc/+residual)
+//   warps 8-15 epilogue, two groups (one per TMEM accumulator): tcgen05.ld TMEM -> registers
+//              -> coalesced st.global (+acc/+residual, prefetched)
 // Pipelines: SMEM stages full/split/empty mbarriers; TMEM accumulators double-buffered.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -38,7 +39,7 @@ namespace {
 
 constexpr int kBM = 128;  // d rows per tile (TMEM lanes)
 constexpr int kBK = 32;   // 32 fp32 = 128 B rows: one SWIZZLE_128B atom width
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;  // 4 role warps, 4 split warps, 2 x 4 epilogue warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -168,7 +169,7 @@ struct Ring {
 // barrier (split warps wait for their CTA's W tile before arriving), accumulator drain on the
 // leader's `tempty`.
 //   warp 0: W producer    warp 1: TMEM alloc + MMA issuer    warp 2: Λ producer
-//   warps 4-7: split/transpose Λ -> L_hi/L_lo    warps 8-11: epilogue
+//   warps 4-7: split/transpose Λ -> L_hi/L_lo    warps 8-15: epilogue (2 groups)
 template <int BN, int S, int R, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     lam_gemm_kernel(const __grid_constant__ CUtensorMap tm_lam, const __grid_constant__ CUtensorMap tm_whi,
@@ -377,48 +378,76 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 8) {
     // ---------------- epilogue: TMEM -> registers -> global (coalesced along d) ----------------
+    // The operand added to the accumulator (the previous value when accumulating, else the
+    // residual) is software-prefetched: chunk 0 before waiting for the accumulator (its load
+    // latency overlaps the tile's MMAs), chunk c+1 while chunk c is finished.
+    // Two epilogue groups (warps 8-11, 12-15), one per TMEM accumulator: group g drains the
+    // tiles with it % 2 == g, so two tiles' read-modify-write epilogues are in flight.
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
+    const int grp = (warp - 8) >> 2;
+    const bool has_x = p.accumulate || p.res;
+    const long long xld = p.accumulate ? p.ldn_out : p.ldn_res;
     int it = 0;
     for (int t = unit; t < num_tiles; t += nunits, ++it) {
+      if (p.epi_groups == 2 ? ((it & 1) != grp) : (grp != 0)) continue;
       int b[4], m0, n0;
       decode(t, b, m0, n0);
       const int acc = it & 1;
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
-      tc_fence_after();
       const int dd = m0 + q * 32 + lane;
       float* out_b = p.out + lin5l(p.out_c, b) + dd;
       const float* res = p.res ? p.res + lin5l(p.res_c, b) + (long long)n0 * p.ldn_res + dd : nullptr;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      auto chunk_out = [&](int c) -> float* {
         const int n = n0 + c * 32;
         float* out = p.n_split ? out_b + (long long)(n / p.n_split) * p.split_stride +
                                      (long long)(n % p.n_split) * p.ldn_out - (long long)c * 32 * p.ldn_out
                                : out_b + (long long)n0 * p.ldn_out;
+        return out + (long long)c * 32 * p.ldn_out;
+      };
+      auto chunk_x = [&](int c) -> const float* {
+        return p.accumulate ? chunk_out(c) : res + (long long)c * 32 * p.ldn_res;
+      };
+      // two chunks of the added operand in flight before the accumulator is ready, then a
+      // rolling refill two chunks ahead (register double buffer pa / pb)
+      constexpr int NCH = BN / 32;
+      float pa[32], pb[32];
+      auto load_x = [&](int c, float (&dst)[32]) {
+        const float* xs = chunk_x(c);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) dst[j] = xs[j * xld];
+      };
+      auto finish = [&](int c, const float (&xv)[32]) {
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
-        // all loads of the chunk are issued before its first store (out/res may alias as far
-        // as the compiler knows: interleaving would serialize 32 global round trips)
+        float* oc = chunk_out(c);
         float o[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) o[j] = p.alpha * __uint_as_float(v[j]);
-        float* oc = out + (long long)c * 32 * p.ldn_out;
-        if (p.accumulate) {
-          float old[32];
+        if (has_x) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) old[j] = oc[j * p.ldn_out];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] += old[j];
+          for (int j = 0; j < 32; ++j) o[j] += xv[j];
         }
-        if (res) {
+        if (p.accumulate && res) {  // both (unused by the pass): residual loaded directly
           const float* rc = res + (long long)c * 32 * p.ldn_res;
-          float rr[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) rr[j] = __ldg(rc + j * p.ldn_res);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] += rr[j];
+          for (int j = 0; j < 32; ++j) o[j] += rc[j * p.ldn_res];
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) __stcs(oc + j * p.ldn_out, o[j]);
+      };
+      if (has_x) {
+        load_x(0, pa);
+        if (NCH > 1) load_x(1, pb);
+      }
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < NCH; c += 2) {
+        finish(c, pa);
+        if (has_x && c + 2 < NCH) load_x(c + 2, pa);
+        if (c + 1 < NCH) {
+          finish(c + 1, pb);
+          if (has_x && c + 3 < NCH) load_x(c + 3, pb);
+        }
       }
       tc_fence_before();
       if (PAIR) mbar_arrive_cta0(&tempty[acc]);
@@ -532,6 +561,14 @@ bool umma_pair_enabled() {
 
 int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, LamGemm p, int bn,
                     cudaStream_t st, const void* tm2_whi, const void* tm2_wlo) {
+  {
+    static int groups = 0;
+    if (!groups) {
+      const char* e = std::getenv("FG_EPI_GROUPS");
+      groups = (e && e[0] == '1') ? 1 : 2;
+    }
+    p.epi_groups = groups;
+  }
   if (p.M % kBM || p.K % kBK || p.K0 % kBK || bn <= 0 || p.N % bn) return -1;
   if (tm2_whi && tm2_wlo && p.M % (2 * kBM) == 0 && bn >= 64 && umma_pair_enabled()) {
     if (!g_num_sms) {
@@ -565,7 +602,8 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
   switch (bn) {
     case 256: return launch_ring<256, 2, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
     case 128: return launch_ring<128, 3, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
-    case 64: return launch_ring<64, 4, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+    // skinny K / small N (McCormick y-side terms): HBM-bound, so a deep Λ ring
+    case 64: return launch_ring<64, 2, 6, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
     case 32: return launch_ring<32, 4, 3, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
   }
   return -1;
