@@ -183,6 +183,10 @@ fg_status fg_model_create(fg_ctx* ctx, const fg_config* cfg, const double* param
 void fg_model_destroy(fg_model* model);
 /* Exact f64 forward pass (model::forward, model.cpp:566-571) -> logits[classes]; host. */
 fg_status fg_forward(fg_model* model, const double* x, double* logits);
+/* The same function for N inputs on the GPU (f64 kernels, FMA-contracted: agrees with the
+ * host forward to ~1e-13 relative): the soundness oracle for sampled perturbations at full
+ * model sizes.  x [N, L, E] host, logits [N, classes] host. */
+fg_status fg_forward_batch(fg_model* model, int N, const double* x, double* logits);
 
 /* One word-level verification pass (graph::evaluate over fuse_all(build_graph), graph.cpp:
  * 505-673) for S independent sentences.  x [S, L, E] host f64; positions [S, words];

@@ -25,6 +25,7 @@ SOURCES = {
     "fg_host.cu": [],
     "fg_ops64.cu": [],
     "fg_shard.cu": [],
+    "fg_forward.cu": [],
 }
 
 

@@ -1353,6 +1353,40 @@ fg_status fg_forward(fg_model* m, const double* x, double* logits) {
   return FG_OK;
 }
 
+fg_status fg_forward_batch(fg_model* m, int N, const double* x, double* logits) {
+  fg_ctx* ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  if (N < 1) return fail(ctx, FG_EINVAL, "fg_forward_batch: N must be >= 1");
+  const fg_config& c = m->cfg;
+  const long long L = c.length, E = c.embed, F = c.ffn, C = c.classes, rows = (long long)N * L;
+  cudaStream_t st = ctx->stream;
+  DBuf X, QKV, CT, FF, LG;
+  CK(X.alloc(sizeof(double) * rows * E));
+  CK(QKV.alloc(sizeof(double) * rows * 3 * E));
+  CK(CT.alloc(sizeof(double) * rows * E));
+  CK(FF.alloc(sizeof(double) * rows * F));
+  CK(LG.alloc(sizeof(double) * N * C));
+  CK(cudaMemcpyAsync(X.p, x, sizeof(double) * rows * E, cudaMemcpyHostToDevice, st));
+  double *xd = X.as<double>(), *qkv = QKV.as<double>(), *ct = CT.as<double>(), *ff = FF.as<double>();
+  for (int l = 0; l < c.layers; ++l) {
+    const DevLayer& L_ = m->layers[l];
+    LAUNCH(launch_dense_f64(xd, L_.qkv.w64.as<double>(), L_.qkv.b64.as<double>(), nullptr, qkv, rows, (int)E,
+                            (int)(3 * E), -1, st));
+    LAUNCH(launch_attention_f64(qkv, ct, N, (int)L, (int)E, c.heads, st));
+    LAUNCH(launch_dense_f64(ct, L_.wo.w64.as<double>(), L_.wo.b64.as<double>(), xd, xd, rows, (int)E, (int)E, -1,
+                            st));
+    LAUNCH(launch_dense_f64(xd, L_.w1.w64.as<double>(), L_.w1.b64.as<double>(), nullptr, ff, rows, (int)E, (int)F,
+                            c.activation, st));
+    LAUNCH(launch_dense_f64(ff, L_.w2.w64.as<double>(), L_.w2.b64.as<double>(), xd, xd, rows, (int)F, (int)E, -1,
+                            st));
+  }
+  LAUNCH(launch_pool_head_f64(xd, m->wc64.as<double>(), m->bc64.as<double>(), LG.as<double>(), N, (int)L, (int)E,
+                              (int)C, st));
+  CK(cudaMemcpyAsync(logits, LG.p, sizeof(double) * N * C, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return FG_OK;
+}
+
 size_t fg_node_dump_size(const fg_config* c) {
   size_t L = c->length, E = c->embed, H = c->heads, F = c->ffn;
   return c->layers * (8 * L * E + 4 * H * L * L + 2 * H * L + 2 * L * F) + E + c->classes;

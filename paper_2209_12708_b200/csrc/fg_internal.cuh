@@ -242,4 +242,11 @@ int launch_head_partial(const double* pc, const double* pr, const double* plb, c
 int launch_head_finish(const double* part, const double* bias, int S, int C, int norm, const double* eps,
                        double* out_lo, double* out_hi, int* status, int site, cudaStream_t st);
 
+// ---- exact f64 forward on the GPU (fg_forward.cu): the soundness oracle at full sizes ----
+int launch_dense_f64(const double* X, const double* W, const double* b, const double* R, double* Y, long long rows,
+                     int C, int O, int act, cudaStream_t st);  // act: RELAX_RELU/TANH/SILU or -1
+int launch_attention_f64(const double* qkv, double* ctx, long long N, int L, int E, int H, cudaStream_t st);
+int launch_pool_head_f64(const double* x, const double* wc, const double* bc, double* logits, long long N, int L,
+                         int E, int C, cudaStream_t st);
+
 }  // namespace fg

@@ -121,6 +121,7 @@ def load_library():
     L.fg_model_create.argtypes = [vp, C.POINTER(FgConfig), _dp, C.POINTER(vp)]
     L.fg_model_destroy.argtypes = [vp]
     L.fg_forward.argtypes = [vp, _dp, _dp]
+    L.fg_forward_batch.argtypes = [vp, C.c_int, _dp, _dp]
     L.fg_node_dump_size.restype = sz
     L.fg_node_dump_size.argtypes = [C.POINTER(FgConfig)]
     L.fg_bound_pass.argtypes = [vp, C.c_int, _dp, _ip, C.c_int, C.c_int, _dp, _dp, _dp, _ip]
@@ -528,6 +529,13 @@ class Model:
         if pos.shape[0] != x.shape[0]:
             raise InvalidArgument("positions / inputs batch mismatch")
         return x, pos
+
+    def forward_batch(self, xs) -> np.ndarray:
+        """fg_forward_batch: exact f64 forward of N inputs [N, L*E] on the GPU -> logits [N, C]."""
+        xs = _f64(xs).reshape(-1, self.cfg.length * self.cfg.embed)
+        out = np.zeros((xs.shape[0], self.cfg.classes))
+        self.ctx._check(self.lib.fg_forward_batch(self.handle, xs.shape[0], _d(xs), _d(out)), "fg_forward_batch")
+        return out
 
     def bound_pass(self, x, positions, norm: str, eps):
         """fg_bound_pass -> (logits_lo [S,C], logits_hi [S,C], status [S])."""

@@ -1,1 +1,3 @@
-for cfg in "0 32" "0 64" "0 128" "1 32" "1 64" "1 128"; do set -- $cfg; echo "persist=$1 tile=$2"; FG_SM3_TRACE=1 FG_SM3_PERSIST=$1 FG_SM3_TILE_KB=$2 python tools/prof_pass.py --passes 1 2>&1 | grep -A5 "sm3 cs" | tail -6; done
+for i in 1 2; do
+for cfg in "0 64" "0 128" "1 64" "1 128" "1 32"; do set -- $cfg; echo "persist=$1 tile=$2"; FG_SM3_PERSIST=$1 FG_SM3_TILE_KB=$2 timeout 120 python tools/prof_pass.py --passes 1 2>&1 | grep sites | sed 's/.*softmax/softmax/' | cut -c1-22; done
+done
