@@ -8,7 +8,7 @@ oracle/Makefile) on the BASELINE workloads and writes small fixtures:
                         (float32; strided subsample for c3) in fo_bound_pass order
   <cfg>_maxeps_s<s>.json cmd_maxeps result (ε, verification calls, predicted class)
 
-Usage: python oracle/make_golden.py c1|c2|c3 [--what pass|maxeps] [--sentence S]
+Usage: python oracle/make_golden.py c1|c2|c3|c4m [--what pass|maxeps] [--sentence S]
 """
 import argparse, json, os, sys, time
 import numpy as np
@@ -16,10 +16,10 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from oracle.oracle import Oracle, ModelConfig  # noqa: E402
-from paper_2209_12708_b200.configs import CONFIGS  # noqa: E402
+from paper_2209_12708_b200.configs import ALL as CONFIGS  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden")
-STRIDE = {"c1": 1, "c2": 1, "c3": 7}
+STRIDE = {"c1": 1, "c2": 1, "c3": 7, "c4m": 31}
 
 
 def model_config(w):

@@ -32,7 +32,7 @@ class Workload:
 
     @property
     def model_seed(self) -> int:
-        return 1000 + int(self.name[1:])
+        return 1000 + int("".join(ch for ch in self.name[1:] if ch.isdigit()))
 
     @property
     def pert_dim(self) -> int:
@@ -67,3 +67,13 @@ CONFIGS = {
     "c5": Workload("c5", 12, 12, 768, 3072, 128, 2, "l2", 0.001, 8,
                    description="12-layer BERT-base-shaped d=768 12 heads ffn=3072, seq 128, two words l2"),
 }
+
+
+# Shape-coverage workloads for the parity tests (not benchmarks): the c4/c5 structure (8 heads,
+# 128 tokens) at sizes the reference itself evaluates in minutes on one core, so their golden
+# vectors come from the unmodified reference build (oracle/make_golden.py).
+SHAPE_CHECKS = {
+    "c4m": Workload("c4m", 2, 8, 256, 512, 128, 1, "linf", 1e-4, 1,
+                    description="c4-shaped mini: 2 layers d=256 8 heads ffn=512, seq 128, one word linf"),
+}
+ALL = {**CONFIGS, **SHAPE_CHECKS}

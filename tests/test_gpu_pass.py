@@ -11,7 +11,7 @@ import pytest
 from helpers import close, model_config, sample_in_ball
 from oracle.oracle import ModelConfig as OCfg, node_layout
 from paper_2209_12708_b200 import faith_gpu as F
-from paper_2209_12708_b200.configs import CONFIGS
+from paper_2209_12708_b200.configs import ALL as CONFIGS
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")

@@ -11,7 +11,7 @@ import pytest
 
 from helpers import model_config, random_bounds, random_consistent_bounds
 from oracle.oracle import ModelConfig, node_layout
-from paper_2209_12708_b200.configs import CONFIGS
+from paper_2209_12708_b200.configs import ALL as CONFIGS
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -164,8 +164,8 @@ def test_port_matches_golden_pass(port, path):
     name = os.path.basename(path).split("_")[0]
     s = int(os.path.basename(path).split("_s")[1].split(".")[0])
     w = CONFIGS[name]
-    if name == "c3" and not os.environ.get("FAITH_SLOW_TESTS"):
-        pytest.skip("c3 reference pass takes minutes on one core (set FAITH_SLOW_TESTS=1)")
+    if name in ("c3", "c4m") and not os.environ.get("FAITH_SLOW_TESTS"):
+        pytest.skip(f"{name} reference pass takes minutes on one core (set FAITH_SLOW_TESTS=1)")
     cfg = model_config(w)
     params = port.gen_model(cfg, w.model_seed)
     x = port.gen_input(cfg, w.input_seed(s))
