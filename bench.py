@@ -61,10 +61,12 @@ def peaks():
 # algorithmic work per sentence-pass
 # ---------------------------------------------------------------------------
 def affine_flops(w) -> float:
-    """Useful flops of the bound GEMMs: 4*L*C*O*D per affine (both bounds, one product each)."""
+    """Useful flops of the bound GEMMs: 4*L*C*O*D per affine (both bounds, one product each).
+    The first layer's Q/K/V affine acts on the one-hot Λ0 and is a scatter of W, not a GEMM
+    (DESIGN.md §5), so it is not counted."""
     L, E, F, D = w.length, w.embed, w.ffn, w.pert_dim
     per_layer = 4.0 * L * D * (E * 3 * E + E * E + E * F + F * E)
-    return w.layers * per_layer
+    return w.layers * per_layer - 4.0 * L * D * E * 3 * E
 
 
 def site_bytes(w) -> dict:
@@ -354,7 +356,8 @@ def main():
             "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
             "frac": (ach / pk["bf16_tflops"]) if ach else None, "traffic": traffic,
             "peak_source": f"{pk_kind} dense bf16 (MEASURED_PEAKS.json)",
-            "algorithmic": f"{affine_flops(w):.4g} useful flop per sentence-pass x {B} sentences per launch set",
+            "algorithmic": f"{affine_flops(w):.4g} useful flop per sentence-pass (4*L*C*O*D per GEMM affine; "
+                           f"layer-1 Q/K/V is a one-hot scatter) x {B} sentences per launch set",
             "launches_per_pass": gemm_k, "share_of_pass": gemm_ms / total if total else None,
         }
         mem = {}

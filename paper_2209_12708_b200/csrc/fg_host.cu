@@ -840,6 +840,11 @@ struct Dumper {
   }
 };
 
+bool onehot_first_layer() {
+  const char* e = std::getenv("FG_NO_ONEHOT");
+  return !(e && e[0] == '1');
+}
+
 // All-reduce of concretization partials across the column shards (stream-ordered).
 fg_status shard_allreduce(fg_model* m, double* buf, size_t count, int norm) {
   fg_ctx* ctx = m->ctx;
@@ -902,7 +907,9 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
 
   g_tag = "init";
   LAUNCH(launch_fill_int(status, kStatusClear, S, st));
-  LAUNCH(launch_init_input(X, w.crX, X_lb, X_ub, w.x_all.as<double>(), w.pos_all.as<int>(),
+  // Λ0 is one-hot: the first layer consumes it analytically (no Λ0 in HBM) unless dumping
+  const bool onehot = !dump && onehot_first_layer();
+  LAUNCH(launch_init_input(onehot ? nullptr : X, w.crX, X_lb, X_ub, w.x_all.as<double>(), w.pos_all.as<int>(),
                            w.slot_map.as<int>(), S, L, E, w.W, st, D, w.col0));
   const bool sharded = m->shard.active();
   for (int l = 0; l < c.layers; ++l) {
@@ -910,8 +917,13 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     const size_t base = (size_t)l * per_layer;
     // Q, K, V = propagate_affine(cur, Wq|Wk|Wv)   (one N=3E affine)
     g_tag = "affine_gemm";
-    LAUNCH(launch_affine_lambda(lw.qkv, w.tm_ok ? &w.tm_X : nullptr, X, w.crX, QKV, w.crQKV, nullptr, 0,
-                                (long long)S * L, D, st));
+    if (l == 0 && onehot) {
+      LAUNCH(launch_onehot_affine(QKV, w.crQKV, lw.qkv.w32.as<float>(), w.pos_all.as<int>(), w.slot_map.as<int>(), S,
+                                  L, E, 3 * E, w.W, D, w.col0, st));
+    } else {
+      LAUNCH(launch_affine_lambda(lw.qkv, w.tm_ok ? &w.tm_X : nullptr, X, w.crX, QKV, w.crQKV, nullptr, 0,
+                                  (long long)S * L, D, st));
+    }
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(X_lb, X_ub, lw.qkv.w64.as<double>(), lw.qkv.b64.as<double>(), nullptr,
                               nullptr, Q_lb, Q_ub, S, L, E, 3 * E, st));
@@ -1045,8 +1057,10 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     }
     // res1 = cur + affine(ctx, Wo)
     g_tag = "affine_gemm";
-    LAUNCH(launch_affine_lambda(lw.wo, w.tm_ok ? &w.tm_CTX : nullptr, CTX, w.crX, R1, w.crX, X, w.crX,
-                                (long long)S * L, D, st));
+    const bool res0 = l == 0 && onehot;  // the Λ0 residual is a +1 scatter instead of a read
+    LAUNCH(launch_affine_lambda(lw.wo, w.tm_ok ? &w.tm_CTX : nullptr, CTX, w.crX, R1, w.crX, res0 ? nullptr : X,
+                                res0 ? 0 : w.crX, (long long)S * L, D, st));
+    if (res0) LAUNCH(launch_add_onehot(R1, w.pos_all.as<int>(), w.slot_map.as<int>(), S, L, E, w.W, D, w.col0, st));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(CTX_lb, CTX_ub, lw.wo.w64.as<double>(), lw.wo.b64.as<double>(), X_lb, X_ub,
                               R1_lb, R1_ub, S, L, E, E, st));

@@ -108,6 +108,13 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
 int launch_init_input(float* lam, long long cr, double* lb, double* ub, const double* x,
                       const int* positions, const int* slot_map, int S, int L, int E, int W,
                       cudaStream_t st, int D = 0, int col0 = 0);
+// First layer from the one-hot Λ0 analytically: Q/K/V Λ = W scattered into the perturbed rows
+// (exact, no GEMM), and the Λ0 residual of the first attention block as a +1 scatter.
+// launch_init_input with lam == nullptr binds lb/ub only.
+int launch_onehot_affine(float* lam, long long cr, const float* w, const int* positions, const int* slot_map, int S,
+                         int L, int E, int O, int W, int D, int col0, cudaStream_t st);
+int launch_add_onehot(float* lam, const int* positions, const int* slot_map, int S, int L, int E, int W, int D,
+                      int col0, cudaStream_t st);
 // MeanPool (graph.cpp:628-634) -> pooled f64 planes [S, E, D] (+ lb/ub [S, E]).
 int launch_meanpool(const float* lam, long long cr, const double* lb, const double* ub,
                     double* pooled_c, double* pooled_r, double* plb, double* pub, int S, int L,

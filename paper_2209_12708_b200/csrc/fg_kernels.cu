@@ -1443,6 +1443,12 @@ __global__ void init_input_kernel(float* lam, long long cr, double* lb, double* 
   int tok = (int)((row / E) % L);
   int s = (int)(row / ((long long)L * E));
   int src = slot_map ? slot_map[s] : s;
+  if (lane == 0) {
+    long long xi = ((long long)src * L + tok) * E + e;
+    lb[row] = x[xi];
+    ub[row] = x[xi];
+  }
+  if (!lam) return;  // bias-only binding (the first layer consumes Λ0 analytically)
   float* c = lam + row * D;
   float* r = c + cr;
   int hot = -1;
@@ -1455,11 +1461,56 @@ __global__ void init_input_kernel(float* lam, long long cr, double* lb, double* 
     *reinterpret_cast<float4*>(c + d) = make_float4(v[0], v[1], v[2], v[3]);
     *reinterpret_cast<float4*>(r + d) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  if (lane == 0) {
-    long long xi = ((long long)src * L + tok) * E + e;
-    lb[row] = x[xi];
-    ub[row] = x[xi];
+}
+
+// First-layer Q/K/V Λ without a GEMM.  Λ0 is one-hot (centre plane 1 at column w*E + e of the
+// perturbed token pos[w], radius 0), so propagate_affine's Λ output is W itself scattered:
+//   out_c[s, t, o, d] = W[e][o] if t == pos[w] and d == w*E + e (global column), else 0;
+//   out_r = |W| . 0 = 0.
+// Exact (no TF32 splitting of a product with 1).  Row (s, t, o) per warp, float4 stores.
+__global__ void onehot_affine_kernel(float* lam, long long cr, const float* __restrict__ w, const int* positions,
+                                     const int* slot_map, int S, int L, int E, int O, int W, int D, int col0) {
+  long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+  int lane = threadIdx.x & (kWarp - 1);
+  long long nrows = (long long)S * L * O;
+  if (row >= nrows) return;
+  const int o = (int)(row % O);
+  const int tok = (int)((row / O) % L);
+  const int s = (int)(row / ((long long)L * O));
+  const int src = slot_map ? slot_map[s] : s;
+  int word = -1;
+  for (int q = 0; q < W; ++q)
+    if (positions[src * W + q] == tok) word = q;
+  float* c = lam + row * D;
+  float* r = c + cr;
+  for (int d = lane * 4; d < D; d += 4 * kWarp) {
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (word >= 0) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int e = col0 + d + t - word * E;  // embedding index of this (global) column
+        if (e >= 0 && e < E) v[t] = w[(long long)e * O + o];
+      }
+    }
+    *reinterpret_cast<float4*>(c + d) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(r + d) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+}
+
+// Residual add of Λ0 (propagate_add(x, .), relax.cpp:656-674) without reading it: +1 on the
+// centre plane at (s, pos[w], e, column w*E + e).
+__global__ void add_onehot_kernel(float* lam, const int* positions, const int* slot_map, int S, int L, int E, int W,
+                                  int D, int col0) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)S * W * E) return;
+  const int e = (int)(t % E);
+  const int q = (int)((t / E) % W);
+  const int s = (int)(t / ((long long)W * E));
+  const int src = slot_map ? slot_map[s] : s;
+  const int col = q * E + e - col0;
+  if (col < 0 || col >= D) return;
+  const int tok = positions[src * W + q];
+  lam[(((long long)s * L + tok) * E + e) * D + col] += 1.0f;
 }
 
 __global__ void meanpool_kernel(const float* lam, long long cr, const double* lb, const double* ub,
@@ -1922,6 +1973,21 @@ int launch_init_input(float* lam, long long cr, double* lb, double* ub, const do
   if (D <= 0) D = W * E;
   init_input_kernel<<<blocks_for(nrows, 8), 256, 0, st>>>(lam, cr, lb, ub, x, positions, slot_map, S,
                                                           L, E, W, D, col0);
+  return 1;
+}
+
+int launch_onehot_affine(float* lam, long long cr, const float* w, const int* positions, const int* slot_map, int S,
+                         int L, int E, int O, int W, int D, int col0, cudaStream_t st) {
+  const long long nrows = (long long)S * L * O;
+  onehot_affine_kernel<<<blocks_for(nrows, 8), 256, 0, st>>>(lam, cr, w, positions, slot_map, S, L, E, O, W, D,
+                                                             col0);
+  return 1;
+}
+
+int launch_add_onehot(float* lam, const int* positions, const int* slot_map, int S, int L, int E, int W, int D,
+                      int col0, cudaStream_t st) {
+  const long long n = (long long)S * W * E;
+  add_onehot_kernel<<<blocks_for(n, 256), 256, 0, st>>>(lam, positions, slot_map, S, L, E, W, D, col0);
   return 1;
 }
 
