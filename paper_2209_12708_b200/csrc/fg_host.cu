@@ -928,9 +928,15 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
     LAUNCH(launch_affine_bias(X_lb, X_ub, lw.qkv.w64.as<double>(), lw.qkv.b64.as<double>(), nullptr,
                               nullptr, Q_lb, Q_ub, S, L, E, 3 * E, st));
     g_tag = "concretize";
-    if (fg_status s = concretize_site(m, QKV, w.crQKV, Q_lb, Q_ub, (long long)L * 3 * E, nQKV, D, norm, eps,
-                                      Q_lo, Q_hi))
+    // first layer under the one-hot binding: Q/K/V Λ rows are zero outside the perturbed tokens
+    const bool sparse0 = l == 0 && onehot && !sharded;
+    if (sparse0) {
+      LAUNCH(launch_concretize_tokens(QKV, w.crQKV, Q_lb, Q_ub, (long long)L * 3 * E, nQKV, D, norm, eps, Q_lo, Q_hi,
+                                      w.pos_all.as<int>(), w.slot_map.as<int>(), w.W, 3 * E, st));
+    } else if (fg_status s = concretize_site(m, QKV, w.crQKV, Q_lb, Q_ub, (long long)L * 3 * E, nQKV, D, norm,
+                                             eps, Q_lo, Q_hi)) {
       return s;
+    }
     if (dump) {
       for (int t = 0; t < 3; ++t)
         if (fg_status s = dump->copy(base + (size_t)t * L * E, Q_lo, Q_hi, 0, 3 * E, E, (size_t)t * E, L)) return s;
@@ -961,6 +967,16 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
       gx.ldn_out = D;
       gx.n_split = L; gx.split_stride = w.crSC;
       gx.alpha = (float)scale;
+      if (l == 0 && onehot) {
+        // Q/K Λ rows vanish off the perturbed tokens: scores Λ[i, j] != 0 only for i or j
+        // perturbed -> zero the scores, x-side terms for perturbed queries i, y-side terms for
+        // perturbed keys j (gathered batch coordinate)
+        CK(cudaMemsetAsync(SC, 0, sizeof(float) * 2 * w.crSC, st));
+        gx.nb[2] = w.W;
+        gx.gather = w.pos_all.as<int>();
+        gx.gather_slot = w.slot_map.as<int>();
+        gx.gather_ld = w.W;
+      }
       LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_x[0].bytes, w.tm_sim_x[1].bytes, gx, w.bn_simx, st,
                              w.dots2_ok ? w.tm2_sim_x[0].bytes : nullptr, w.dots2_ok ? w.tm2_sim_x[1].bytes : nullptr));
       // y-side: scores[s,h,i,j,:] += sum_k lx[i,k] K_p[j, E + h*hd + k]   (per plane p)
@@ -978,6 +994,12 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
       gy.out_c[3] = w.crSC; gy.ldn_out = (long long)L * D;
       gy.alpha = (float)scale;
       gy.accumulate = 1;
+      if (l == 0 && onehot) {
+        gy.nb[2] = w.W;
+        gy.gather = w.pos_all.as<int>();
+        gy.gather_slot = w.slot_map.as<int>();
+        gy.gather_ld = w.W;
+      }
       LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_y[0].bytes, w.tm_sim_y[1].bytes, gy, w.bn_sim, st,
                              w.dots2_ok ? w.tm2_sim_y[0].bytes : nullptr, w.dots2_ok ? w.tm2_sim_y[1].bytes : nullptr));
     } else {

@@ -68,6 +68,12 @@ int launch_concretize(const float* lam, long long cr, const double* lb, const do
                       long long rows_per_s, long long nrows, int D, int norm, const double* eps,
                       double* lo, double* hi, cudaStream_t st);
 
+// concretize of token rows whose Λ is zero outside the perturbed tokens (first-layer Q/K/V)
+int launch_concretize_tokens(const float* lam, long long cr, const double* lb, const double* ub,
+                             long long rows_per_s, long long nrows, int D, int norm, const double* eps,
+                             double* lo, double* hi, const int* positions, const int* slot_map, int W, int width,
+                             cudaStream_t st);
+
 int launch_elementwise_verify(int kind, float* lam, long long cr, double* lb, double* ub,
                               long long rows_per_s, long long nrows, int D, int norm,
                               const double* eps, int* status, int site, double* lo_out,
@@ -167,6 +173,11 @@ struct LamGemm {
   int accumulate;
   int tiles_m, tiles_n, num_tiles;  // set by launch_lam_gemm
   int epi_groups;                   // epilogue warp groups draining tiles (1 or 2; launch_lam_gemm)
+  // optional gather of batch coordinate b2 (sparse first-layer McCormick terms): when set,
+  // b2 <- gather[slot_map[b0] * gather_ld + b2] (the perturbed token of word b2 of sentence b0)
+  const int* gather;
+  const int* gather_slot;
+  int gather_ld;
 };
 bool umma_available();
 int umma_pick_bn(int N);  // 256 / 128 / 64, or 0 when N is not a multiple of 64

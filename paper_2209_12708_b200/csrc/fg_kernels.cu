@@ -295,6 +295,42 @@ __global__ void __launch_bounds__(256) concretize_kernel(const float* __restrict
   }
 }
 
+// concretize of a token-row tensor whose Λ rows are zero outside the perturbed tokens (the
+// first layer's Q/K/V under the one-hot binding): unperturbed rows get lo = lb, hi = ub
+// (eps * ||0|| = 0 exactly) without reading Λ.  row = (s, token, f), f < width.
+template <int Q>
+__global__ void __launch_bounds__(256) concretize_tokens_kernel(
+    const float* __restrict__ lam, long long cr, const double* __restrict__ lb, const double* __restrict__ ub,
+    long long rows_per_s, long long nrows, int D, const double* __restrict__ eps, double* __restrict__ lo,
+    double* __restrict__ hi, const int* __restrict__ positions, const int* __restrict__ slot_map, int W, int width) {
+  long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
+  int lane = threadIdx.x & (kWarp - 1);
+  if (row >= nrows) return;
+  const long long s = row / rows_per_s;
+  const int tok = (int)((row % rows_per_s) / width);
+  const int src = slot_map[s];
+  bool hot = false;
+  for (int q = 0; q < W; ++q) hot |= positions[src * W + q] == tok;
+  if (!hot) {
+    if (lane == 0) {
+      lo[row] = lb[row];
+      hi[row] = ub[row];
+    }
+    return;
+  }
+  const float* c = lam + row * D;
+  const float* r = c + cr;
+  NormAcc<Q> acc;
+  for (int d = lane * 4; d < D; d += 4 * kWarp)
+    acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
+  acc.warp_reduce();
+  if (lane == 0) {
+    double e = eps[s];
+    lo[row] = lb[row] - e * acc.fin(acc.l);
+    hi[row] = ub[row] + e * acc.fin(acc.u);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // elementwise_verify (graph.cpp:484-501) fused: concretize -> envelope -> compose,
 // in place, one warp per neuron row.  Λ is read from HBM once (the second sweep
@@ -1758,6 +1794,17 @@ int launch_concretize(const float* lam, long long cr, const double* lb, const do
   dim3 grid(blocks_for(nrows, 8)), block(256);
   DISPATCH_Q(dual_norm(norm), concretize_kernel,
              <<<grid, block, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi));
+  return 1;
+}
+
+int launch_concretize_tokens(const float* lam, long long cr, const double* lb, const double* ub,
+                             long long rows_per_s, long long nrows, int D, int norm, const double* eps,
+                             double* lo, double* hi, const int* positions, const int* slot_map, int W, int width,
+                             cudaStream_t st) {
+  if (nrows <= 0) return 0;
+  DISPATCH_Q(dual_norm(norm), concretize_tokens_kernel,
+             <<<blocks_for(nrows, 8), 256, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi, positions,
+                                                     slot_map, W, width));
   return 1;
 }
 

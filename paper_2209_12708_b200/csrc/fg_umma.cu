@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     batch /= p.nb[2];
     b[1] = batch % p.nb[1];
     b[0] = batch / p.nb[1];
+    if (p.gather) b[2] = p.gather[p.gather_slot[b[0]] * p.gather_ld + b[2]];
     m0 = mt * (PAIR ? 2 : 1) * kBM + (int)rank * kBM;  // this CTA's first d-row
     n0 = nt * BN;
   };
