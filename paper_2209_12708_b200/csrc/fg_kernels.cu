@@ -443,7 +443,9 @@ __global__ void __launch_bounds__(kBiasCols) affine_bias_kernel(
     }
     __syncthreads();
     if (j < O) {
-      // i ascending per (row, j): the reference's accumulation order (relax.cpp:280-287)
+      // i ascending per (row, j): the reference's accumulation order (relax.cpp:280-287);
+      // unrolled so several weight loads are in flight per thread
+#pragma unroll 8
       for (int i = 0; i < n; ++i) {
         const double wv = w[(long long)(i0 + i) * O + j];
         const double wp = (wv < 0.0) ? 0.0 : wv;
