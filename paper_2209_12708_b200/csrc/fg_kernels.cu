@@ -548,43 +548,113 @@ __device__ __forceinline__ void term_bias(double lx, double ly, double uy, doubl
   }
 }
 
-// scores bias for (s,h,i,j), then the Scale node (propagate_scale, relax.cpp:683-687).
-__global__ void sim_bias_kernel(NView q, NView k, NView out, int S, int H, int L, int hd,
-                                double scale) {
-  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long total = (long long)S * H * L * L;
-  if (t >= total) return;
-  int j = (int)(t % L);
-  int i = (int)((t / L) % L);
-  int h = (int)((t / ((long long)L * L)) % H);
-  long long s = t / ((long long)H * L * L);
-  double olb = 0.0, oub = 0.0;
-  for (int kk = 0; kk < hd; ++kk) {
-    long long xi = nidx(q, s, i, h * hd + kk), yi = nidx(k, s, j, h * hd + kk);
-    term_bias(q.lo[xi], k.lo[yi], k.hi[yi], q.lb[xi], q.ub[xi], k.lb[yi], k.ub[yi], olb, oub);
+// McCormick product biases as a tiled f64 kernel (relax.cpp:546-547, 560-561, 635-651):
+//   out[a, b] = scale * sum_c term(X[a, c], Y[b, c])     c ascending (the reference order)
+// similarity: a = query row i, b = key row j, c = head feature kk   (X = Q, Y = K)
+// weighted:   a = query row i, b = head feature kk, c = key row j   (X = P, Y = V)
+// One CTA per (sentence, head, 32 a x 64 b tile); c is staged through shared memory in chunks
+// of 16, so every Y element is read from HBM/L2 once per tile and reused by 32 outputs.
+struct McBias {
+  const double *xlo, *xlb, *xub, *ylo, *yhi, *ylb, *yub;
+  double *olb, *oub;
+  long long xs, ys, os;  // per-sentence strides
+  long long xh, yh, oh;  // per-head offsets
+  long long xa, xc, yb, yc, oa, ob;
+  int H, A, B, C;
+  double scale;
+};
+
+constexpr int kMbA = 32, kMbB = 64, kMbC = 16, kMbThreads = 256, kMbR = kMbA / (kMbThreads / kMbB);
+
+__global__ void __launch_bounds__(kMbThreads) mc_bias_kernel(McBias p) {
+  __shared__ double ys[4][kMbC][kMbB];
+  __shared__ double xs[3][kMbC][kMbA];
+  const int ta = (p.A + kMbA - 1) / kMbA, tb = (p.B + kMbB - 1) / kMbB;
+  long long blk = blockIdx.x;
+  const int bt = (int)(blk % tb);
+  blk /= tb;
+  const int at = (int)(blk % ta);
+  blk /= ta;
+  const int h = (int)(blk % p.H);
+  const long long s = blk / p.H;
+  const int a0 = at * kMbA, b0 = bt * kMbB;
+  const long long xbase = s * p.xs + h * p.xh, ybase = s * p.ys + h * p.yh;
+  const int tid = threadIdx.x, bl = tid % kMbB, ag = tid / kMbB;
+  double olb[kMbR], oub[kMbR];
+#pragma unroll
+  for (int r = 0; r < kMbR; ++r) olb[r] = oub[r] = 0.0;
+  for (int c0 = 0; c0 < p.C; c0 += kMbC) {
+    const int nc = min(kMbC, p.C - c0);
+    __syncthreads();
+    for (int idx = tid; idx < kMbC * kMbB; idx += kMbThreads) {
+      int b, c;
+      if (p.yc == 1) c = idx % kMbC, b = idx / kMbC;
+      else b = idx % kMbB, c = idx / kMbB;
+      if (c < nc && b0 + b < p.B) {
+        const long long g = ybase + (long long)(b0 + b) * p.yb + (long long)(c0 + c) * p.yc;
+        ys[0][c][b] = p.ylo[g];
+        ys[1][c][b] = p.yhi[g];
+        ys[2][c][b] = p.ylb[g];
+        ys[3][c][b] = p.yub[g];
+      }
+    }
+    for (int idx = tid; idx < kMbC * kMbA; idx += kMbThreads) {
+      const int c = idx % kMbC, a = idx / kMbC;
+      if (c < nc && a0 + a < p.A) {
+        const long long g = xbase + (long long)(a0 + a) * p.xa + (long long)(c0 + c) * p.xc;
+        xs[0][c][a] = p.xlo[g];
+        xs[1][c][a] = p.xlb[g];
+        xs[2][c][a] = p.xub[g];
+      }
+    }
+    __syncthreads();
+    for (int c = 0; c < nc; ++c) {
+      const double ly = ys[0][c][bl], uy = ys[1][c][bl], ylb = ys[2][c][bl], yub = ys[3][c][bl];
+#pragma unroll
+      for (int r = 0; r < kMbR; ++r) {
+        const int a = ag * kMbR + r;
+        term_bias(xs[0][c][a], ly, uy, xs[1][c][a], xs[2][c][a], ylb, yub, olb[r], oub[r]);
+      }
+    }
   }
-  long long o = nidx(out, s, (long long)h * L + i, j);
-  out.lb[o] = scale * olb;
-  out.ub[o] = scale * oub;
+  if (b0 + bl >= p.B) return;
+#pragma unroll
+  for (int r = 0; r < kMbR; ++r) {
+    const int a = a0 + ag * kMbR + r;
+    if (a >= p.A) break;
+    const long long o = s * p.os + h * p.oh + (long long)a * p.oa + (long long)(b0 + bl) * p.ob;
+    p.olb[o] = p.scale * olb[r];
+    p.oub[o] = p.scale * oub[r];
+  }
 }
 
-// context bias for (s,i,h,k): sum over key rows j (relax.cpp:635-651).
-__global__ void wv_bias_kernel(NView p, NView v, NView out, int S, int H, int L, int hd) {
-  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long total = (long long)S * L * H * hd;
-  if (t >= total) return;
-  int kk = (int)(t % hd);
-  int h = (int)((t / hd) % H);
-  int i = (int)((t / ((long long)hd * H)) % L);
-  long long s = t / ((long long)hd * H * L);
-  double olb = 0.0, oub = 0.0;
-  for (int j = 0; j < L; ++j) {
-    long long xi = nidx(p, s, (long long)h * L + i, j), yi = nidx(v, s, j, h * hd + kk);
-    term_bias(p.lo[xi], v.lo[yi], v.hi[yi], p.lb[xi], p.ub[xi], v.lb[yi], v.ub[yi], olb, oub);
-  }
-  long long o = nidx(out, s, i, h * hd + kk);
-  out.lb[o] = olb;
-  out.ub[o] = oub;
+// scores bias for (s,h,i,j), then the Scale node (propagate_scale, relax.cpp:683-687)
+void sim_bias(const NView& q, const NView& k, const NView& out, int S, int H, int L, int hd, double scale,
+              cudaStream_t st) {
+  McBias p{q.lo, q.lb, q.ub, k.lo, k.hi, k.lb, k.ub, out.lb, out.ub};
+  p.xs = q.s_stride; p.ys = k.s_stride; p.os = out.s_stride;
+  p.xh = hd; p.yh = hd; p.oh = (long long)L * out.row_stride;
+  p.xlo += q.col0; p.xlb += q.col0; p.xub += q.col0;
+  p.ylo += k.col0; p.yhi += k.col0; p.ylb += k.col0; p.yub += k.col0;
+  p.olb += out.col0; p.oub += out.col0;
+  p.xa = q.row_stride; p.xc = 1; p.yb = k.row_stride; p.yc = 1; p.oa = out.row_stride; p.ob = 1;
+  p.H = H; p.A = L; p.B = L; p.C = hd; p.scale = scale;
+  const long long blocks = (long long)S * H * ((L + kMbA - 1) / kMbA) * ((L + kMbB - 1) / kMbB);
+  mc_bias_kernel<<<(unsigned)blocks, kMbThreads, 0, st>>>(p);
+}
+
+// context bias for (s,i,h,k): sum over key rows j (relax.cpp:635-651)
+void wv_bias(const NView& pv, const NView& v, const NView& out, int S, int H, int L, int hd, cudaStream_t st) {
+  McBias p{pv.lo, pv.lb, pv.ub, v.lo, v.hi, v.lb, v.ub, out.lb, out.ub};
+  p.xs = pv.s_stride; p.ys = v.s_stride; p.os = out.s_stride;
+  p.xh = (long long)L * pv.row_stride; p.yh = hd; p.oh = hd;
+  p.xlo += pv.col0; p.xlb += pv.col0; p.xub += pv.col0;
+  p.ylo += v.col0; p.yhi += v.col0; p.ylb += v.col0; p.yub += v.col0;
+  p.olb += out.col0; p.oub += out.col0;
+  p.xa = pv.row_stride; p.xc = 1; p.yb = 1; p.yc = v.row_stride; p.oa = out.row_stride; p.ob = 1;
+  p.H = H; p.A = L; p.B = hd; p.C = L; p.scale = 1.0;
+  const long long blocks = (long long)S * H * ((L + kMbA - 1) / kMbA) * ((hd + kMbB - 1) / kMbB);
+  mc_bias_kernel<<<(unsigned)blocks, kMbThreads, 0, st>>>(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -1858,8 +1928,7 @@ int launch_dot_similarity(const NView& q, const NView& k, const NView& out, int 
   int n = 0;
   sim_coef_kernel<<<S * H, 256, 0, st>>>(q, k, H, L, hd, ws);
   ++n;
-  long long total = (long long)S * H * L * L;
-  sim_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(q, k, out, S, H, L, hd, (double)scale);
+  sim_bias(q, k, out, S, H, L, hd, (double)scale, st);
   ++n;
   const long long per = 6LL * hd * L;
   // x-side (Q rows scaled by K-derived coefficients): batch (s, h, i, out plane)
@@ -1894,8 +1963,7 @@ int launch_dot_weighted(const NView& p, const NView& v, const NView& out, int S,
   int n = 0;
   wv_coef_kernel<<<S * H, 256, 0, st>>>(p, v, H, L, hd, ws);
   ++n;
-  long long total = (long long)S * L * H * hd;
-  wv_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(p, v, out, S, H, L, hd);
+  wv_bias(p, v, out, S, H, L, hd, st);
   ++n;
   const long long per = 4LL * L * hd + 2LL * L * L;
   // x-side (P rows scaled by V-derived coefficients): batch (s, h, i, out plane)
@@ -2114,15 +2182,13 @@ int launch_wv_coef_split(const NView& p, const NView& v, int S, int H, int L, in
 
 int launch_sim_bias(const NView& q, const NView& k, const NView& out, int S, int H, int L, int hd,
                     double scale, cudaStream_t st) {
-  long long total = (long long)S * H * L * L;
-  sim_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(q, k, out, S, H, L, hd, scale);
+  sim_bias(q, k, out, S, H, L, hd, scale, st);
   return 1;
 }
 
 int launch_wv_bias(const NView& p, const NView& v, const NView& out, int S, int H, int L, int hd,
                    cudaStream_t st) {
-  long long total = (long long)S * L * H * hd;
-  wv_bias_kernel<<<blocks_for(total, 128), 128, 0, st>>>(p, v, out, S, H, L, hd);
+  wv_bias(p, v, out, S, H, L, hd, st);
   return 1;
 }
 

@@ -504,6 +504,13 @@ class Model:
                    "fg_model_create")
         self.handle = h
 
+    @classmethod
+    def from_file(cls, ctx: Context, manifest: str, strict: bool = True) -> "Model":
+        """A faith-model/v1 manifest (model::load_model, model.cpp:287-335) straight to the device."""
+        from .formats import load_model
+        cfg, params = load_model(manifest, strict=strict)
+        return cls(ctx, cfg, params)
+
     def close(self):
         if getattr(self, "handle", None):
             self.lib.fg_model_destroy(self.handle)

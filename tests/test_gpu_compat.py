@@ -113,3 +113,20 @@ def test_fused_pass_on_reference_models(tmp_path, case):
     ea = float(re.search(r"= ([0-9.e+-]+)", a.stdout).group(1))
     eb = float(re.search(r"= ([0-9.e+-]+)", b.stdout).group(1))
     assert abs(ea - eb) <= 1e-3 * ea + 1e-5, (a.stdout, b.stdout)
+
+
+def test_reference_model_file_to_device_verdict():
+    """A faith-model/v1 file written by the reference (tests/golden/formats) loaded by
+    Model.from_file: the whole-embedding certify (all L tokens perturbed, D = L*E, the reference's
+    input_bounds mode) gives the reference cmd_verify verdict recorded next to it."""
+    import numpy as np
+    from paper_2209_12708_b200 import faith_gpu as F
+    from paper_2209_12708_b200 import formats as FM
+    gold = os.path.join(ROOT, "tests", "golden", "formats")
+    m = F.Model.from_file(F.Context(0), os.path.join(gold, "m1.json"))
+    x = FM.load_embedding(os.path.join(gold, "x1.json"), m.cfg)
+    r = m.certify(x, np.arange(m.cfg.length), "l2", 0.01)
+    with open(os.path.join(gold, "m1_verify.txt")) as f:
+        want = f.read().split()
+    assert want[0] == "verified" and bool(r["verified"][0])
+    assert want[-1] == f"class={int(r['predicted'][0])}"
