@@ -297,6 +297,68 @@ typedef struct {
 } fg_run_stats;
 fg_status fg_last_run_stats(const fg_model* model, fg_run_stats* out);
 
+/* ---- verification-graph executor (faith-graph/v1) ------------------------
+ * graph::evaluate (proj/src/graph.cpp:505-673) over an arbitrary verification graph:
+ * every node -- the split (SplitSigns / MatmulPair / CombineHalves), per-side (AffineBound /
+ * MergeSides) and fused (AffineVerify) affine forms, dot products, scales, adds, mean-pool,
+ * the activation / exp / recip envelopes, Softmax, SumReduce and MulBroadcast -- runs on the
+ * device in the exact f64 arithmetic of FG_PRECISION_F64 (reference operation order), with
+ * every intermediate value resident in HBM and released after its last consumer, as the
+ * reference does (graph.cpp:655-660).  The JSON schema (graph.cpp:781-850) is parsed on the
+ * host (paper_2209_12708_b200/graph.py); this level takes the decoded node table. */
+#define FG_NODE_INPUT 0
+#define FG_NODE_WEIGHT 1
+#define FG_NODE_SPLIT_SIGNS 2
+#define FG_NODE_MATMUL_PAIR 3
+#define FG_NODE_COMBINE_HALVES 4
+#define FG_NODE_AFFINE_BOUND 5
+#define FG_NODE_MERGE_SIDES 6
+#define FG_NODE_AFFINE_VERIFY 7
+#define FG_NODE_DOT_PRODUCT 8
+#define FG_NODE_SCALE 9
+#define FG_NODE_ADD 10
+#define FG_NODE_MEAN_POOL 11
+#define FG_NODE_RELU_VERIFY 12
+#define FG_NODE_TANH_VERIFY 13
+#define FG_NODE_SILU_VERIFY 14
+#define FG_NODE_SOFTMAX 15
+#define FG_NODE_EXP_VERIFY 16
+#define FG_NODE_SUM_REDUCE 17
+#define FG_NODE_RECIP_VERIFY 18
+#define FG_NODE_MUL_BROADCAST 19
+#define FG_GRAPH_MAX_RANK 8
+
+typedef struct fg_graph fg_graph;
+/* One node of graph::VerGraph (graph.hpp:59-75).  inputs[] in the reference's edge-role order
+ * (graph.cpp:684-706): MatmulPair {x, halves}; CombineHalves {pos, neg[, bias]}; affine
+ * {x, w[, bias]}; MergeSides / DotProduct / Add {a, b}; MulBroadcast {x, r}; others {x}. */
+typedef struct {
+  int kind;       /* FG_NODE_* */
+  int n_inputs;   /* 0..3 */
+  int inputs[3];  /* producer node ids, each < this node's index */
+  int sign;       /* MatmulPair: 0 positive half, 1 negative half */
+  int side;       /* AffineBound: 0 lower, 1 upper */
+  int layout;     /* DotProduct: FG_DOT_* */
+  int heads;      /* DotProduct */
+  int axis;       /* Softmax / SumReduce / MulBroadcast / MeanPool */
+  double scale;   /* Scale */
+  int constant;   /* Weight: index into the constant table */
+  int input;      /* Input: binding slot of fg_graph_evaluate */
+} fg_node;
+/* Constants (the Weight table) are uploaded once.  const_shape is [n_constants][FG_GRAPH_MAX_RANK].
+ * Structural errors of VerGraph::validate (graph.cpp:133-160) -> FG_EINVAL. */
+fg_status fg_graph_create(fg_ctx* ctx, size_t n_nodes, const fg_node* nodes, size_t n_constants,
+                          const size_t* const_rank, const size_t* const_shape, const double* const* const_data,
+                          fg_graph** out);
+void fg_graph_destroy(fg_graph* graph);
+/* Binds input slot i to the tensor (in_rank[i], in_shape[i][..], in_data[i]) -- input_bounds
+ * (bounds.cpp:101-120): numel must equal dim -- and evaluates to the unique operator sink.
+ * The result stays on the device until the next evaluate or destroy. */
+fg_status fg_graph_evaluate(fg_graph* graph, size_t n_inputs, const size_t* in_rank, const size_t* in_shape,
+                            const double* const* in_data, int norm, double eps, size_t dim);
+fg_status fg_graph_result_shape(const fg_graph* graph, size_t* rank, size_t* shape, size_t* d);
+fg_status fg_graph_result(fg_graph* graph, double* lw, double* lb, double* uw, double* ub);
+
 #ifdef __cplusplus
 }
 #endif

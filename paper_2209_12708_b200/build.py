@@ -26,6 +26,7 @@ SOURCES = {
     "fg_ops64.cu": [],
     "fg_shard.cu": [],
     "fg_forward.cu": [],
+    "fg_graph.cu": ["-fmad=false"],
 }
 
 
