@@ -1289,6 +1289,350 @@ __global__ void __launch_bounds__(kSm3Threads) softmax3_kernel(NView sc, int row
   cluster_wait();
 }
 
+// ---------------------------------------------------------------------------
+// Softmax chain, streaming version (D <= 512, D % 128 == 0; the pass uses it when it applies).
+//
+// Persistent CTAs, one score row (s, h, i) at a time with the FULL perturbation width, so no
+// norm ever crosses a CTA: one producer warp streams key rows (c and r planes, 8·D bytes)
+// through an NS-stage shared-memory ring with cp.async.bulk + mbarriers, and NC consumer warps
+// take one key row each:
+//   pass 1  per key: q-norms of the exp input (warp reduction) -> ExpVerify envelope
+//           (relax.cpp:363-394) -> Σ_j e_j accumulated in the warp's registers;
+//   then    Σ rows combined over the warps in a fixed order -> RecipVerify (relax.cpp:396-424)
+//           -> r rows and their norms (block reduction among the consumers);
+//   pass 2  per key: McCormick e_j * r (relax.cpp:744-775) written to HBM, probs lb/ub/lo/hi.
+// Every row is streamed twice (the second read is an L2 hit for the row the CTA just read) and
+// written once.  The producer never waits on the consumers' reductions: it prefetches pass 2
+// of the row and pass 1 of the next row while Σ / recip / r are being formed, so HBM traffic
+// stays in flight through the serial part of the chain.  Element math f32, norms and O(N)
+// state f64, as softmax3_kernel.
+constexpr int kSm4Consumers = 8;
+// A multiple of the consumer count: the items of one stage are then always taken by the same
+// warp, so a warp never waits on a stage whose previous fill (issued earlier, but possibly
+// completing later -- bulk copies complete out of order) is still pending, which would let the
+// parity wait succeed one phase early.
+constexpr int kSm4Stages = 16;
+static_assert(kSm4Stages % kSm4Consumers == 0, "stage ownership must be per warp");
+constexpr int kSm4Threads = (kSm4Consumers + 1) * 32;
+
+__device__ __forceinline__ void sm4_sync() {  // consumer warps only
+  asm volatile("bar.sync 1, %0;" ::"r"(kSm4Consumers * 32) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
+               : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void sm4_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ double sm4_reduce(double v, double* red) {  // consumer-block q-combine
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = (Q == NORM_LINF) ? warp_max(v) : warp_sum(v);
+  sm4_sync();
+  if (lane == 0) red[w] = v;
+  sm4_sync();
+  double r = red[0];
+  for (int i = 1; i < kSm4Consumers; ++i) r = qcombine<Q>(r, red[i]);
+  return r;
+}
+
+size_t softmax4_smem(int n, int D) {
+  return (size_t)kSm4Stages * 8 * D              // ring
+         + (size_t)kSm4Consumers * 2 * D * 4     // Σ partials per warp
+         + (size_t)2 * D * 4                     // r rows (f32)
+         + (size_t)(n + 1) * (2 * 4 + 3 * 8)     // a_lo_f, a_up_f, e_lb, e_ub, e_lo
+         + 64 * 8                                // red + scal
+         + 2 * kSm4Stages * 8 + 64;              // barriers + alignment
+}
+
+template <int Q, int KG>  // KG = D / 128 float4 groups per lane per plane
+__global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int rows_per_s, int nrows, int n,
+                                                                  const double* __restrict__ eps,
+                                                                  int* __restrict__ status, int site_exp,
+                                                                  int site_recip) {
+  constexpr int D = KG * 128;
+  extern __shared__ __align__(16) unsigned char sm4[];
+  float* ring = reinterpret_cast<float*>(sm4);                          // [NS][c|r][D]
+  float* part = ring + (size_t)kSm4Stages * 2 * D;                      // [NC][u|l][D]
+  float* ru_f = part + (size_t)kSm4Consumers * 2 * D;                   // [D]
+  float* rl_f = ru_f + D;                                               // [D]
+  const int n2 = (n + 1) & ~1;                                          // keeps the f64 arrays aligned
+  float* a_lo_f = rl_f + D;                                             // [n]
+  float* a_up_f = a_lo_f + n2;                                          // [n]
+  double* e_lb = reinterpret_cast<double*>(a_up_f + n2);                // [n]
+  double* e_ub = e_lb + n;
+  double* e_lo = e_ub + n;
+  double* red = e_lo + n;    // [32]
+  double* scal = red + 32;   // [32]
+  uint64_t* full = reinterpret_cast<uint64_t*>(scal + 32);
+  uint64_t* empty = full + kSm4Stages;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int b = 0; b < kSm4Stages; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(full + b)) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(empty + b)) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kSm4Consumers) {  // ---- producer
+    if (lane == 0) {
+      long long t = 0;
+      for (int rid = blockIdx.x; rid < nrows; rid += gridDim.x) {
+        const int s = rid / rows_per_s, row = rid % rows_per_s;
+        const long long nb = (long long)s * sc.s_stride + (long long)row * n;
+        const float* cb = sc.lam + nb * D;
+        const float* rb = cb + sc.cr;
+        for (int p = 0; p < 2; ++p)
+          for (int j = 0; j < n; ++j, ++t) {
+            const int st = (int)(t % kSm4Stages);
+            const uint32_t ph = (uint32_t)((t / kSm4Stages) & 1);
+            if (t >= kSm4Stages) sm4_wait(empty + st, ph ^ 1u);
+            float* dst = ring + (size_t)st * 2 * D;
+            mbar_expect(full + st, 8u * D);
+            asm volatile(
+                "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(dst)),
+                "l"(cb + (long long)j * D), "r"(4u * D), "r"(smem_addr(full + st))
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(dst + D)),
+                "l"(rb + (long long)j * D), "r"(4u * D), "r"(smem_addr(full + st))
+                : "memory");
+          }
+      }
+    }
+    __syncwarp();
+  } else {  // ---- consumers
+  NormAcc<Q> fin;
+  long long t0 = 0;
+  for (int rid = blockIdx.x; rid < nrows; rid += gridDim.x, t0 += 2LL * n) {
+    const int s = rid / rows_per_s, row = rid % rows_per_s;
+    const long long nb = (long long)s * sc.s_stride + (long long)row * n;
+    float* cbw = sc.lam + nb * D;
+    float* rbw = cbw + sc.cr;
+    const double e = eps[s];
+
+    // pass 1: exp envelopes per key, Σ_j e_j in registers
+    float su[KG * 4], sl[KG * 4];
+#pragma unroll
+    for (int k = 0; k < KG * 4; ++k) su[k] = sl[k] = 0.f;
+    int err_exp = 0;
+    for (int j = warp; j < n; j += kSm4Consumers) {
+      const long long ti = t0 + j;
+      const int st = (int)(ti % kSm4Stages);
+      const double xlb = sc.lb[nb + j], xub = sc.ub[nb + j];  // issued before the wait
+      sm4_wait(full + st, (uint32_t)((ti / kSm4Stages) & 1));
+      const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * D);
+      const float4* r4 = c4 + D / 4;
+      float4 cv[KG], rv[KG];
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        cv[k] = c4[lane + 32 * k];
+        rv[k] = r4[lane + 32 * k];
+      }
+      // generic-proxy reads of the stage precede the producer's next async-proxy (TMA) write
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(empty + st);
+      float fu = 0.f, fl = 0.f;
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        fu = qacc_f<Q>(fu, cv[k].x + rv[k].x); fl = qacc_f<Q>(fl, cv[k].x - rv[k].x);
+        fu = qacc_f<Q>(fu, cv[k].y + rv[k].y); fl = qacc_f<Q>(fl, cv[k].y - rv[k].y);
+        fu = qacc_f<Q>(fu, cv[k].z + rv[k].z); fl = qacc_f<Q>(fl, cv[k].z - rv[k].z);
+        fu = qacc_f<Q>(fu, cv[k].w + rv[k].w); fl = qacc_f<Q>(fl, cv[k].w - rv[k].w);
+      }
+      const double nu = fin.fin(group_reduce<Q>((double)fu, 32)), nl = fin.fin(group_reduce<Q>((double)fl, 32));
+      Lines ln;
+      const int code = envelope(RELAX_EXP, xlb - e * nl, xub + e * nu, ln);
+      if (code) err_exp = err_exp ? min(err_exp, code) : code;
+      const float au = (float)ln.au, al = (float)ln.al;
+      if (lane == 0) {
+        a_lo_f[j] = al;
+        a_up_f[j] = au;
+        const double ub2 = ln.au * (ln.au >= 0.0 ? xub : xlb) + ln.bu;
+        const double lb2 = ln.al * (ln.al >= 0.0 ? xlb : xub) + ln.bl;
+        e_ub[j] = ub2;
+        e_lb[j] = lb2;
+        e_lo[j] = lb2 - e * fabs(ln.al) * (ln.al >= 0.0 ? nl : nu);  // ||a v||_q = |a| ||v||_q
+      }
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        const float cc[4] = {cv[k].x, cv[k].y, cv[k].z, cv[k].w}, rr[4] = {rv[k].x, rv[k].y, rv[k].z, rv[k].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float u = cc[q] + rr[q], l = cc[q] - rr[q];
+          su[4 * k + q] += au * (au >= 0.f ? u : l);
+          sl[4 * k + q] += al * (al >= 0.f ? l : u);
+        }
+      }
+    }
+    if (err_exp && lane == 0) set_status(status, s, site_exp, err_exp);
+    {
+      float4* pu = reinterpret_cast<float4*>(part + (size_t)warp * 2 * D);
+      float4* pl = pu + D / 4;
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        pu[lane + 32 * k] = make_float4(su[4 * k], su[4 * k + 1], su[4 * k + 2], su[4 * k + 3]);
+        pl[lane + 32 * k] = make_float4(sl[4 * k], sl[4 * k + 1], sl[4 * k + 2], sl[4 * k + 3]);
+      }
+    }
+    sm4_sync();
+    // Σ rows (warp partials combined in warp order, f64), their norms, the SumReduce bias
+    double pnu = 0.0, pnl = 0.0;
+    double sud[D / (kSm4Consumers * 32) > 0 ? D / (kSm4Consumers * 32) : 1];
+    double sld[D / (kSm4Consumers * 32) > 0 ? D / (kSm4Consumers * 32) : 1];
+    constexpr int kPer = D / (kSm4Consumers * 32);  // columns per consumer thread (D >= 256)
+    if (kPer > 0) {
+#pragma unroll
+      for (int m = 0; m < kPer; ++m) {
+        const int d = tid + m * kSm4Consumers * 32;
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < kSm4Consumers; ++w) {
+          a += (double)part[(size_t)w * 2 * D + d];
+          b += (double)part[(size_t)w * 2 * D + D + d];
+        }
+        sud[m] = a;
+        sld[m] = b;
+        pnu = qcombine<Q>(pnu, qpart<Q>(a));
+        pnl = qcombine<Q>(pnl, qpart<Q>(b));
+      }
+    } else if (tid < D) {
+      double a = 0.0, b = 0.0;
+      for (int w = 0; w < kSm4Consumers; ++w) {
+        a += (double)part[(size_t)w * 2 * D + tid];
+        b += (double)part[(size_t)w * 2 * D + D + tid];
+      }
+      sud[0] = a;
+      sld[0] = b;
+      pnu = qpart<Q>(a);
+      pnl = qpart<Q>(b);
+    }
+    if (warp == 0) {  // propagate_sum_axis bias (relax.cpp:728-731)
+      double a = 0.0, b = 0.0;
+      for (int j = lane; j < n; j += 32) {
+        a += e_lb[j];
+        b += e_ub[j];
+      }
+      a = warp_sum(a);
+      b = warp_sum(b);
+      if (lane == 0) {
+        scal[4] = a;
+        scal[5] = b;
+      }
+    }
+    const double nsu = sm4_reduce<Q>(pnu, red);
+    const double nsl = sm4_reduce<Q>(pnl, red);
+    if (tid == 0) {
+      const double slb = scal[4], sub_ = scal[5];
+      Lines ln;
+      const int code = envelope(RELAX_RECIP, slb - e * fin.fin(nsl), sub_ + e * fin.fin(nsu), ln);
+      if (code) set_status(status, s, site_recip, code);
+      scal[0] = ln.al;
+      scal[1] = ln.au;
+      scal[2] = ln.al * (ln.al >= 0.0 ? slb : sub_) + ln.bl;
+      scal[3] = ln.au * (ln.au >= 0.0 ? sub_ : slb) + ln.bu;
+    }
+    sm4_sync();
+    const double r_al = scal[0], r_au = scal[1], r_lb = scal[2], r_ub = scal[3];
+    pnu = pnl = 0.0;
+    const int nmine = kPer > 0 ? kPer : (tid < D ? 1 : 0);
+    for (int m = 0; m < nmine; ++m) {
+      const int d = tid + m * kSm4Consumers * 32;
+      const double u = sud[m], l = sld[m];
+      const double yu = r_au * (r_au >= 0.0 ? u : l), yl = r_al * (r_al >= 0.0 ? l : u);
+      ru_f[d] = (float)yu;
+      rl_f[d] = (float)yl;
+      pnu = qcombine<Q>(pnu, qpart<Q>(yu));
+      pnl = qcombine<Q>(pnl, qpart<Q>(yl));
+    }
+    const double nru = sm4_reduce<Q>(pnu, red);
+    const double nrl = sm4_reduce<Q>(pnl, red);  // (its barriers also publish ru_f / rl_f)
+    const double r_lo = r_lb - e * fin.fin(nrl);
+    const double r_hi = r_ub + e * fin.fin(nru);
+
+    // pass 2: MulBroadcast per key, written to HBM
+    const float ly = (float)r_lo, uy = (float)r_hi;
+    const bool ly_p = ly >= 0.f, uy_p = uy >= 0.f;
+    float4 yuv[KG], ylv[KG];
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      yuv[k] = reinterpret_cast<const float4*>(ru_f)[lane + 32 * k];
+      ylv[k] = reinterpret_cast<const float4*>(rl_f)[lane + 32 * k];
+    }
+    for (int j = warp; j < n; j += kSm4Consumers) {
+      const long long ti = t0 + n + j;
+      const int st = (int)(ti % kSm4Stages);
+      const float au = a_up_f[j], al = a_lo_f[j], lx = (float)e_lo[j];
+      const bool au_p = au >= 0.f, al_p = al >= 0.f, lx_p = lx >= 0.f;
+      sm4_wait(full + st, (uint32_t)((ti / kSm4Stages) & 1));
+      const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * D);
+      const float4* r4 = c4 + D / 4;
+      float4 cv[KG], rv[KG];
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        cv[k] = c4[lane + 32 * k];
+        rv[k] = r4[lane + 32 * k];
+      }
+      // generic-proxy reads of the stage precede the producer's next async-proxy (TMA) write
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(empty + st);
+      float4* gc = reinterpret_cast<float4*>(cbw + (long long)j * D);
+      float4* gr = reinterpret_cast<float4*>(rbw + (long long)j * D);
+      float fu = 0.f, fl = 0.f;
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        const float cc[4] = {cv[k].x, cv[k].y, cv[k].z, cv[k].w}, rr[4] = {rv[k].x, rv[k].y, rv[k].z, rv[k].w};
+        const float yuu[4] = {yuv[k].x, yuv[k].y, yuv[k].z, yuv[k].w};
+        const float yll[4] = {ylv[k].x, ylv[k].y, ylv[k].z, ylv[k].w};
+        float oc[4], orr[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float u = cc[q] + rr[q], l = cc[q] - rr[q];
+          const float eu = au * (au_p ? u : l), el = al * (al_p ? l : u);
+          // relax.cpp:542-567: lower plane (cx = ly, cy = lx), upper plane (cx = uy, cy = lx)
+          const float p_l = __fmaf_rn(ly, ly_p ? el : eu, lx * (lx_p ? yll[q] : yuu[q]));
+          const float p_u = __fmaf_rn(uy, uy_p ? eu : el, lx * (lx_p ? yuu[q] : yll[q]));
+          oc[q] = 0.5f * (p_u + p_l);
+          orr[q] = 0.5f * (p_u - p_l);
+          fu = qacc_f<Q>(fu, p_u);
+          fl = qacc_f<Q>(fl, p_l);
+        }
+        gc[lane + 32 * k] = make_float4(oc[0], oc[1], oc[2], oc[3]);
+        gr[lane + 32 * k] = make_float4(orr[0], orr[1], orr[2], orr[3]);
+      }
+      const double gu = group_reduce<Q>((double)fu, 32), gl = group_reduce<Q>((double)fl, 32);
+      if (lane == 0) {
+        double olb = 0.0, oub = 0.0;
+        term_bias(e_lo[j], r_lo, r_hi, e_lb[j], e_ub[j], r_lb, r_ub, olb, oub);
+        const long long o = nb + j;
+        sc.lb[o] = olb;
+        sc.ub[o] = oub;
+        if (sc.lo) {
+          sc.lo[o] = olb - e * fin.fin(gl);
+          sc.hi[o] = oub + e * fin.fin(gu);
+        }
+      }
+    }
+    sm4_sync();  // per-key arrays / partials are rewritten by the next row
+  }
+  }
+  __syncthreads();  // the producer warp stays resident until every stage has been consumed
+}
+
 size_t softmax3_smem(int n, int Dc, int CS, int nbuf) {
   return (size_t)nbuf * n * Dc * 8 + (size_t)Dc * 8 + (size_t)Dc * 16 + (size_t)n * 6 * 8 +
          (size_t)2 * CS * 2 * n * 8 + (size_t)8 * CS * 8 + (32 + 8) * 8 + (size_t)8 * kSm3Threads * 8 +
@@ -2000,6 +2344,54 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
   const char* pe = getenv("FG_SM3_PERSIST");
   const char* te = getenv("FG_SM3_TILE_KB");
   const int nbuf = (pe && pe[0] == '1') ? 2 : 1;
+  const bool legacy = ver && (ver[0] == '1' || ver[0] == '2' || ver[0] == '3');
+  if (!legacy && (D == 128 || D == 256 || D == 512)) {  // streaming kernel (full D per CTA)
+    static const size_t pad = getenv("FG_SM4_PAD") ? (size_t)atoi(getenv("FG_SM4_PAD")) * 1024 : 0;
+    const size_t smem = softmax4_smem(n, D) + pad;
+    static size_t attr4[3][3] = {};
+    static int grid4[3][3] = {};
+    const int q = dual_norm(norm), kg = D == 128 ? 0 : (D == 256 ? 1 : 2);
+    const int nrows = S * rows_per_s;
+    auto launch = [&](auto kern) {
+      if (attr4[q][kg] < smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr4[q][kg] = smem;
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSm4Threads, smem) != cudaSuccess ||
+            per_sm < 1)
+          per_sm = 1;
+        grid4[q][kg] = per_sm * sms;
+      }
+      static const int grid_cap = getenv("FG_SM4_GRID") ? atoi(getenv("FG_SM4_GRID")) : 0;
+      const int gmax = grid_cap > 0 ? grid_cap : grid4[q][kg];
+      const int grid = nrows < gmax ? nrows : gmax;
+      // launched as (1-CTA) clusters: the bulk copies address the ring through the shared::cluster window
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)grid);
+      cfg.blockDim = dim3(kSm4Threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 1;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, kern, sc, rows_per_s, nrows, n, eps, status, site_exp, site_recip);
+    };
+#define SM4(QQ)                                                        \
+  if (kg == 0) launch(softmax4_kernel<QQ, 1>);                         \
+  else if (kg == 1) launch(softmax4_kernel<QQ, 2>);                    \
+  else launch(softmax4_kernel<QQ, 4>);
+    if (q == NORM_L1) { SM4(NORM_L1) }
+    else if (q == NORM_L2) { SM4(NORM_L2) }
+    else { SM4(NORM_LINF) }
+#undef SM4
+    return 1;
+  }
   const int cs = softmax3_cluster(n, D, nbuf, te ? atoi(te) : 64);
   if (cs > 0 && !(ver && (ver[0] == '1' || ver[0] == '2'))) {
     const size_t smem = softmax3_smem(n, D / cs, cs, nbuf);
