@@ -1292,31 +1292,36 @@ __global__ void __launch_bounds__(kSm3Threads) softmax3_kernel(NView sc, int row
 // ---------------------------------------------------------------------------
 // Softmax chain, streaming version (D <= 512, D % 128 == 0; the pass uses it when it applies).
 //
-// Persistent CTAs, one score row (s, h, i) at a time with the FULL perturbation width, so no
-// norm ever crosses a CTA: one producer warp streams key rows (c and r planes, 8·D bytes)
-// through an NS-stage shared-memory ring with cp.async.bulk + mbarriers, and NC consumer warps
-// take one key row each:
+// Persistent CTAs (4 per SM), one score row (s, h, i) at a time with the FULL perturbation
+// width, so no norm ever crosses a CTA: one producer warp streams key rows (c and r planes,
+// 8·D bytes) through a 2·NC-stage shared-memory ring with cp.async.bulk + mbarriers, and NC = 4
+// consumer warps take one key row each (stage s always belongs to warp s mod NC):
 //   pass 1  per key: q-norms of the exp input (warp reduction) -> ExpVerify envelope
 //           (relax.cpp:363-394) -> Σ_j e_j accumulated in the warp's registers;
 //   then    Σ rows combined over the warps in a fixed order -> RecipVerify (relax.cpp:396-424)
 //           -> r rows and their norms (block reduction among the consumers);
 //   pass 2  per key: McCormick e_j * r (relax.cpp:744-775) written to HBM, probs lb/ub/lo/hi.
-// Every row is streamed twice (the second read is an L2 hit for the row the CTA just read) and
-// written once.  The producer never waits on the consumers' reductions: it prefetches pass 2
+// Every row is streamed twice -- pass 2 in reverse key order, so it starts on the keys the CTA
+// read last, which are still in L2 -- and written once.  The producer warp stays resident to
+// the end (lanes of a warp exiting early while others still issue bulk copies lost mbarrier
+// arrivals on the B200 when two CTAs shared an SM).  The producer never waits on the consumers' reductions: it prefetches pass 2
 // of the row and pass 1 of the next row while Σ / recip / r are being formed, so HBM traffic
 // stays in flight through the serial part of the chain.  Element math f32, norms and O(N)
 // state f64, as softmax3_kernel.
-constexpr int kSm4Consumers = 8;
-// A multiple of the consumer count: the items of one stage are then always taken by the same
-// warp, so a warp never waits on a stage whose previous fill (issued earlier, but possibly
-// completing later -- bulk copies complete out of order) is still pending, which would let the
-// parity wait succeed one phase early.
-constexpr int kSm4Stages = 16;
-static_assert(kSm4Stages % kSm4Consumers == 0, "stage ownership must be per warp");
-constexpr int kSm4Threads = (kSm4Consumers + 1) * 32;
+// A stage count that is a multiple of the consumer count: the items of one stage are then always
+// taken by the same warp, so a warp never waits on a stage whose previous fill (issued earlier,
+// but possibly completing later -- bulk copies complete out of order) is still pending, which
+// would let the parity wait succeed one phase early.
+template <int NC>
+struct Sm4 {
+  static constexpr int kStages = 2 * NC;
+  static constexpr int kThreads = (NC + 1) * 32;
+  static_assert(kStages % NC == 0, "stage ownership must be per warp");
+};
 
+template <int NC>
 __device__ __forceinline__ void sm4_sync() {  // consumer warps only
-  asm volatile("bar.sync 1, %0;" ::"r"(kSm4Consumers * 32) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
@@ -1332,37 +1337,50 @@ __device__ __forceinline__ void sm4_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-template <int Q>
-__device__ __forceinline__ double sm4_reduce(double v, double* red) {  // consumer-block q-combine
+// consumer-block q-combine of two values at once (red: >= 2*NC doubles)
+template <int Q, int NC>
+__device__ __forceinline__ void sm4_reduce2(double& a, double& b, double* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  v = (Q == NORM_LINF) ? warp_max(v) : warp_sum(v);
-  sm4_sync();
-  if (lane == 0) red[w] = v;
-  sm4_sync();
-  double r = red[0];
-  for (int i = 1; i < kSm4Consumers; ++i) r = qcombine<Q>(r, red[i]);
-  return r;
+  if (Q == NORM_LINF) {
+    a = warp_max(a);
+    b = warp_max(b);
+  } else {
+    a = warp_sum(a);
+    b = warp_sum(b);
+  }
+  sm4_sync<NC>();
+  if (lane == 0) {
+    red[w] = a;
+    red[NC + w] = b;
+  }
+  sm4_sync<NC>();
+  a = red[0];
+  b = red[NC];
+  for (int i = 1; i < NC; ++i) {
+    a = qcombine<Q>(a, red[i]);
+    b = qcombine<Q>(b, red[NC + i]);
+  }
 }
 
-size_t softmax4_smem(int n, int D) {
-  return (size_t)kSm4Stages * 8 * D              // ring
-         + (size_t)kSm4Consumers * 2 * D * 4     // Σ partials per warp
+size_t softmax4_smem(int n, int D, int NC) {
+  return (size_t)(2 * NC) * 8 * D                // ring
+         + (size_t)NC * 2 * D * 4                // Σ partials per warp
          + (size_t)2 * D * 4                     // r rows (f32)
          + (size_t)(n + 1) * (2 * 4 + 3 * 8)     // a_lo_f, a_up_f, e_lb, e_ub, e_lo
          + 64 * 8                                // red + scal
-         + 2 * kSm4Stages * 8 + 64;              // barriers + alignment
+         + 2 * (2 * NC) * 8 + 64;                // barriers + alignment
 }
 
-template <int Q, int KG>  // KG = D / 128 float4 groups per lane per plane
-__global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int rows_per_s, int nrows, int n,
+template <int Q, int KG, int NC>  // KG = D / 128 float4 groups per lane per plane; NC consumer warps
+__global__ void __launch_bounds__(Sm4<NC>::kThreads, NC <= 2 ? 6 : (NC <= 4 ? 4 : 2)) softmax4_kernel(NView sc, int rows_per_s, int nrows, int n,
                                                                   const double* __restrict__ eps,
                                                                   int* __restrict__ status, int site_exp,
                                                                   int site_recip) {
   constexpr int D = KG * 128;
   extern __shared__ __align__(16) unsigned char sm4[];
   float* ring = reinterpret_cast<float*>(sm4);                          // [NS][c|r][D]
-  float* part = ring + (size_t)kSm4Stages * 2 * D;                      // [NC][u|l][D]
-  float* ru_f = part + (size_t)kSm4Consumers * 2 * D;                   // [D]
+  float* part = ring + (size_t)Sm4<NC>::kStages * 2 * D;                      // [NC][u|l][D]
+  float* ru_f = part + (size_t)NC * 2 * D;                   // [D]
   float* rl_f = ru_f + D;                                               // [D]
   const int n2 = (n + 1) & ~1;                                          // keeps the f64 arrays aligned
   float* a_lo_f = rl_f + D;                                             // [n]
@@ -1373,11 +1391,11 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
   double* red = e_lo + n;    // [32]
   double* scal = red + 32;   // [32]
   uint64_t* full = reinterpret_cast<uint64_t*>(scal + 32);
-  uint64_t* empty = full + kSm4Stages;
+  uint64_t* empty = full + Sm4<NC>::kStages;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    for (int b = 0; b < kSm4Stages; ++b) {
+    for (int b = 0; b < Sm4<NC>::kStages; ++b) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(full + b)) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(empty + b)) : "memory");
     }
@@ -1385,7 +1403,7 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
   }
   __syncthreads();
 
-  if (warp == kSm4Consumers) {  // ---- producer
+  if (warp == NC) {  // ---- producer
     if (lane == 0) {
       long long t = 0;
       for (int rid = blockIdx.x; rid < nrows; rid += gridDim.x) {
@@ -1395,20 +1413,21 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
         const float* rb = cb + sc.cr;
         for (int p = 0; p < 2; ++p)
           for (int j = 0; j < n; ++j, ++t) {
-            const int st = (int)(t % kSm4Stages);
-            const uint32_t ph = (uint32_t)((t / kSm4Stages) & 1);
-            if (t >= kSm4Stages) sm4_wait(empty + st, ph ^ 1u);
+            const int st = (int)(t % Sm4<NC>::kStages);
+            const uint32_t ph = (uint32_t)((t / Sm4<NC>::kStages) & 1);
+            if (t >= Sm4<NC>::kStages) sm4_wait(empty + st, ph ^ 1u);
             float* dst = ring + (size_t)st * 2 * D;
+            const int key = p == 0 ? j : n - 1 - j;  // pass 2 in reverse: the latest keys are still in L2
             mbar_expect(full + st, 8u * D);
             asm volatile(
                 "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                     smem_addr(dst)),
-                "l"(cb + (long long)j * D), "r"(4u * D), "r"(smem_addr(full + st))
+                "l"(cb + (long long)key * D), "r"(4u * D), "r"(smem_addr(full + st))
                 : "memory");
             asm volatile(
                 "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                     smem_addr(dst + D)),
-                "l"(rb + (long long)j * D), "r"(4u * D), "r"(smem_addr(full + st))
+                "l"(rb + (long long)key * D), "r"(4u * D), "r"(smem_addr(full + st))
                 : "memory");
           }
       }
@@ -1429,11 +1448,11 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
 #pragma unroll
     for (int k = 0; k < KG * 4; ++k) su[k] = sl[k] = 0.f;
     int err_exp = 0;
-    for (int j = warp; j < n; j += kSm4Consumers) {
+    for (int j = warp; j < n; j += NC) {
       const long long ti = t0 + j;
-      const int st = (int)(ti % kSm4Stages);
+      const int st = (int)(ti % Sm4<NC>::kStages);
       const double xlb = sc.lb[nb + j], xub = sc.ub[nb + j];  // issued before the wait
-      sm4_wait(full + st, (uint32_t)((ti / kSm4Stages) & 1));
+      sm4_wait(full + st, (uint32_t)((ti / Sm4<NC>::kStages) & 1));
       const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * D);
       const float4* r4 = c4 + D / 4;
       float4 cv[KG], rv[KG];
@@ -1489,18 +1508,18 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
         pl[lane + 32 * k] = make_float4(sl[4 * k], sl[4 * k + 1], sl[4 * k + 2], sl[4 * k + 3]);
       }
     }
-    sm4_sync();
+    sm4_sync<NC>();
     // Σ rows (warp partials combined in warp order, f64), their norms, the SumReduce bias
     double pnu = 0.0, pnl = 0.0;
-    double sud[D / (kSm4Consumers * 32) > 0 ? D / (kSm4Consumers * 32) : 1];
-    double sld[D / (kSm4Consumers * 32) > 0 ? D / (kSm4Consumers * 32) : 1];
-    constexpr int kPer = D / (kSm4Consumers * 32);  // columns per consumer thread (D >= 256)
+    double sud[D / (NC * 32) > 0 ? D / (NC * 32) : 1];
+    double sld[D / (NC * 32) > 0 ? D / (NC * 32) : 1];
+    constexpr int kPer = D / (NC * 32);  // columns per consumer thread (D >= 256)
     if (kPer > 0) {
 #pragma unroll
       for (int m = 0; m < kPer; ++m) {
-        const int d = tid + m * kSm4Consumers * 32;
+        const int d = tid + m * NC * 32;
         double a = 0.0, b = 0.0;
-        for (int w = 0; w < kSm4Consumers; ++w) {
+        for (int w = 0; w < NC; ++w) {
           a += (double)part[(size_t)w * 2 * D + d];
           b += (double)part[(size_t)w * 2 * D + D + d];
         }
@@ -1511,7 +1530,7 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
       }
     } else if (tid < D) {
       double a = 0.0, b = 0.0;
-      for (int w = 0; w < kSm4Consumers; ++w) {
+      for (int w = 0; w < NC; ++w) {
         a += (double)part[(size_t)w * 2 * D + tid];
         b += (double)part[(size_t)w * 2 * D + D + tid];
       }
@@ -1533,8 +1552,8 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
         scal[5] = b;
       }
     }
-    const double nsu = sm4_reduce<Q>(pnu, red);
-    const double nsl = sm4_reduce<Q>(pnl, red);
+    sm4_reduce2<Q, NC>(pnu, pnl, red);
+    const double nsu = pnu, nsl = pnl;
     if (tid == 0) {
       const double slb = scal[4], sub_ = scal[5];
       Lines ln;
@@ -1545,12 +1564,12 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
       scal[2] = ln.al * (ln.al >= 0.0 ? slb : sub_) + ln.bl;
       scal[3] = ln.au * (ln.au >= 0.0 ? sub_ : slb) + ln.bu;
     }
-    sm4_sync();
+    sm4_sync<NC>();
     const double r_al = scal[0], r_au = scal[1], r_lb = scal[2], r_ub = scal[3];
     pnu = pnl = 0.0;
     const int nmine = kPer > 0 ? kPer : (tid < D ? 1 : 0);
     for (int m = 0; m < nmine; ++m) {
-      const int d = tid + m * kSm4Consumers * 32;
+      const int d = tid + m * NC * 32;
       const double u = sud[m], l = sld[m];
       const double yu = r_au * (r_au >= 0.0 ? u : l), yl = r_al * (r_al >= 0.0 ? l : u);
       ru_f[d] = (float)yu;
@@ -1558,8 +1577,8 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
       pnu = qcombine<Q>(pnu, qpart<Q>(yu));
       pnl = qcombine<Q>(pnl, qpart<Q>(yl));
     }
-    const double nru = sm4_reduce<Q>(pnu, red);
-    const double nrl = sm4_reduce<Q>(pnl, red);  // (its barriers also publish ru_f / rl_f)
+    sm4_reduce2<Q, NC>(pnu, pnl, red);  // (its barriers also publish ru_f / rl_f)
+    const double nru = pnu, nrl = pnl;
     const double r_lo = r_lb - e * fin.fin(nrl);
     const double r_hi = r_ub + e * fin.fin(nru);
 
@@ -1572,12 +1591,13 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
       yuv[k] = reinterpret_cast<const float4*>(ru_f)[lane + 32 * k];
       ylv[k] = reinterpret_cast<const float4*>(rl_f)[lane + 32 * k];
     }
-    for (int j = warp; j < n; j += kSm4Consumers) {
-      const long long ti = t0 + n + j;
-      const int st = (int)(ti % kSm4Stages);
+    for (int m = warp; m < n; m += NC) {
+      const int j = n - 1 - m;  // the producer streams pass 2 in reverse key order
+      const long long ti = t0 + n + m;
+      const int st = (int)(ti % Sm4<NC>::kStages);
       const float au = a_up_f[j], al = a_lo_f[j], lx = (float)e_lo[j];
       const bool au_p = au >= 0.f, al_p = al >= 0.f, lx_p = lx >= 0.f;
-      sm4_wait(full + st, (uint32_t)((ti / kSm4Stages) & 1));
+      sm4_wait(full + st, (uint32_t)((ti / Sm4<NC>::kStages) & 1));
       const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * D);
       const float4* r4 = c4 + D / 4;
       float4 cv[KG], rv[KG];
@@ -1627,7 +1647,7 @@ __global__ void __launch_bounds__(kSm4Threads, 2) softmax4_kernel(NView sc, int 
         }
       }
     }
-    sm4_sync();  // per-key arrays / partials are rewritten by the next row
+    sm4_sync<NC>();  // per-key arrays / partials are rewritten by the next row
   }
   }
   __syncthreads();  // the producer warp stays resident until every stage has been consumed
@@ -2346,49 +2366,43 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
   const int nbuf = (pe && pe[0] == '1') ? 2 : 1;
   const bool legacy = ver && (ver[0] == '1' || ver[0] == '2' || ver[0] == '3');
   if (!legacy && (D == 128 || D == 256 || D == 512)) {  // streaming kernel (full D per CTA)
+    static const int nc_env = getenv("FG_SM4_NC") ? atoi(getenv("FG_SM4_NC")) : 0;
+    const int NCsel = nc_env == 8 ? 8 : 4;  // default: 4 consumer warps, 4 CTAs per SM
     static const size_t pad = getenv("FG_SM4_PAD") ? (size_t)atoi(getenv("FG_SM4_PAD")) * 1024 : 0;
-    const size_t smem = softmax4_smem(n, D) + pad;
-    static size_t attr4[3][3] = {};
-    static int grid4[3][3] = {};
-    const int q = dual_norm(norm), kg = D == 128 ? 0 : (D == 256 ? 1 : 2);
+    const size_t smem = softmax4_smem(n, D, NCsel) + pad;
+    static size_t attr4[3][3][3] = {};
+    static int grid4[3][3][3] = {};
+    const int q = dual_norm(norm), kg = D == 128 ? 0 : (D == 256 ? 1 : 2), ci = NCsel == 4 ? 0 : 1;
     const int nrows = S * rows_per_s;
-    auto launch = [&](auto kern) {
-      if (attr4[q][kg] < smem) {
+    auto launch = [&](auto kern, int threads) {
+      if (attr4[ci][q][kg] < smem) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr4[q][kg] = smem;
+        attr4[ci][q][kg] = smem;
         int per_sm = 0, dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSm4Threads, smem) != cudaSuccess ||
-            per_sm < 1)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
           per_sm = 1;
-        grid4[q][kg] = per_sm * sms;
+        grid4[ci][q][kg] = per_sm * sms;
       }
       static const int grid_cap = getenv("FG_SM4_GRID") ? atoi(getenv("FG_SM4_GRID")) : 0;
-      const int gmax = grid_cap > 0 ? grid_cap : grid4[q][kg];
+      const int gmax = grid_cap > 0 ? grid_cap : grid4[ci][q][kg];
       const int grid = nrows < gmax ? nrows : gmax;
-      // launched as (1-CTA) clusters: the bulk copies address the ring through the shared::cluster window
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)grid);
-      cfg.blockDim = dim3(kSm4Threads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = st;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 1;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, kern, sc, rows_per_s, nrows, n, eps, status, site_exp, site_recip);
+      kern<<<grid, threads, smem, st>>>(sc, rows_per_s, nrows, n, eps, status, site_exp, site_recip);
     };
-#define SM4(QQ)                                                        \
-  if (kg == 0) launch(softmax4_kernel<QQ, 1>);                         \
-  else if (kg == 1) launch(softmax4_kernel<QQ, 2>);                    \
-  else launch(softmax4_kernel<QQ, 4>);
-    if (q == NORM_L1) { SM4(NORM_L1) }
-    else if (q == NORM_L2) { SM4(NORM_L2) }
-    else { SM4(NORM_LINF) }
+#define SM4(QQ, NCC)                                                                  \
+  if (kg == 0) launch(softmax4_kernel<QQ, 1, NCC>, Sm4<NCC>::kThreads);               \
+  else if (kg == 1) launch(softmax4_kernel<QQ, 2, NCC>, Sm4<NCC>::kThreads);          \
+  else launch(softmax4_kernel<QQ, 4, NCC>, Sm4<NCC>::kThreads);
+    if (NCsel == 4) {
+      if (q == NORM_L1) { SM4(NORM_L1, 4) }
+      else if (q == NORM_L2) { SM4(NORM_L2, 4) }
+      else { SM4(NORM_LINF, 4) }
+    } else {
+      if (q == NORM_L1) { SM4(NORM_L1, 8) }
+      else if (q == NORM_L2) { SM4(NORM_L2, 8) }
+      else { SM4(NORM_LINF, 8) }
+    }
 #undef SM4
     return 1;
   }
