@@ -1312,9 +1312,10 @@ __global__ void __launch_bounds__(kSm3Threads) softmax3_kernel(NView sc, int row
 // taken by the same warp, so a warp never waits on a stage whose previous fill (issued earlier,
 // but possibly completing later -- bulk copies complete out of order) is still pending, which
 // would let the parity wait succeed one phase early.
-template <int NC>
+template <int NC, int KG>
 struct Sm4 {
-  static constexpr int kStages = 2 * NC;
+  // 8·D-byte key rows; 32 KB of ring per CTA whatever D is (more, smaller stages for small D)
+  static constexpr int kStages = NC * (8 / KG);
   static constexpr int kThreads = (NC + 1) * 32;
   static_assert(kStages % NC == 0, "stage ownership must be per warp");
 };
@@ -1363,23 +1364,23 @@ __device__ __forceinline__ void sm4_reduce2(double& a, double& b, double* red) {
 }
 
 size_t softmax4_smem(int n, int D, int NC) {
-  return (size_t)(2 * NC) * 8 * D                // ring
+  return (size_t)NC * (8 / (D / 128)) * 8 * D    // ring
          + (size_t)NC * 2 * D * 4                // Σ partials per warp
          + (size_t)2 * D * 4                     // r rows (f32)
          + (size_t)(n + 1) * (2 * 4 + 3 * 8)     // a_lo_f, a_up_f, e_lb, e_ub, e_lo
          + 64 * 8                                // red + scal
-         + 2 * (2 * NC) * 8 + 64;                // barriers + alignment
+         + 2 * (size_t)NC * (8 / (D / 128)) * 8 + 64;  // barriers + alignment
 }
 
 template <int Q, int KG, int NC>  // KG = D / 128 float4 groups per lane per plane; NC consumer warps
-__global__ void __launch_bounds__(Sm4<NC>::kThreads, NC <= 2 ? 6 : (NC <= 4 ? 4 : 2)) softmax4_kernel(NView sc, int rows_per_s, int nrows, int n,
+__global__ void __launch_bounds__(Sm4<NC, KG>::kThreads, NC <= 4 ? 4 : 2) softmax4_kernel(NView sc, int rows_per_s, int nrows, int n,
                                                                   const double* __restrict__ eps,
                                                                   int* __restrict__ status, int site_exp,
                                                                   int site_recip) {
   constexpr int D = KG * 128;
   extern __shared__ __align__(16) unsigned char sm4[];
   float* ring = reinterpret_cast<float*>(sm4);                          // [NS][c|r][D]
-  float* part = ring + (size_t)Sm4<NC>::kStages * 2 * D;                      // [NC][u|l][D]
+  float* part = ring + (size_t)Sm4<NC, KG>::kStages * 2 * D;                      // [NC][u|l][D]
   float* ru_f = part + (size_t)NC * 2 * D;                   // [D]
   float* rl_f = ru_f + D;                                               // [D]
   const int n2 = (n + 1) & ~1;                                          // keeps the f64 arrays aligned
@@ -1391,11 +1392,11 @@ __global__ void __launch_bounds__(Sm4<NC>::kThreads, NC <= 2 ? 6 : (NC <= 4 ? 4 
   double* red = e_lo + n;    // [32]
   double* scal = red + 32;   // [32]
   uint64_t* full = reinterpret_cast<uint64_t*>(scal + 32);
-  uint64_t* empty = full + Sm4<NC>::kStages;
+  uint64_t* empty = full + Sm4<NC, KG>::kStages;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
-    for (int b = 0; b < Sm4<NC>::kStages; ++b) {
+    for (int b = 0; b < Sm4<NC, KG>::kStages; ++b) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(full + b)) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(empty + b)) : "memory");
     }
@@ -1413,9 +1414,9 @@ __global__ void __launch_bounds__(Sm4<NC>::kThreads, NC <= 2 ? 6 : (NC <= 4 ? 4 
         const float* rb = cb + sc.cr;
         for (int p = 0; p < 2; ++p)
           for (int j = 0; j < n; ++j, ++t) {
-            const int st = (int)(t % Sm4<NC>::kStages);
-            const uint32_t ph = (uint32_t)((t / Sm4<NC>::kStages) & 1);
-            if (t >= Sm4<NC>::kStages) sm4_wait(empty + st, ph ^ 1u);
+            const int st = (int)(t % Sm4<NC, KG>::kStages);
+            const uint32_t ph = (uint32_t)((t / Sm4<NC, KG>::kStages) & 1);
+            if (t >= Sm4<NC, KG>::kStages) sm4_wait(empty + st, ph ^ 1u);
             float* dst = ring + (size_t)st * 2 * D;
             const int key = p == 0 ? j : n - 1 - j;  // pass 2 in reverse: the latest keys are still in L2
             mbar_expect(full + st, 8u * D);
@@ -1450,9 +1451,9 @@ __global__ void __launch_bounds__(Sm4<NC>::kThreads, NC <= 2 ? 6 : (NC <= 4 ? 4 
     int err_exp = 0;
     for (int j = warp; j < n; j += NC) {
       const long long ti = t0 + j;
-      const int st = (int)(ti % Sm4<NC>::kStages);
+      const int st = (int)(ti % Sm4<NC, KG>::kStages);
       const double xlb = sc.lb[nb + j], xub = sc.ub[nb + j];  // issued before the wait
-      sm4_wait(full + st, (uint32_t)((ti / Sm4<NC>::kStages) & 1));
+      sm4_wait(full + st, (uint32_t)((ti / Sm4<NC, KG>::kStages) & 1));
       const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * D);
       const float4* r4 = c4 + D / 4;
       float4 cv[KG], rv[KG];
@@ -1594,10 +1595,10 @@ __global__ void __launch_bounds__(Sm4<NC>::kThreads, NC <= 2 ? 6 : (NC <= 4 ? 4 
     for (int m = warp; m < n; m += NC) {
       const int j = n - 1 - m;  // the producer streams pass 2 in reverse key order
       const long long ti = t0 + n + m;
-      const int st = (int)(ti % Sm4<NC>::kStages);
+      const int st = (int)(ti % Sm4<NC, KG>::kStages);
       const float au = a_up_f[j], al = a_lo_f[j], lx = (float)e_lo[j];
       const bool au_p = au >= 0.f, al_p = al >= 0.f, lx_p = lx >= 0.f;
-      sm4_wait(full + st, (uint32_t)((ti / Sm4<NC>::kStages) & 1));
+      sm4_wait(full + st, (uint32_t)((ti / Sm4<NC, KG>::kStages) & 1));
       const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * D);
       const float4* r4 = c4 + D / 4;
       float4 cv[KG], rv[KG];
@@ -2365,7 +2366,11 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
   const char* te = getenv("FG_SM3_TILE_KB");
   const int nbuf = (pe && pe[0] == '1') ? 2 : 1;
   const bool legacy = ver && (ver[0] == '1' || ver[0] == '2' || ver[0] == '3');
-  if (!legacy && (D == 128 || D == 256 || D == 512)) {  // streaming kernel (full D per CTA)
+  // streaming kernel (full D per CTA) where a key row is wide enough to amortise its per-key
+  // envelope and reductions (measured: D = 512 3.3 vs 7.2 ms per c3 pass; D = 128 2.06 vs 1.98 ms
+  // per c2 pass for the cluster kernel, which stays the choice there)
+  static const bool force4 = getenv("FG_SM4_ALL") != nullptr;
+  if (!legacy && (D == 256 || D == 512 || (force4 && D == 128))) {
     static const int nc_env = getenv("FG_SM4_NC") ? atoi(getenv("FG_SM4_NC")) : 0;
     const int NCsel = nc_env == 8 ? 8 : 4;  // default: 4 consumer warps, 4 CTAs per SM
     static const size_t pad = getenv("FG_SM4_PAD") ? (size_t)atoi(getenv("FG_SM4_PAD")) * 1024 : 0;
@@ -2391,9 +2396,9 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
       kern<<<grid, threads, smem, st>>>(sc, rows_per_s, nrows, n, eps, status, site_exp, site_recip);
     };
 #define SM4(QQ, NCC)                                                                  \
-  if (kg == 0) launch(softmax4_kernel<QQ, 1, NCC>, Sm4<NCC>::kThreads);               \
-  else if (kg == 1) launch(softmax4_kernel<QQ, 2, NCC>, Sm4<NCC>::kThreads);          \
-  else launch(softmax4_kernel<QQ, 4, NCC>, Sm4<NCC>::kThreads);
+  if (kg == 0) launch(softmax4_kernel<QQ, 1, NCC>, Sm4<NCC, 1>::kThreads);               \
+  else if (kg == 1) launch(softmax4_kernel<QQ, 2, NCC>, Sm4<NCC, 2>::kThreads);          \
+  else launch(softmax4_kernel<QQ, 4, NCC>, Sm4<NCC, 4>::kThreads);
     if (NCsel == 4) {
       if (q == NORM_L1) { SM4(NORM_L1, 4) }
       else if (q == NORM_L2) { SM4(NORM_L2, 4) }
