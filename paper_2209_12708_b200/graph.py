@@ -1,6 +1,6 @@
 """faith-graph/v1 verification graphs on the device.
 
-``load_graph`` / ``graph_from_json`` parse the reference's graph schema (``graph::to_json`` /
+``load_graph`` / ``graph_from_json`` / ``to_json`` read and write the reference's graph schema (``graph::to_json`` /
 ``graph_from_json``, proj/src/graph.cpp:781-850, README "File formats") and check it the way
 ``VerGraph::validate`` does (graph.cpp:133-160: dense ordered ids, no forward edges, weights bound
 to constants, every operator in exactly one fusion group).  :class:`Graph` uploads the constant
@@ -138,6 +138,24 @@ def graph_from_json(text: str) -> VerGraph:
     g = VerGraph(nodes, constants, groups)
     g.validate()
     return g
+
+
+def to_json(g: VerGraph) -> str:
+    """graph::to_json (graph.cpp:781-814): nodes with kind, attrs, role-named edges, shape and
+    the constant index of weights; the constant table; the fusion groups.  Keys sorted and
+    compact separators, as nlohmann::json::dump() writes them."""
+    nodes = []
+    for n in g.nodes:
+        jn = {"id": n.id, "kind": n.kind, "attrs": dict(n.attrs), "shape": list(n.shape)}
+        if n.inputs:
+            jn["edges"] = {r: x for r, x in zip(input_roles(n.kind, len(n.inputs)), n.inputs)}
+        if n.kind == "weight":
+            jn["constant"] = n.constant
+        nodes.append(jn)
+    consts = [{"shape": list(c.shape), "data": [float(v) for v in np.asarray(c, dtype=np.float64).reshape(-1)]}
+              for c in g.constants]
+    j = {"format": "faith-graph/v1", "nodes": nodes, "constants": consts, "fusion_groups": g.fusion_groups}
+    return json.dumps(j, sort_keys=True, separators=(",", ":"))
 
 
 def load_graph(path: str) -> VerGraph:

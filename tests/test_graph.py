@@ -70,3 +70,11 @@ def test_missing_fusion_groups_default_to_singletons():
     g = G.graph_from_json(_mutate(lambda j: j.pop("fusion_groups")))
     ops = [n.id for n in g.nodes if n.kind not in ("input", "weight")]
     assert g.fusion_groups == [[i] for i in ops]
+
+
+@pytest.mark.parametrize("path", GRAPHS, ids=[os.path.basename(p)[:-11] for p in GRAPHS])
+def test_export_is_byte_identical_to_reference(path):
+    """graph::to_json (graph.cpp:781-814): parse -> export reproduces the reference's own bytes."""
+    with open(path) as f:
+        text = f.read().strip()
+    assert G.to_json(G.graph_from_json(text)) == text
