@@ -170,6 +170,28 @@ __device__ __forceinline__ double silu_derivative(double x) {
   return s * (1.0 + x * (1.0 - s));
 }
 
+// ExpVerify envelope alone (relax.cpp:363-394), inlined where it sits on a per-key dependency
+// chain (the three exponentials are independent and overlap).  Same arithmetic as envelope().
+__device__ __forceinline__ int exp_envelope(double lo, double hi, Lines& r) {
+  r.al = r.bl = r.au = r.bu = 0.0;
+  if (lo > hi) return kCodeInval;
+  const double m = 0.5 * (lo + hi), c2 = lo + 15.0 / 16.0;
+  const double d = (c2 < m) ? c2 : m;
+  const double ed = exp(d), elo = exp(lo), ehi = exp(hi);
+  r.al = ed;
+  r.bl = ed - ed * d;
+  if (lo == hi) {
+    r.au = ed;
+    r.bu = ed - ed * d;
+  } else {
+    const double sl = (ehi - elo) / (hi - lo);
+    r.au = sl;
+    r.bu = elo - sl * lo;
+  }
+  if (!isfinite(r.bl) || !isfinite(r.au) || !isfinite(r.bu)) return kCodeDomain;
+  return 0;
+}
+
 // Envelope of `kind` on [lo, hi].  For SiLU the 257-point grid (relax.cpp:452-460) is
 // spread over the lanes of a warp when `lane`/`lanes` say so (min/max are exact, so the
 // result does not depend on the split).
@@ -1456,27 +1478,18 @@ __global__ void __launch_bounds__(Sm4<NC, KG>::kThreads, NC <= 4 ? 4 : 2) softma
       sm4_wait(full + st, (uint32_t)((ti / Sm4<NC, KG>::kStages) & 1));
       const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * D);
       const float4* r4 = c4 + D / 4;
-      float4 cv[KG], rv[KG];
-#pragma unroll
-      for (int k = 0; k < KG; ++k) {
-        cv[k] = c4[lane + 32 * k];
-        rv[k] = r4[lane + 32 * k];
-      }
-      // generic-proxy reads of the stage precede the producer's next async-proxy (TMA) write
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive1(empty + st);
       float fu = 0.f, fl = 0.f;
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
-        fu = qacc_f<Q>(fu, cv[k].x + rv[k].x); fl = qacc_f<Q>(fl, cv[k].x - rv[k].x);
-        fu = qacc_f<Q>(fu, cv[k].y + rv[k].y); fl = qacc_f<Q>(fl, cv[k].y - rv[k].y);
-        fu = qacc_f<Q>(fu, cv[k].z + rv[k].z); fl = qacc_f<Q>(fl, cv[k].z - rv[k].z);
-        fu = qacc_f<Q>(fu, cv[k].w + rv[k].w); fl = qacc_f<Q>(fl, cv[k].w - rv[k].w);
+        const float4 cv = c4[lane + 32 * k], rv = r4[lane + 32 * k];
+        fu = qacc_f<Q>(fu, cv.x + rv.x); fl = qacc_f<Q>(fl, cv.x - rv.x);
+        fu = qacc_f<Q>(fu, cv.y + rv.y); fl = qacc_f<Q>(fl, cv.y - rv.y);
+        fu = qacc_f<Q>(fu, cv.z + rv.z); fl = qacc_f<Q>(fl, cv.z - rv.z);
+        fu = qacc_f<Q>(fu, cv.w + rv.w); fl = qacc_f<Q>(fl, cv.w - rv.w);
       }
       const double nu = fin.fin(group_reduce<Q>((double)fu, 32)), nl = fin.fin(group_reduce<Q>((double)fl, 32));
       Lines ln;
-      const int code = envelope(RELAX_EXP, xlb - e * nl, xub + e * nu, ln);
+      const int code = exp_envelope(xlb - e * nl, xub + e * nu, ln);
       if (code) err_exp = err_exp ? min(err_exp, code) : code;
       const float au = (float)ln.au, al = (float)ln.al;
       if (lane == 0) {
@@ -1489,8 +1502,9 @@ __global__ void __launch_bounds__(Sm4<NC, KG>::kThreads, NC <= 4 ? 4 : 2) softma
         e_lo[j] = lb2 - e * fabs(ln.al) * (ln.al >= 0.0 ? nl : nu);  // ||a v||_q = |a| ||v||_q
       }
 #pragma unroll
-      for (int k = 0; k < KG; ++k) {
-        const float cc[4] = {cv[k].x, cv[k].y, cv[k].z, cv[k].w}, rr[4] = {rv[k].x, rv[k].y, rv[k].z, rv[k].w};
+      for (int k = 0; k < KG; ++k) {  // second read of the stage (SMEM): no row data live across the envelope
+        const float4 cv = c4[lane + 32 * k], rv = r4[lane + 32 * k];
+        const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float u = cc[q] + rr[q], l = cc[q] - rr[q];
@@ -1498,6 +1512,10 @@ __global__ void __launch_bounds__(Sm4<NC, KG>::kThreads, NC <= 4 ? 4 : 2) softma
           sl[4 * k + q] += al * (al >= 0.f ? l : u);
         }
       }
+      // generic-proxy reads of the stage precede the producer's next async-proxy (TMA) write
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(empty + st);
     }
     if (err_exp && lane == 0) set_status(status, s, site_exp, err_exp);
     {
@@ -1512,33 +1530,22 @@ __global__ void __launch_bounds__(Sm4<NC, KG>::kThreads, NC <= 4 ? 4 : 2) softma
     sm4_sync<NC>();
     // Σ rows (warp partials combined in warp order, f64), their norms, the SumReduce bias
     double pnu = 0.0, pnl = 0.0;
-    double sud[D / (NC * 32) > 0 ? D / (NC * 32) : 1];
-    double sld[D / (NC * 32) > 0 ? D / (NC * 32) : 1];
-    constexpr int kPer = D / (NC * 32);  // columns per consumer thread (D >= 256)
-    if (kPer > 0) {
+    constexpr int kPer = D / (NC * 32) > 0 ? D / (NC * 32) : 1;  // columns per consumer thread
+    double sud[kPer], sld[kPer];  // fully unrolled: registers
 #pragma unroll
-      for (int m = 0; m < kPer; ++m) {
-        const int d = tid + m * NC * 32;
-        double a = 0.0, b = 0.0;
+    for (int m = 0; m < kPer; ++m) {
+      const int d = tid + m * NC * 32;
+      double a = 0.0, b = 0.0;
+      if (d < D) {
         for (int w = 0; w < NC; ++w) {
           a += (double)part[(size_t)w * 2 * D + d];
           b += (double)part[(size_t)w * 2 * D + D + d];
         }
-        sud[m] = a;
-        sld[m] = b;
         pnu = qcombine<Q>(pnu, qpart<Q>(a));
         pnl = qcombine<Q>(pnl, qpart<Q>(b));
       }
-    } else if (tid < D) {
-      double a = 0.0, b = 0.0;
-      for (int w = 0; w < NC; ++w) {
-        a += (double)part[(size_t)w * 2 * D + tid];
-        b += (double)part[(size_t)w * 2 * D + D + tid];
-      }
-      sud[0] = a;
-      sld[0] = b;
-      pnu = qpart<Q>(a);
-      pnl = qpart<Q>(b);
+      sud[m] = a;
+      sld[m] = b;
     }
     if (warp == 0) {  // propagate_sum_axis bias (relax.cpp:728-731)
       double a = 0.0, b = 0.0;
@@ -1568,9 +1575,10 @@ __global__ void __launch_bounds__(Sm4<NC, KG>::kThreads, NC <= 4 ? 4 : 2) softma
     sm4_sync<NC>();
     const double r_al = scal[0], r_au = scal[1], r_lb = scal[2], r_ub = scal[3];
     pnu = pnl = 0.0;
-    const int nmine = kPer > 0 ? kPer : (tid < D ? 1 : 0);
-    for (int m = 0; m < nmine; ++m) {
+#pragma unroll
+    for (int m = 0; m < kPer; ++m) {
       const int d = tid + m * NC * 32;
+      if (d >= D) continue;
       const double u = sud[m], l = sld[m];
       const double yu = r_au * (r_au >= 0.0 ? u : l), yl = r_al * (r_al >= 0.0 ? l : u);
       ru_f[d] = (float)yu;
@@ -1586,12 +1594,8 @@ __global__ void __launch_bounds__(Sm4<NC, KG>::kThreads, NC <= 4 ? 4 : 2) softma
     // pass 2: MulBroadcast per key, written to HBM
     const float ly = (float)r_lo, uy = (float)r_hi;
     const bool ly_p = ly >= 0.f, uy_p = uy >= 0.f;
-    float4 yuv[KG], ylv[KG];
-#pragma unroll
-    for (int k = 0; k < KG; ++k) {
-      yuv[k] = reinterpret_cast<const float4*>(ru_f)[lane + 32 * k];
-      ylv[k] = reinterpret_cast<const float4*>(rl_f)[lane + 32 * k];
-    }
+    const float4* yu4 = reinterpret_cast<const float4*>(ru_f);  // r rows: re-read from SMEM per key
+    const float4* yl4 = reinterpret_cast<const float4*>(rl_f);  // (keeps pass 2 free of spills)
     for (int m = warp; m < n; m += NC) {
       const int j = n - 1 - m;  // the producer streams pass 2 in reverse key order
       const long long ti = t0 + n + m;
@@ -1617,8 +1621,9 @@ __global__ void __launch_bounds__(Sm4<NC, KG>::kThreads, NC <= 4 ? 4 : 2) softma
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
         const float cc[4] = {cv[k].x, cv[k].y, cv[k].z, cv[k].w}, rr[4] = {rv[k].x, rv[k].y, rv[k].z, rv[k].w};
-        const float yuu[4] = {yuv[k].x, yuv[k].y, yuv[k].z, yuv[k].w};
-        const float yll[4] = {ylv[k].x, ylv[k].y, ylv[k].z, ylv[k].w};
+        const float4 yuv = yu4[lane + 32 * k], ylv = yl4[lane + 32 * k];
+        const float yuu[4] = {yuv.x, yuv.y, yuv.z, yuv.w};
+        const float yll[4] = {ylv.x, ylv.y, ylv.z, ylv.w};
         float oc[4], orr[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
