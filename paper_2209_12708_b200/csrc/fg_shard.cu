@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -43,7 +44,13 @@ struct NcclApi {
 NcclApi& nccl() {
   static NcclApi api = [] {
     NcclApi a;
-    a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // RTLD_LOCAL: when torch has already loaded its bundled NCCL this resolves to that same
+    // library (matched by soname); otherwise the copy found here must not export its symbols
+    // globally, or a later `import torch` binds libtorch_cuda against it (a different NCCL
+    // version: missing symbols at import time).
+    const char* path = std::getenv("FG_NCCL_LIB");  // an explicit libnccl (e.g. the one torch bundles)
+    if (path && path[0]) a.h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!a.h) a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!a.h) return a;
     a.get_unique_id = (int (*)(NcclUid*))dlsym(a.h, "ncclGetUniqueId");
     a.comm_init_rank = (int (*)(NcclComm*, int, NcclUid, int))dlsym(a.h, "ncclCommInitRank");

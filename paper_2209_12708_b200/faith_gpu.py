@@ -452,8 +452,30 @@ def gen_positions(seed: int, length: int, words: int) -> np.ndarray:
     return p
 
 
+def _preload_nccl() -> None:
+    """Make the NCCL the library dlopen()s (by soname) the one torch ships (nvidia-nccl wheel):
+    loading the system libnccl first would leave a different NCCL version resident, and a later
+    `import torch` fails to bind libtorch_cuda against it."""
+    global _nccl_preloaded
+    if _nccl_preloaded:
+        return
+    _nccl_preloaded = True
+    try:
+        import nvidia.nccl as nn
+        base = nn.__file__ and os.path.dirname(nn.__file__) or list(nn.__path__)[0]
+        path = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(path):
+            C.CDLL(path, mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+    except (ImportError, OSError):
+        pass
+
+
+_nccl_preloaded = False
+
+
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id for fg_model_shard_nccl (create on rank 0, share with all ranks)."""
+    _preload_nccl()
     lib = load_library()
     buf = C.create_string_buffer(128)
     if lib.fg_nccl_unique_id(buf) != FG_OK:
@@ -489,6 +511,7 @@ class Model:
     def shard_columns_nccl(self, rank: int, nranks: int, uid: bytes):
         """Column-shard the perturbation dimension over `nranks` GPUs; partial norms all-reduced
         with NCCL.  Every rank must then call the same passes."""
+        _preload_nccl()
         self.ctx._check(self.lib.fg_model_shard_nccl(self.handle, rank, nranks, uid), "fg_model_shard_nccl")
 
     def shard_columns_loopback(self, group: LoopbackGroup, rank: int):
