@@ -5,6 +5,8 @@
 // the correctness baseline for every Λ contraction and the path
 // for the small attention contractions; the affine bound GEMM additionally has
 // a tcgen05 path (fg_umma.cu).
+#include <algorithm>
+
 #include "fg_internal.cuh"
 
 namespace fg {
@@ -155,10 +157,28 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(GemmArgs g) {
 static bool al4(long long v) { return (v & 3) == 0; }
 static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-int launch_gemm(const GemmArgs& g, cudaStream_t st) {
-  if (g.M <= 0 || g.N <= 0) return 0;
+int launch_gemm(const GemmArgs& g0, cudaStream_t st) {
+  if (g0.M <= 0 || g0.N <= 0) return 0;
+  const long long inner = (long long)g0.nb[1] * g0.nb[2] * g0.nb[3];
+  if (g0.nb[0] <= 0 || inner <= 0 || inner > 65535 || g0.K <= 0) return -1;
+  if ((long long)g0.nb[0] * inner > 65535) {  // gridDim.z limit: launch slices of the outermost batch dim
+    const int per = (int)(65535 / inner);
+    int n = 0;
+    for (int b0 = 0; b0 < g0.nb[0]; b0 += per) {
+      GemmArgs g = g0;
+      g.nb[0] = std::min(per, g0.nb[0] - b0);
+      g.A += b0 * g0.sA[0];
+      g.B += b0 * g0.sB[0];
+      g.C += b0 * g0.sC[0];
+      if (g.R) g.R += b0 * g0.sR[0];
+      const int r = launch_gemm(g, st);
+      if (r < 0) return r;
+      n += r;
+    }
+    return n;
+  }
+  const GemmArgs& g = g0;
   long long batches = (long long)g.nb[0] * g.nb[1] * g.nb[2] * g.nb[3];
-  if (batches <= 0 || batches > 65535 || g.K <= 0) return -1;
   bool aligned = al4(g.M) && al4(g.N) && al4(g.lda) && al4(g.ldb) && al4(g.ldc) && al4(g.b_off1) &&
                  al16(g.A) && al16(g.B) && al16(g.C) && (!g.R || (al16(g.R) && al4(g.ldr)));
   for (int i = 0; i < 4; ++i)

@@ -2312,7 +2312,11 @@ int launch_dot_similarity(const NView& q, const NView& k, const NView& out, int 
   g.sA[0] = H * per; g.sA[1] = per; g.sA[2] = 0; g.sA[3] = 2LL * hd * L;
   g.sB[0] = q.s_stride * D; g.sB[1] = (long long)hd * D; g.sB[2] = (long long)q.row_stride * D; g.sB[3] = 0;
   g.sC[0] = out.s_stride * D; g.sC[1] = (long long)L * L * D; g.sC[2] = (long long)L * D; g.sC[3] = out.cr;
-  n += launch_gemm(g, st);
+  {
+    const int r = launch_gemm(g, st);
+    if (r < 0) return r;  // unsupported shape: reported by the caller, never silently skipped
+    n += r;
+  }
   // y-side (K rows scaled by lx of Q): batch (s, h, j, plane), accumulate
   GemmArgs t{};
   t.M = L; t.N = D; t.K = hd; t.K0 = hd;
@@ -2324,7 +2328,11 @@ int launch_dot_similarity(const NView& q, const NView& k, const NView& out, int 
   t.sA[0] = H * per; t.sA[1] = per; t.sA[2] = 0; t.sA[3] = (long long)hd * L;
   t.sB[0] = k.s_stride * D; t.sB[1] = (long long)hd * D; t.sB[2] = (long long)k.row_stride * D; t.sB[3] = k.cr;
   t.sC[0] = out.s_stride * D; t.sC[1] = (long long)L * L * D; t.sC[2] = D; t.sC[3] = out.cr;
-  n += launch_gemm(t, st);
+  {
+    const int r = launch_gemm(t, st);
+    if (r < 0) return r;  // unsupported shape: reported by the caller, never silently skipped
+    n += r;
+  }
   return n;
 }
 
@@ -2347,7 +2355,11 @@ int launch_dot_weighted(const NView& p, const NView& v, const NView& out, int S,
   g.sA[0] = H * per; g.sA[1] = per; g.sA[2] = 0; g.sA[3] = 2LL * L * hd;
   g.sB[0] = p.s_stride * D; g.sB[1] = (long long)L * L * D; g.sB[2] = (long long)L * D; g.sB[3] = 0;
   g.sC[0] = out.s_stride * D; g.sC[1] = (long long)hd * D; g.sC[2] = (long long)out.row_stride * D; g.sC[3] = out.cr;
-  n += launch_gemm(g, st);
+  {
+    const int r = launch_gemm(g, st);
+    if (r < 0) return r;  // unsupported shape: reported by the caller, never silently skipped
+    n += r;
+  }
   // y-side (V rows scaled by lx of P): batch (s, h, plane); N spans (k, d) of the head
   GemmArgs t{};
   t.M = L; t.N = hd * D; t.K = L; t.K0 = L;
@@ -2359,7 +2371,11 @@ int launch_dot_weighted(const NView& p, const NView& v, const NView& out, int S,
   t.sA[0] = H * per; t.sA[1] = per; t.sA[2] = (long long)L * L; t.sA[3] = 0;
   t.sB[0] = v.s_stride * D; t.sB[1] = (long long)hd * D; t.sB[2] = v.cr; t.sB[3] = 0;
   t.sC[0] = out.s_stride * D; t.sC[1] = (long long)hd * D; t.sC[2] = out.cr; t.sC[3] = 0;
-  n += launch_gemm(t, st);
+  {
+    const int r = launch_gemm(t, st);
+    if (r < 0) return r;  // unsupported shape: reported by the caller, never silently skipped
+    n += r;
+  }
   return n;
 }
 

@@ -207,3 +207,20 @@ def test_sampled_soundness(models, port, norm, eps):
         slack = 1e-6 * np.maximum(1.0, np.abs(logits))  # f32 Λ: 1e-6 (reference uses 1e-7 in f64)
         worst = max(worst, float(np.max(lo[0] - logits - slack)), float(np.max(logits - hi[0] - slack)))
     assert worst <= 0.0, worst
+
+
+def test_many_slots_beyond_grid_limits():
+    """c1 (D = 64: FP32 SIMT GEMMs, whose batch index lives in gridDim.z) with 300 resident
+    sentences: the McCormick GEMMs need S*H*L*2 = 76800 > 65535 batches and are launched in
+    slices.  Every sentence's certified epsilon must equal the 60-slot run's."""
+    from paper_2209_12708_b200.configs import CONFIGS as C5
+    w = C5["c1"]
+    cfg = F.ModelConfig(w.layers, w.heads, w.embed, w.ffn, w.length, w.classes, w.activation)
+    m = F.Model(F.Context(0), cfg, F.gen_synthetic(cfg, w.model_seed))
+    n = 300
+    xs = np.stack([F.gen_input(cfg, w.input_seed(s)) for s in range(n)])
+    ps = np.stack([F.gen_positions(w.position_seed(s), w.length, w.words) for s in range(n)])
+    big = m.maxeps(xs, ps, w.norm, w.eps_max, 1e-4, slots=n)
+    small = m.maxeps(xs, ps, w.norm, w.eps_max, 1e-4, slots=60)
+    assert np.array_equal(big["calls"], small["calls"])
+    assert np.array_equal(big["eps"], small["eps"], equal_nan=True)
