@@ -369,6 +369,10 @@ def main():
                 gbs = nbytes * B / (world if columns else 1) / (prof[site][0] / 1e3) / 1e9
                 mem[site] = {"GB/s": gbs, "frac_hbm": gbs / pk["hbm_gbs"], "ms": prof[site][0]}
         line["kernels"] = {k: {"ms_per_pass": v[0], "launches": v[1]} for k, v in sorted(prof.items())}
+        mem["_note"] = ("GB/s = algorithmic bytes (each Λ read once, written once) / site time; a site that "
+                        "reads what the previous kernel just wrote (concretize after the Q/K/V GEMM) partly "
+                        "hits the 126 MB L2, so its rate can exceed the HBM peak; DRAM bytes per launch are in "
+                        "profiles/r1c_ncu_launches_c3.txt")
         line["hbm_sites"] = mem
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
