@@ -2064,6 +2064,75 @@ __global__ void head_kernel(const double* pc, const double* pr, const double* pl
   }
 }
 
+// The same classifier head, one CTA per sentence for all classes at once (C <= kHeadMaxC): each
+// pooled Λ element is loaded once for every class, and a CTA's 512 threads cover D, so the
+// whole head is one short wave instead of S*C single CTAs walking E serially.  Per (s, class, d)
+// the accumulation is the same (e ascending, same operations) as head_kernel.
+constexpr int kHeadMaxC = 8;
+constexpr int kHeadThreads = 512;
+
+template <int Q>
+__global__ void __launch_bounds__(kHeadThreads) head_all_kernel(const double* pc, const double* pr,
+                                                                const double* plb, const double* pub,
+                                                                const double* wc, const double* bc, int E, int C,
+                                                                int D, const double* eps, double* out_lo,
+                                                                double* out_hi, int* status, int site) {
+  __shared__ double red[32];
+  const int s = blockIdx.x;
+  double nu[kHeadMaxC], nl[kHeadMaxC];
+#pragma unroll
+  for (int c = 0; c < kHeadMaxC; ++c) nu[c] = nl[c] = 0.0;
+  int finite = 1;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    double ac[kHeadMaxC], ar[kHeadMaxC];
+#pragma unroll
+    for (int c = 0; c < kHeadMaxC; ++c) ac[c] = ar[c] = 0.0;
+    for (int e = 0; e < E; ++e) {
+      const double vc = pc[((long long)s * E + e) * D + d], vr = pr[((long long)s * E + e) * D + d];
+#pragma unroll
+      for (int c = 0; c < kHeadMaxC; ++c) {
+        if (c >= C) break;
+        const double w = wc[e * C + c];
+        ac[c] += w * vc;
+        ar[c] += fabs(w) * vr;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kHeadMaxC; ++c) {
+      if (c >= C) break;
+      const double u = ac[c] + ar[c], l = ac[c] - ar[c];
+      finite &= (isfinite(u) && isfinite(l));
+      if (Q == NORM_L1) { nu[c] += fabs(u); nl[c] += fabs(l); }
+      else if (Q == NORM_L2) { nu[c] += u * u; nl[c] += l * l; }
+      else { nu[c] = fmax(nu[c], fabs(u)); nl[c] = fmax(nl[c], fabs(l)); }
+    }
+  }
+  finite = __syncthreads_and(finite);
+  for (int c = 0; c < C; ++c) {
+    const double gu = block_reduce<Q>(nu[c], red);
+    const double gl = block_reduce<Q>(nl[c], red);
+    if (threadIdx.x == 0) {
+      double ub_pos = 0.0, ub_neg = 0.0, lb_pos = 0.0, lb_neg = 0.0;  // relax.cpp:280-299
+      for (int i = 0; i < E; ++i) {
+        const double wv = wc[i * C + c];
+        const double wp = (wv < 0.0) ? 0.0 : wv, wn = (0.0 < wv) ? 0.0 : wv;
+        const double xu = pub[(long long)s * E + i], xl = plb[(long long)s * E + i];
+        ub_pos += wp * xu;
+        ub_neg += wn * xl;
+        lb_pos += wp * xl;
+        lb_neg += wn * xu;
+      }
+      const double yub = ub_pos + ub_neg + bc[c];
+      const double ylb = lb_pos + lb_neg + bc[c];
+      if (!finite || !isfinite(yub) || !isfinite(ylb)) set_status(status, s, site, kCodeDomain);
+      NormAcc<Q> fin;
+      const double e = eps[s];
+      out_lo[(long long)s * C + c] = ylb - e * fin.fin(gl);
+      out_hi[(long long)s * C + c] = yub + e * fin.fin(gu);
+    }
+  }
+}
+
 template <int Q>
 __global__ void concretize_f64_kernel(const double* pc, const double* pr, const double* lb,
                                       const double* ub, long long rows_per_s, long long nrows,
@@ -2553,9 +2622,15 @@ int launch_head(const double* pc, const double* pr, const double* plb, const dou
                 const double* eps, double* out_lo, double* out_hi, int* status, int site,
                 double* pooled_lo, double* pooled_hi, cudaStream_t st) {
   int q = dual_norm(norm);
-  DISPATCH_Q(q, head_kernel,
-             <<<S * C, 256, 0, st>>>(pc, pr, plb, pub, wc, bc, E, C, D, eps, out_lo, out_hi,
-                                     status, site));
+  if (C <= kHeadMaxC) {
+    DISPATCH_Q(q, head_all_kernel,
+               <<<S, kHeadThreads, 0, st>>>(pc, pr, plb, pub, wc, bc, E, C, D, eps, out_lo, out_hi, status,
+                                            site));
+  } else {
+    DISPATCH_Q(q, head_kernel,
+               <<<S * C, 256, 0, st>>>(pc, pr, plb, pub, wc, bc, E, C, D, eps, out_lo, out_hi,
+                                       status, site));
+  }
   int n = 1;
   if (pooled_lo) {
     long long nrows = (long long)S * E;
