@@ -1659,6 +1659,257 @@ __global__ void __launch_bounds__(Sm4<NC, KG>::kThreads, NC <= 4 ? 4 : 2) softma
   __syncthreads();  // the producer warp stays resident until every stage has been consumed
 }
 
+// Streaming softmax for any D % 128 == 0 (the wide rows of c5, D = 1536): softmax4_kernel's
+// structure with runtime D -- the warps' Σ partials accumulate in SHARED memory (read-modify-
+// write per key) instead of registers, and nothing per column is held in registers across a
+// key, so the register budget does not grow with D.  ns stages (a multiple of NC).
+template <int Q, int NC>
+__global__ void __launch_bounds__((NC + 1) * 32) softmax5_kernel(NView sc, int rows_per_s, int nrows, int n, int D,
+                                                                 int ns, const double* __restrict__ eps,
+                                                                 int* __restrict__ status, int site_exp,
+                                                                 int site_recip) {
+  extern __shared__ __align__(16) unsigned char sm5[];
+  const int KG = D / 128;
+  float* ring = reinterpret_cast<float*>(sm5);        // [ns][c|r][D]
+  float* part = ring + (size_t)ns * 2 * D;            // [NC][u|l][D]
+  float* ru_f = part + (size_t)NC * 2 * D;            // [D]
+  float* rl_f = ru_f + D;                             // [D]
+  const int n2 = (n + 1) & ~1;
+  float* a_lo_f = rl_f + D;
+  float* a_up_f = a_lo_f + n2;
+  double* e_lb = reinterpret_cast<double*>(a_up_f + n2);
+  double* e_ub = e_lb + n;
+  double* e_lo = e_ub + n;
+  double* red = e_lo + n;   // [32]
+  double* scal = red + 32;  // [32]
+  uint64_t* full = reinterpret_cast<uint64_t*>(scal + 32);
+  uint64_t* empty = full + ns;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int b = 0; b < ns; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(full + b)) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(empty + b)) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NC) {  // ---- producer (stays resident to the end, see softmax4_kernel)
+    if (lane == 0) {
+      long long t = 0;
+      for (int rid = blockIdx.x; rid < nrows; rid += gridDim.x) {
+        const int s = rid / rows_per_s, row = rid % rows_per_s;
+        const long long nb = (long long)s * sc.s_stride + (long long)row * n;
+        const float* cb = sc.lam + nb * D;
+        const float* rb = cb + sc.cr;
+        for (int p = 0; p < 2; ++p)
+          for (int j = 0; j < n; ++j, ++t) {
+            const int st = (int)(t % ns);
+            const uint32_t ph = (uint32_t)((t / ns) & 1);
+            if (t >= ns) sm4_wait(empty + st, ph ^ 1u);
+            float* dst = ring + (size_t)st * 2 * D;
+            const int key = p == 0 ? j : n - 1 - j;
+            mbar_expect(full + st, 8u * D);
+            asm volatile(
+                "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(dst)),
+                "l"(cb + (long long)key * D), "r"(4u * D), "r"(smem_addr(full + st))
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(dst + D)),
+                "l"(rb + (long long)key * D), "r"(4u * D), "r"(smem_addr(full + st))
+                : "memory");
+          }
+      }
+    }
+    __syncwarp();
+  } else {  // ---- consumers
+    NormAcc<Q> fin;
+    float4* pu = reinterpret_cast<float4*>(part + (size_t)warp * 2 * D);
+    float4* pl = pu + D / 4;
+    long long t0 = 0;
+    for (int rid = blockIdx.x; rid < nrows; rid += gridDim.x, t0 += 2LL * n) {
+      const int s = rid / rows_per_s, row = rid % rows_per_s;
+      const long long nb = (long long)s * sc.s_stride + (long long)row * n;
+      float* cbw = sc.lam + nb * D;
+      float* rbw = cbw + sc.cr;
+      const double e = eps[s];
+      for (int k = 0; k < KG; ++k) {
+        pu[lane + 32 * k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        pl[lane + 32 * k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      // pass 1: exp envelopes per key; Σ_j e_j accumulated into the warp's SMEM partial
+      int err_exp = 0;
+      for (int j = warp; j < n; j += NC) {
+        const long long ti = t0 + j;
+        const int st = (int)(ti % ns);
+        const double xlb = sc.lb[nb + j], xub = sc.ub[nb + j];
+        sm4_wait(full + st, (uint32_t)((ti / ns) & 1));
+        const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * D);
+        const float4* r4 = c4 + D / 4;
+        float fu = 0.f, fl = 0.f;
+        for (int k = 0; k < KG; ++k) {
+          const float4 cv = c4[lane + 32 * k], rv = r4[lane + 32 * k];
+          fu = qacc_f<Q>(fu, cv.x + rv.x); fl = qacc_f<Q>(fl, cv.x - rv.x);
+          fu = qacc_f<Q>(fu, cv.y + rv.y); fl = qacc_f<Q>(fl, cv.y - rv.y);
+          fu = qacc_f<Q>(fu, cv.z + rv.z); fl = qacc_f<Q>(fl, cv.z - rv.z);
+          fu = qacc_f<Q>(fu, cv.w + rv.w); fl = qacc_f<Q>(fl, cv.w - rv.w);
+        }
+        const double nu = fin.fin(group_reduce<Q>((double)fu, 32)), nl = fin.fin(group_reduce<Q>((double)fl, 32));
+        Lines ln;
+        const int code = exp_envelope(xlb - e * nl, xub + e * nu, ln);
+        if (code) err_exp = err_exp ? min(err_exp, code) : code;
+        const float au = (float)ln.au, al = (float)ln.al;
+        if (lane == 0) {
+          a_lo_f[j] = al;
+          a_up_f[j] = au;
+          const double ub2 = ln.au * (ln.au >= 0.0 ? xub : xlb) + ln.bu;
+          const double lb2 = ln.al * (ln.al >= 0.0 ? xlb : xub) + ln.bl;
+          e_ub[j] = ub2;
+          e_lb[j] = lb2;
+          e_lo[j] = lb2 - e * fabs(ln.al) * (ln.al >= 0.0 ? nl : nu);
+        }
+        for (int k = 0; k < KG; ++k) {
+          const float4 cv = c4[lane + 32 * k], rv = r4[lane + 32 * k];
+          float4 a = pu[lane + 32 * k], b = pl[lane + 32 * k];
+          const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+          float* ap = &a.x;
+          float* bp = &b.x;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float uu = cc[q] + rr[q], ll = cc[q] - rr[q];
+            ap[q] += au * (au >= 0.f ? uu : ll);
+            bp[q] += al * (al >= 0.f ? ll : uu);
+          }
+          pu[lane + 32 * k] = a;
+          pl[lane + 32 * k] = b;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(empty + st);
+      }
+      if (err_exp && lane == 0) set_status(status, s, site_exp, err_exp);
+      sm4_sync<NC>();
+      // Σ rows: warp partials combined in warp order (f64) -- recomputed below for r
+      double pnu = 0.0, pnl = 0.0;
+      for (int d = tid; d < D; d += NC * 32) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < NC; ++w) {
+          a += (double)part[(size_t)w * 2 * D + d];
+          b += (double)part[(size_t)w * 2 * D + D + d];
+        }
+        pnu = qcombine<Q>(pnu, qpart<Q>(a));
+        pnl = qcombine<Q>(pnl, qpart<Q>(b));
+      }
+      if (warp == 0) {  // propagate_sum_axis bias (relax.cpp:728-731)
+        double a = 0.0, b = 0.0;
+        for (int j = lane; j < n; j += 32) {
+          a += e_lb[j];
+          b += e_ub[j];
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        if (lane == 0) {
+          scal[4] = a;
+          scal[5] = b;
+        }
+      }
+      sm4_reduce2<Q, NC>(pnu, pnl, red);
+      if (tid == 0) {
+        const double slb = scal[4], sub_ = scal[5];
+        Lines ln;
+        const int code = envelope(RELAX_RECIP, slb - e * fin.fin(pnl), sub_ + e * fin.fin(pnu), ln);
+        if (code) set_status(status, s, site_recip, code);
+        scal[0] = ln.al;
+        scal[1] = ln.au;
+        scal[2] = ln.al * (ln.al >= 0.0 ? slb : sub_) + ln.bl;
+        scal[3] = ln.au * (ln.au >= 0.0 ? sub_ : slb) + ln.bu;
+      }
+      sm4_sync<NC>();
+      const double r_al = scal[0], r_au = scal[1], r_lb = scal[2], r_ub = scal[3];
+      pnu = pnl = 0.0;
+      for (int d = tid; d < D; d += NC * 32) {
+        double u = 0.0, l = 0.0;
+        for (int w = 0; w < NC; ++w) {
+          u += (double)part[(size_t)w * 2 * D + d];
+          l += (double)part[(size_t)w * 2 * D + D + d];
+        }
+        const double yu = r_au * (r_au >= 0.0 ? u : l), yl = r_al * (r_al >= 0.0 ? l : u);
+        ru_f[d] = (float)yu;
+        rl_f[d] = (float)yl;
+        pnu = qcombine<Q>(pnu, qpart<Q>(yu));
+        pnl = qcombine<Q>(pnl, qpart<Q>(yl));
+      }
+      sm4_reduce2<Q, NC>(pnu, pnl, red);  // (its barriers also publish ru_f / rl_f)
+      const double r_lo = r_lb - e * fin.fin(pnl);
+      const double r_hi = r_ub + e * fin.fin(pnu);
+
+      // pass 2: MulBroadcast per key (reverse key order), written to HBM
+      const float ly = (float)r_lo, uy = (float)r_hi;
+      const bool ly_p = ly >= 0.f, uy_p = uy >= 0.f;
+      const float4* yu4 = reinterpret_cast<const float4*>(ru_f);
+      const float4* yl4 = reinterpret_cast<const float4*>(rl_f);
+      for (int m = warp; m < n; m += NC) {
+        const int j = n - 1 - m;
+        const long long ti = t0 + n + m;
+        const int st = (int)(ti % ns);
+        const float au = a_up_f[j], al = a_lo_f[j], lx = (float)e_lo[j];
+        const bool au_p = au >= 0.f, al_p = al >= 0.f, lx_p = lx >= 0.f;
+        sm4_wait(full + st, (uint32_t)((ti / ns) & 1));
+        const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * D);
+        const float4* r4 = c4 + D / 4;
+        float4* gc = reinterpret_cast<float4*>(cbw + (long long)j * D);
+        float4* gr = reinterpret_cast<float4*>(rbw + (long long)j * D);
+        float fu = 0.f, fl = 0.f;
+        for (int k = 0; k < KG; ++k) {
+          const float4 cv = c4[lane + 32 * k], rv = r4[lane + 32 * k];
+          const float4 yuv = yu4[lane + 32 * k], ylv = yl4[lane + 32 * k];
+          const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+          const float yuu[4] = {yuv.x, yuv.y, yuv.z, yuv.w}, yll[4] = {ylv.x, ylv.y, ylv.z, ylv.w};
+          float oc[4], orr[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float u = cc[q] + rr[q], l = cc[q] - rr[q];
+            const float eu = au * (au_p ? u : l), el = al * (al_p ? l : u);
+            const float p_l = __fmaf_rn(ly, ly_p ? el : eu, lx * (lx_p ? yll[q] : yuu[q]));
+            const float p_u = __fmaf_rn(uy, uy_p ? eu : el, lx * (lx_p ? yuu[q] : yll[q]));
+            oc[q] = 0.5f * (p_u + p_l);
+            orr[q] = 0.5f * (p_u - p_l);
+            fu = qacc_f<Q>(fu, p_u);
+            fl = qacc_f<Q>(fl, p_l);
+          }
+          gc[lane + 32 * k] = make_float4(oc[0], oc[1], oc[2], oc[3]);
+          gr[lane + 32 * k] = make_float4(orr[0], orr[1], orr[2], orr[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(empty + st);
+        const double gu = group_reduce<Q>((double)fu, 32), gl = group_reduce<Q>((double)fl, 32);
+        if (lane == 0) {
+          double olb = 0.0, oub = 0.0;
+          term_bias(e_lo[j], r_lo, r_hi, e_lb[j], e_ub[j], r_lb, r_ub, olb, oub);
+          const long long o = nb + j;
+          sc.lb[o] = olb;
+          sc.ub[o] = oub;
+          if (sc.lo) {
+            sc.lo[o] = olb - e * fin.fin(gl);
+            sc.hi[o] = oub + e * fin.fin(gu);
+          }
+        }
+      }
+      sm4_sync<NC>();
+    }
+  }
+  __syncthreads();
+}
+
+size_t softmax5_smem(int n, int D, int NC, int ns) {
+  return (size_t)ns * 8 * D + (size_t)NC * 2 * D * 4 + (size_t)2 * D * 4 + (size_t)(n + 1) * (2 * 4 + 3 * 8) +
+         64 * 8 + 2 * (size_t)ns * 8 + 64;
+}
+
 size_t softmax3_smem(int n, int Dc, int CS, int nbuf) {
   return (size_t)nbuf * n * Dc * 8 + (size_t)Dc * 8 + (size_t)Dc * 16 + (size_t)n * 6 * 8 +
          (size_t)2 * CS * 2 * n * 8 + (size_t)8 * CS * 8 + (32 + 8) * 8 + (size_t)8 * kSm3Threads * 8 +
@@ -2456,6 +2707,41 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
   const char* te = getenv("FG_SM3_TILE_KB");
   const int nbuf = (pe && pe[0] == '1') ? 2 : 1;
   const bool legacy = ver && (ver[0] == '1' || ver[0] == '2' || ver[0] == '3');
+  static const bool force5 = getenv("FG_SM5_ALL") != nullptr;  // comparison runs
+  if (!legacy && D % 128 == 0 && (D > 512 || force5)) {  // wide rows (c5): streaming kernel, Σ partials in SMEM
+    constexpr int NC5 = 2;
+    static const int ns_env = getenv("FG_SM5_NS") ? atoi(getenv("FG_SM5_NS")) : 0;
+    // one stage per consumer warp and three CTAs per SM measured best on c5 (40 ms per pass vs 50 ms
+    // with two stages per warp at two CTAs per SM, 148 ms for the cluster kernel)
+    int ns = ns_env >= NC5 && ns_env % NC5 == 0 ? ns_env : NC5;
+    while (ns > NC5 && softmax5_smem(n, D, NC5, ns) > (ns_env ? 220 : 110) * 1024) ns -= NC5;  // ... 2 CTAs/SM
+    const size_t smem = softmax5_smem(n, D, NC5, ns);
+    if (smem <= 227 * 1024) {
+      static size_t attr5[2][3] = {};
+      static int grid5[2][3] = {};
+      const int q = dual_norm(norm);
+      const int nrows = S * rows_per_s;
+      auto launch = [&](auto kern) {
+        if (attr5[NC5 - 1][q] < smem) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          attr5[NC5 - 1][q] = smem;
+          int per_sm = 0, dev = 0, sms = 0;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NC5 + 1) * 32, smem) != cudaSuccess ||
+              per_sm < 1)
+            per_sm = 1;
+          grid5[NC5 - 1][q] = per_sm * sms;
+        }
+        const int grid = nrows < grid5[NC5 - 1][q] ? nrows : grid5[NC5 - 1][q];
+        kern<<<grid, (NC5 + 1) * 32, smem, st>>>(sc, rows_per_s, nrows, n, D, ns, eps, status, site_exp, site_recip);
+      };
+      if (q == NORM_L1) launch(softmax5_kernel<NORM_L1, NC5>);
+      else if (q == NORM_L2) launch(softmax5_kernel<NORM_L2, NC5>);
+      else launch(softmax5_kernel<NORM_LINF, NC5>);
+      return 1;
+    }
+  }
   // streaming kernel (full D per CTA) where a key row is wide enough to amortise its per-key
   // envelope and reductions (measured: D = 512 3.3 vs 7.2 ms per c3 pass; D = 128 2.06 vs 1.98 ms
   // per c2 pass for the cluster kernel, which stays the choice there)
