@@ -256,7 +256,7 @@ def main():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist = D.init(backend="nccl", device_index=local)
-    B = args.batch or {"c1": 256, "c2": 256, "c3": 64, "c4": 16, "c5": 2}[w.name]
+    B = args.batch or {"c1": 256, "c2": 256, "c3": 64, "c4": 16, "c5": 4}[w.name]
 
     cfg = F.ModelConfig(w.layers, w.heads, w.embed, w.ffn, w.length, w.classes, w.activation)
     ctx = F.Context(local)
