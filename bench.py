@@ -362,6 +362,10 @@ def main():
             "algorithmic": f"{affine_flops(w):.4g} useful flop per sentence-pass (4*L*C*O*D per GEMM affine; "
                            f"layer-1 Q/K/V is a one-hot scatter) x {B} sentences per launch set",
             "launches_per_pass": gemm_k, "share_of_pass": gemm_ms / total if total else None,
+            # the precision north_star asks for (error-compensated 3xTF32): kind::tf32 runs at half the
+            # dense bf16 rate and each useful product costs three MMAs, so its ceiling is bf16 / 6
+            "peak_3xtf32": pk["bf16_tflops"] / 6.0,
+            "frac_3xtf32": (ach / (pk["bf16_tflops"] / 6.0)) if ach else None,
         }
         mem = {}
         for site, nbytes in site_bytes(w).items():
