@@ -497,6 +497,10 @@ fg_status fg_graph_create(fg_ctx* ctx, size_t n_nodes, const fg_node* nodes, siz
       return fail(ctx, FG_ECUDA, "fg_graph_create: constant upload failed");
     }
   }
+  if (cudaStreamSynchronize(0) != cudaSuccess) {  // legacy-stream uploads done before the context stream reads
+    delete g;
+    return fail(ctx, FG_ECUDA, "fg_graph_create: constant upload failed");
+  }
   *out = g;
   return FG_OK;
 }

@@ -1372,6 +1372,9 @@ fg_status fg_model_create(fg_ctx* ctx, const fg_config* cfg, const double* param
   CK(m->bc64.alloc(sizeof(double) * C));
   CK(cudaMemcpy(m->wc64.p, wc, sizeof(double) * E * C, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(m->bc64.p, wc + E * C, sizeof(double) * C, cudaMemcpyHostToDevice));
+  // the uploads above ran on the legacy stream, which does not order the context's non-blocking
+  // stream: wait for them before any pass can read the weights
+  CK(cudaStreamSynchronize(0));
   *out = m.release();
   return FG_OK;
 }
@@ -1934,8 +1937,10 @@ fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_
   CK(Y2.alloc(sizeof(float) * 2 * nout));
   CK(Yref.alloc(sizeof(double) * 2 * nout));
   CK(cudaMemcpy(X.p, x.data(), sizeof(float) * x.size(), cudaMemcpyHostToDevice));
-  CK(cudaMemset(Y1.p, 0, sizeof(float) * 2 * nout));
-  CK(cudaMemset(Y2.p, 0, sizeof(float) * 2 * nout));
+  // on the context's (non-blocking) stream: a legacy-stream memset is not ordered before its kernels
+  CK(cudaMemsetAsync(Y1.p, 0, sizeof(float) * 2 * nout, ctx->stream));
+  CK(cudaMemsetAsync(Y2.p, 0, sizeof(float) * 2 * nout, ctx->stream));
+  CK(cudaStreamSynchronize(0));  // the legacy-stream uploads (weights, X) have landed
   TensorMap tm;
   bool have_tm = D % 128 == 0 && lam_map(tm, X.as<float>(), nin, D, C, rows, 1);
   cudaEvent_t e0, e1;
