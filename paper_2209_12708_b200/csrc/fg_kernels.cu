@@ -2749,8 +2749,7 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
   if (!legacy && (D == 256 || D == 512 || (force4 && D == 128))) {
     static const int nc_env = getenv("FG_SM4_NC") ? atoi(getenv("FG_SM4_NC")) : 0;
     const int NCsel = nc_env == 8 ? 8 : 4;  // default: 4 consumer warps, 4 CTAs per SM
-    static const size_t pad = getenv("FG_SM4_PAD") ? (size_t)atoi(getenv("FG_SM4_PAD")) * 1024 : 0;
-    const size_t smem = softmax4_smem(n, D, NCsel) + pad;
+    const size_t smem = softmax4_smem(n, D, NCsel);
     static size_t attr4[3][3][3] = {};
     static int grid4[3][3][3] = {};
     const int q = dual_norm(norm), kg = D == 128 ? 0 : (D == 256 ? 1 : 2), ci = NCsel == 4 ? 0 : 1;
@@ -2766,9 +2765,7 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
           per_sm = 1;
         grid4[ci][q][kg] = per_sm * sms;
       }
-      static const int grid_cap = getenv("FG_SM4_GRID") ? atoi(getenv("FG_SM4_GRID")) : 0;
-      const int gmax = grid_cap > 0 ? grid_cap : grid4[ci][q][kg];
-      const int grid = nrows < gmax ? nrows : gmax;
+      const int grid = nrows < grid4[ci][q][kg] ? nrows : grid4[ci][q][kg];
       kern<<<grid, threads, smem, st>>>(sc, rows_per_s, nrows, n, eps, status, site_exp, site_recip);
     };
 #define SM4(QQ, NCC)                                                                  \
