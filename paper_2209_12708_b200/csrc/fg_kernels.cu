@@ -1910,6 +1910,272 @@ size_t softmax5_smem(int n, int D, int NC, int ns) {
          64 * 8 + 2 * (size_t)ns * 8 + 64;
 }
 
+// Streaming softmax for narrow rows (D = 64 / 128: c1, c2).  A key row is only 0.5-1 KB, so a
+// stage carries G = 512 / D consecutive keys (4 KB, one pair of bulk copies) and a consumer warp
+// works on all G of them at once: LPK = 32 / G lanes per key, 16 columns per lane.  The per-key
+// scalar work (norm reductions over LPK lanes, the exp envelope, the output bounds) then runs on
+// G keys in parallel instead of one after the other; Σ partials of the G lane groups are
+// combined with two shuffles at the end of pass 1.  Otherwise softmax4_kernel.
+template <int Q, int NC, int G>
+__global__ void __launch_bounds__((NC + 1) * 32, 4) softmax6_kernel(NView sc, int rows_per_s, int nrows, int n,
+                                                                    const double* __restrict__ eps,
+                                                                    int* __restrict__ status, int site_exp,
+                                                                    int site_recip) {
+  constexpr int D = 512 / G, LPK = 32 / G, NS = 2 * NC;  // 4 float4 groups per lane
+  extern __shared__ __align__(16) unsigned char sm6[];
+  float* ring = reinterpret_cast<float*>(sm6);  // [NS][c(G rows)|r(G rows)][D]
+  float* part = ring + (size_t)NS * 2 * G * D;  // [NC][u|l][D]
+  float* ru_f = part + (size_t)NC * 2 * D;
+  float* rl_f = ru_f + D;
+  const int n2 = (n + 1) & ~1;
+  float* a_lo_f = rl_f + D;
+  float* a_up_f = a_lo_f + n2;
+  double* e_lb = reinterpret_cast<double*>(a_up_f + n2);
+  double* e_ub = e_lb + n;
+  double* e_lo = e_ub + n;
+  double* red = e_lo + n;
+  double* scal = red + 32;
+  uint64_t* full = reinterpret_cast<uint64_t*>(scal + 32);
+  uint64_t* empty = full + NS;
+  const int ng = n / G;  // key groups per row
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kg = lane / LPK, sub = lane % LPK;  // key within the group, lane within the key
+  if (tid == 0) {
+    for (int b = 0; b < NS; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(full + b)) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(empty + b)) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NC) {  // ---- producer: one stage = G consecutive keys (contiguous rows)
+    if (lane == 0) {
+      long long t = 0;
+      for (int rid = blockIdx.x; rid < nrows; rid += gridDim.x) {
+        const int s = rid / rows_per_s, row = rid % rows_per_s;
+        const long long nb = (long long)s * sc.s_stride + (long long)row * n;
+        const float* cb = sc.lam + nb * D;
+        const float* rb = cb + sc.cr;
+        for (int p = 0; p < 2; ++p)
+          for (int gi = 0; gi < ng; ++gi, ++t) {
+            const int st = (int)(t % NS);
+            const uint32_t ph = (uint32_t)((t / NS) & 1);
+            if (t >= NS) sm4_wait(empty + st, ph ^ 1u);
+            float* dst = ring + (size_t)st * 2 * G * D;
+            const int grp = p == 0 ? gi : ng - 1 - gi;  // pass 2 in reverse (L2 reuse)
+            mbar_expect(full + st, 8u * G * D);
+            asm volatile(
+                "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(dst)),
+                "l"(cb + (long long)grp * G * D), "r"(4u * G * D), "r"(smem_addr(full + st))
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(dst + G * D)),
+                "l"(rb + (long long)grp * G * D), "r"(4u * G * D), "r"(smem_addr(full + st))
+                : "memory");
+          }
+      }
+    }
+    __syncwarp();
+  } else {  // ---- consumers
+    NormAcc<Q> fin;
+    long long t0 = 0;
+    for (int rid = blockIdx.x; rid < nrows; rid += gridDim.x, t0 += 2LL * ng) {
+      const int s = rid / rows_per_s, row = rid % rows_per_s;
+      const long long nb = (long long)s * sc.s_stride + (long long)row * n;
+      float* cbw = sc.lam + nb * D;
+      float* rbw = cbw + sc.cr;
+      const double e = eps[s];
+      float su[16], sl[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) su[k] = sl[k] = 0.f;
+      int err_exp = 0;
+      for (int gi = warp; gi < ng; gi += NC) {
+        const long long ti = t0 + gi;
+        const int st = (int)(ti % NS);
+        const int j = gi * G + kg;
+        const double xlb = sc.lb[nb + j], xub = sc.ub[nb + j];
+        sm4_wait(full + st, (uint32_t)((ti / NS) & 1));
+        const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * G * D + (size_t)kg * D);
+        const float4* r4 = c4 + G * D / 4;
+        float fu = 0.f, fl = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 cv = c4[sub + LPK * k], rv = r4[sub + LPK * k];
+          fu = qacc_f<Q>(fu, cv.x + rv.x); fl = qacc_f<Q>(fl, cv.x - rv.x);
+          fu = qacc_f<Q>(fu, cv.y + rv.y); fl = qacc_f<Q>(fl, cv.y - rv.y);
+          fu = qacc_f<Q>(fu, cv.z + rv.z); fl = qacc_f<Q>(fl, cv.z - rv.z);
+          fu = qacc_f<Q>(fu, cv.w + rv.w); fl = qacc_f<Q>(fl, cv.w - rv.w);
+        }
+        const double nu = fin.fin(group_reduce<Q>((double)fu, LPK)), nl = fin.fin(group_reduce<Q>((double)fl, LPK));
+        Lines ln;
+        const int code = exp_envelope(xlb - e * nl, xub + e * nu, ln);
+        if (code) err_exp = err_exp ? min(err_exp, code) : code;
+        const float au = (float)ln.au, al = (float)ln.al;
+        if (sub == 0) {
+          a_lo_f[j] = al;
+          a_up_f[j] = au;
+          const double ub2 = ln.au * (ln.au >= 0.0 ? xub : xlb) + ln.bu;
+          const double lb2 = ln.al * (ln.al >= 0.0 ? xlb : xub) + ln.bl;
+          e_ub[j] = ub2;
+          e_lb[j] = lb2;
+          e_lo[j] = lb2 - e * fabs(ln.al) * (ln.al >= 0.0 ? nl : nu);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 cv = c4[sub + LPK * k], rv = r4[sub + LPK * k];
+          const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float uu = cc[q] + rr[q], ll = cc[q] - rr[q];
+            su[4 * k + q] += au * (au >= 0.f ? uu : ll);
+            sl[4 * k + q] += al * (al >= 0.f ? ll : uu);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(empty + st);
+      }
+      if (err_exp) set_status(status, s, site_exp, err_exp);
+      // combine the G lane groups (same columns, different keys) in a fixed order
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        for (int o = LPK; o < 32; o <<= 1) {
+          su[k] += __shfl_xor_sync(0xffffffffu, su[k], o);
+          sl[k] += __shfl_xor_sync(0xffffffffu, sl[k], o);
+        }
+      if (kg == 0) {
+        float4* pu = reinterpret_cast<float4*>(part + (size_t)warp * 2 * D);
+        float4* pl = pu + D / 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          pu[sub + LPK * k] = make_float4(su[4 * k], su[4 * k + 1], su[4 * k + 2], su[4 * k + 3]);
+          pl[sub + LPK * k] = make_float4(sl[4 * k], sl[4 * k + 1], sl[4 * k + 2], sl[4 * k + 3]);
+        }
+      }
+      sm4_sync<NC>();
+      double pnu = 0.0, pnl = 0.0;
+      for (int d = tid; d < D; d += NC * 32) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < NC; ++w) {
+          a += (double)part[(size_t)w * 2 * D + d];
+          b += (double)part[(size_t)w * 2 * D + D + d];
+        }
+        pnu = qcombine<Q>(pnu, qpart<Q>(a));
+        pnl = qcombine<Q>(pnl, qpart<Q>(b));
+      }
+      if (warp == 0) {
+        double a = 0.0, b = 0.0;
+        for (int j = lane; j < n; j += 32) {
+          a += e_lb[j];
+          b += e_ub[j];
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        if (lane == 0) {
+          scal[4] = a;
+          scal[5] = b;
+        }
+      }
+      sm4_reduce2<Q, NC>(pnu, pnl, red);
+      if (tid == 0) {
+        const double slb = scal[4], sub_ = scal[5];
+        Lines ln;
+        const int code = envelope(RELAX_RECIP, slb - e * fin.fin(pnl), sub_ + e * fin.fin(pnu), ln);
+        if (code) set_status(status, s, site_recip, code);
+        scal[0] = ln.al;
+        scal[1] = ln.au;
+        scal[2] = ln.al * (ln.al >= 0.0 ? slb : sub_) + ln.bl;
+        scal[3] = ln.au * (ln.au >= 0.0 ? sub_ : slb) + ln.bu;
+      }
+      sm4_sync<NC>();
+      const double r_al = scal[0], r_au = scal[1], r_lb = scal[2], r_ub = scal[3];
+      pnu = pnl = 0.0;
+      for (int d = tid; d < D; d += NC * 32) {
+        double u = 0.0, l = 0.0;
+        for (int w = 0; w < NC; ++w) {
+          u += (double)part[(size_t)w * 2 * D + d];
+          l += (double)part[(size_t)w * 2 * D + D + d];
+        }
+        const double yu = r_au * (r_au >= 0.0 ? u : l), yl = r_al * (r_al >= 0.0 ? l : u);
+        ru_f[d] = (float)yu;
+        rl_f[d] = (float)yl;
+        pnu = qcombine<Q>(pnu, qpart<Q>(yu));
+        pnl = qcombine<Q>(pnl, qpart<Q>(yl));
+      }
+      sm4_reduce2<Q, NC>(pnu, pnl, red);
+      const double r_lo = r_lb - e * fin.fin(pnl);
+      const double r_hi = r_ub + e * fin.fin(pnu);
+
+      const float ly = (float)r_lo, uy = (float)r_hi;
+      const bool ly_p = ly >= 0.f, uy_p = uy >= 0.f;
+      const float4* yu4 = reinterpret_cast<const float4*>(ru_f);
+      const float4* yl4 = reinterpret_cast<const float4*>(rl_f);
+      for (int m = warp; m < ng; m += NC) {
+        const int grp = ng - 1 - m;  // the producer streams pass 2 in reverse group order
+        const int j = grp * G + kg;
+        const long long ti = t0 + ng + m;
+        const int st = (int)(ti % NS);
+        const float au = a_up_f[j], al = a_lo_f[j], lx = (float)e_lo[j];
+        const bool au_p = au >= 0.f, al_p = al >= 0.f, lx_p = lx >= 0.f;
+        sm4_wait(full + st, (uint32_t)((ti / NS) & 1));
+        const float4* c4 = reinterpret_cast<const float4*>(ring + (size_t)st * 2 * G * D + (size_t)kg * D);
+        const float4* r4 = c4 + G * D / 4;
+        float4* gc = reinterpret_cast<float4*>(cbw + (long long)j * D);
+        float4* gr = reinterpret_cast<float4*>(rbw + (long long)j * D);
+        float fu = 0.f, fl = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 cv = c4[sub + LPK * k], rv = r4[sub + LPK * k];
+          const float4 yuv = yu4[sub + LPK * k], ylv = yl4[sub + LPK * k];
+          const float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
+          const float yuu[4] = {yuv.x, yuv.y, yuv.z, yuv.w}, yll[4] = {ylv.x, ylv.y, ylv.z, ylv.w};
+          float oc[4], orr[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float u = cc[q] + rr[q], l = cc[q] - rr[q];
+            const float eu = au * (au_p ? u : l), el = al * (al_p ? l : u);
+            const float p_l = __fmaf_rn(ly, ly_p ? el : eu, lx * (lx_p ? yll[q] : yuu[q]));
+            const float p_u = __fmaf_rn(uy, uy_p ? eu : el, lx * (lx_p ? yuu[q] : yll[q]));
+            oc[q] = 0.5f * (p_u + p_l);
+            orr[q] = 0.5f * (p_u - p_l);
+            fu = qacc_f<Q>(fu, p_u);
+            fl = qacc_f<Q>(fl, p_l);
+          }
+          gc[sub + LPK * k] = make_float4(oc[0], oc[1], oc[2], oc[3]);
+          gr[sub + LPK * k] = make_float4(orr[0], orr[1], orr[2], orr[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(empty + st);
+        const double gu = group_reduce<Q>((double)fu, LPK), gl = group_reduce<Q>((double)fl, LPK);
+        if (sub == 0) {
+          double olb = 0.0, oub = 0.0;
+          term_bias(e_lo[j], r_lo, r_hi, e_lb[j], e_ub[j], r_lb, r_ub, olb, oub);
+          const long long o = nb + j;
+          sc.lb[o] = olb;
+          sc.ub[o] = oub;
+          if (sc.lo) {
+            sc.lo[o] = olb - e * fin.fin(gl);
+            sc.hi[o] = oub + e * fin.fin(gu);
+          }
+        }
+      }
+      sm4_sync<NC>();
+    }
+  }
+  __syncthreads();
+}
+
+size_t softmax6_smem(int n, int D, int NC) {
+  const int G = 512 / D;
+  return (size_t)2 * NC * 8 * G * D + (size_t)NC * 2 * D * 4 + (size_t)2 * D * 4 +
+         (size_t)(n + 1) * (2 * 4 + 3 * 8) + 64 * 8 + 2 * (size_t)2 * NC * 8 + 64;
+}
+
 size_t softmax3_smem(int n, int Dc, int CS, int nbuf) {
   return (size_t)nbuf * n * Dc * 8 + (size_t)Dc * 8 + (size_t)Dc * 16 + (size_t)n * 6 * 8 +
          (size_t)2 * CS * 2 * n * 8 + (size_t)8 * CS * 8 + (32 + 8) * 8 + (size_t)8 * kSm3Threads * 8 +
@@ -2707,6 +2973,38 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
   const char* te = getenv("FG_SM3_TILE_KB");
   const int nbuf = (pe && pe[0] == '1') ? 2 : 1;
   const bool legacy = ver && (ver[0] == '1' || ver[0] == '2' || ver[0] == '3');
+  static const bool no6 = getenv("FG_SM6_OFF") != nullptr;
+  if (!legacy && !no6 && (D == 64 || D == 128) && n % (512 / D) == 0) {  // narrow rows: G keys per warp step
+    constexpr int NC6 = 4;
+    const size_t smem = softmax6_smem(n, D, NC6);
+    static size_t attr6[2][3] = {};
+    static int grid6[2][3] = {};
+    const int q = dual_norm(norm), gi = D == 64 ? 0 : 1;
+    const int nrows = S * rows_per_s;
+    auto launch = [&](auto kern) {
+      if (attr6[gi][q] < smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr6[gi][q] = smem;
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NC6 + 1) * 32, smem) != cudaSuccess ||
+            per_sm < 1)
+          per_sm = 1;
+        grid6[gi][q] = per_sm * sms;
+      }
+      const int grid = nrows < grid6[gi][q] ? nrows : grid6[gi][q];
+      kern<<<grid, (NC6 + 1) * 32, smem, st>>>(sc, rows_per_s, nrows, n, eps, status, site_exp, site_recip);
+    };
+#define SM6(QQ)                                                \
+  if (D == 64) launch(softmax6_kernel<QQ, NC6, 8>);            \
+  else launch(softmax6_kernel<QQ, NC6, 4>);
+    if (q == NORM_L1) { SM6(NORM_L1) }
+    else if (q == NORM_L2) { SM6(NORM_L2) }
+    else { SM6(NORM_LINF) }
+#undef SM6
+    return 1;
+  }
   static const bool force5 = getenv("FG_SM5_ALL") != nullptr;  // comparison runs
   if (!legacy && D % 128 == 0 && (D > 512 || force5)) {  // wide rows (c5): streaming kernel, Σ partials in SMEM
     constexpr int NC5 = 2;
