@@ -705,6 +705,7 @@ struct fg_model {
   std::vector<DevLayer> layers;
   DBuf wc64, bc64;
   Workspace ws;
+  std::unique_ptr<Workspace> ws0;  // ε = 0 probe workspace (narrow, all-zero Λ; fg_maxeps)
   fg_run_stats stats{};
   fgh::ShardState shard;  // column sharding of the perturbation dimension (fg_model_set_column_shard)
   // offsets of the layers in params (gen_synthetic order)
@@ -716,16 +717,19 @@ struct fg_model {
 
 namespace {
 
-fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot) {
+// `zero_d` > 0 plans the ε = 0 probe workspace instead (fg_maxeps): zero_d columns that lie
+// past every perturbation column (col0 = W·E), so Λ0 — and with it every Λ of the pass — is
+// zero and each concretization reduces to its bias, exactly what ε·‖Λ‖ = 0 gives at full width.
+fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot, Workspace* wsp = nullptr, int zero_d = 0) {
   fg_ctx* ctx = m->ctx;
-  Workspace& w = m->ws;
+  Workspace& w = wsp ? *wsp : m->ws;
   const fg_config& c = m->cfg;
   const int Dg = W * c.embed;  // global perturbation columns
   const int nr = m->shard.active() ? m->shard.nranks : 1;
   if (Dg % (4 * nr) != 0) return fail(ctx, FG_EINVAL, "column shard: words*embed must be a multiple of 4*nranks");
-  const int D = Dg / nr;  // columns of this rank
+  const int D = zero_d > 0 ? zero_d : Dg / nr;  // columns of this rank
   if (w.S == S && w.D == D && w.W == W && w.Ntot >= Ntot) return FG_OK;
-  w.col0 = (m->shard.active() ? m->shard.rank : 0) * D;
+  w.col0 = zero_d > 0 ? Dg : (m->shard.active() ? m->shard.rank : 0) * D;
   w.release_host();
   const long long L = c.length, E = c.embed, F = c.ffn, H = c.heads, hd = E / H;
   const long long nX = S * L * E, nQKV = S * L * 3 * E, nF = S * L * F, nSC = S * H * L * L;
@@ -876,9 +880,9 @@ fg_status concretize_site(fg_model* m, const float* lam, long long cr, const dou
 
 // One batched bound pass over the resident slots (graph.cpp:531-673 node order).
 // Reads ws.eps / ws.slot_map; writes ws.logits / ws.status.
-fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump) {
+fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nullptr) {
   fg_ctx* ctx = m->ctx;
-  Workspace& w = m->ws;
+  Workspace& w = wsp ? *wsp : m->ws;
   const fg_config& c = m->cfg;
   const int S = w.S, D = w.D, L = c.length, E = c.embed, F = c.ffn, H = c.heads, hd = E / H;
   const int C = c.classes;
@@ -1163,9 +1167,9 @@ bool use_graphs() {
 
 // Runs one pass over all slots; eps/slot_map must be staged in the pinned host
 // buffers.  Results land in w.h_logits / w.h_status after the call returns.
-fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, float* ms) {
+fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, float* ms, Workspace* wsp = nullptr) {
   fg_ctx* ctx = m->ctx;
-  Workspace& w = m->ws;
+  Workspace& w = wsp ? *wsp : m->ws;
   cudaStream_t st = ctx->stream;
   const int S = w.S, C = m->cfg.classes;
   CK(cudaMemcpyAsync(w.eps.p, w.h_eps, sizeof(double) * S, cudaMemcpyHostToDevice, st));
@@ -1178,7 +1182,7 @@ fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, floa
       cudaGraph_t g;
       uint64_t before = ctx->launches;
       CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      fg_status s = enqueue_pass(m, norm, nullptr);
+      fg_status s = enqueue_pass(m, norm, nullptr, &w);
       cudaError_t ce = cudaStreamEndCapture(st, &g);
       if (s) return s;
       if (ce != cudaSuccess) return fail(ctx, FG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
@@ -1191,7 +1195,7 @@ fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, floa
     CK(cudaGraphLaunch(w.graph, st));
     ctx->launches += w.graph_launches;
   } else {
-    fg_status s = enqueue_pass(m, norm, nullptr);
+    fg_status s = enqueue_pass(m, norm, nullptr, &w);
     if (s) return s;
   }
   if (ev1) CK(cudaEventRecord(ev1, st));
@@ -1323,6 +1327,39 @@ int default_slots(const fg_model* m, int S, int D) {
   int slots = (int)std::min<size_t>({cap, (size_t)S, (size_t)64});
   int maxb = 65535 / (2 * m->cfg.length);  // GEMM batch-grid limit
   return std::max(1, std::min(slots, maxb));
+}
+
+// Narrow workspace for the ε = 0 probes of fg_maxeps (see ensure_workspace's zero_d), with
+// the staged inputs of m->ws copied in; nullptr where it would not pay (D <= 128), when the
+// pass is column-sharded, under FG_NO_ZERO_PROBE=1, or when it does not fit in free HBM.
+Workspace* zero_workspace(fg_model* m, int S, int words) {
+  const char* e = std::getenv("FG_NO_ZERO_PROBE");
+  if ((e && e[0] == '1') || m->shard.active()) return nullptr;
+  const int D = words * m->cfg.embed;
+  const int zd = D > 128 ? 128 : 0;  // D = 128 -> 64 (SIMT GEMMs) measured slower at c2
+  if (!zd) return nullptr;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t per = bytes_per_sentence(m->cfg, zd);
+  const int maxb = 65535 / (2 * m->cfg.length);
+  int slots = (int)std::min<size_t>({(size_t)(0.5 * (double)free_b) / std::max<size_t>(per, 1), (size_t)S,
+                                     (size_t)256, (size_t)maxb});
+  const Workspace& w = m->ws;
+  if (!m->ws0) m->ws0.reset(new Workspace());
+  Workspace* z = m->ws0.get();
+  if (slots < 1 || ensure_workspace(m, slots, words, S, z, zd) != FG_OK) {
+    cudaGetLastError();
+    m->ctx->err.clear();
+    m->ws0.reset();
+    return nullptr;
+  }
+  cudaStream_t st = m->ctx->stream;
+  if (cudaMemcpyAsync(z->x_all.p, w.x_all.p, sizeof(double) * (size_t)S * m->cfg.length * m->cfg.embed,
+                      cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(z->pos_all.p, w.pos_all.p, sizeof(int) * (size_t)S * words, cudaMemcpyDeviceToDevice,
+                      st) != cudaSuccess)
+    return nullptr;
+  return z;
 }
 
 }  // namespace
@@ -1557,8 +1594,63 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
   int next = 0, done = 0, passes = 0;
   double pass_ms_sum = 0.0, sentence_passes = 0.0;
   for (int s = 0; s < S; ++s) status_out[s] = FG_OK;
-  while (done < S) {
+  // The first probe of every sentence, verified_at(0) (cli.cpp:159), runs up front on the
+  // narrow all-zero-Λ workspace: at ε = 0 every concretization is bias ± 0·‖Λ‖, so the
+  // verdicts, status codes and logits are those of the full-width pass at a fraction of its
+  // GEMM work.  Each sentence keeps its probe sequence; only the ε = 0 probes move earlier.
+  auto zero_phase = [&](int s, fg_status ps, int ok) {
+    Sent& t = sent[s];
+    ++t.calls;
+    if (ps != FG_OK || !ok) {
+      status_out[s] = ps != FG_OK ? ps : FG_ERUNTIME;  // misclassified input (cli.cpp:159-161)
+      t.phase = P_DONE;
+      eps_out[s] = std::numeric_limits<double>::quiet_NaN();
+      calls_out[s] = t.calls;
+      ++done;
+    } else {
+      t.phase = P_MAX;
+      t.eps = eps_max;
+    }
+  };
+  // The verdicts are decoded after the first full-width pass has run, so the host forward
+  // behind the predicted classes (predict_all) stays overlapped with GPU work; sentences enter
+  // that pass at ε_max tentatively, and one that fails at ε = 0 has its ε_max result dropped.
+  std::vector<int> zst;
+  std::vector<double> zlog;
+  if (Workspace* z = zero_workspace(m, S, words)) {
+    zst.resize(S);
+    zlog.resize((size_t)S * 2 * C);
+    for (int s0 = 0; s0 < S && !st; s0 += z->S) {
+      for (int i = 0; i < z->S; ++i) {
+        z->h_slot[i] = s0 + i < S ? s0 + i : 0;
+        z->h_eps[i] = 0.0;
+      }
+      if ((st = run_pass(m, norm, nullptr, nullptr, nullptr, z))) break;
+      for (int i = 0; i < z->S && s0 + i < S; ++i) {
+        zst[s0 + i] = z->h_status[i];
+        for (int k = 0; k < C; ++k) {
+          zlog[(size_t)(s0 + i) * 2 * C + k] = z->h_logits[(size_t)i * C + k];
+          zlog[(size_t)(s0 + i) * 2 * C + C + k] = z->h_logits[(size_t)z->S * C + (size_t)i * C + k];
+        }
+      }
+    }
+    for (int s = 0; s < S; ++s) {
+      sent[s].phase = P_MAX;
+      sent[s].eps = eps_max;
+    }
+  }
+  auto decode_zero = [&]() {
+    for (int s = 0; s < S; ++s) {
+      fg_status ps = decode_status(zst[s]);
+      int ok = 0;
+      if (ps == FG_OK)
+        fg_check_robust((size_t)C, &zlog[(size_t)s * 2 * C], &zlog[(size_t)s * 2 * C + C], (size_t)pred[s], 0.0, &ok);
+      zero_phase(s, ps, ok);
+    }
+  };
+  while (done < S && !st) {
     for (int i = 0; i < slots; ++i) {
+      while (slot[i] < 0 && next < S && sent[next].phase == P_DONE) ++next;
       if (slot[i] < 0 && next < S) slot[i] = next++;
       int s = slot[i];
       w.h_slot[i] = s >= 0 ? s : 0;
@@ -1571,31 +1663,30 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
     if (!have_pred) {
       pred = fut.get();
       have_pred = true;
+      if (!zst.empty()) decode_zero();
     }
     for (int i = 0; i < slots; ++i) {
       int s = slot[i];
       if (s < 0) continue;
-      sentence_passes += 1.0;
       Sent& t = sent[s];
-      ++t.calls;
+      if (t.phase == P_DONE) {  // failed at ε = 0 (decode_zero): this ε_max probe never happened
+        slot[i] = -1;
+        continue;
+      }
+      sentence_passes += 1.0;
       fg_status ps = decode_status(w.h_status[i]);
       int ok = 0;
       if (ps == FG_OK)
         fg_check_robust((size_t)C, w.h_logits + (size_t)i * C, w.h_logits + (size_t)slots * C + (size_t)i * C,
                         (size_t)pred[s], 0.0, &ok);
-      bool finished = false;
       if (t.phase == P_ZERO) {  // verified_at(0, tolerate=false)
-        if (ps != FG_OK) {
-          status_out[s] = ps;
-          finished = true;
-        } else if (!ok) {
-          status_out[s] = FG_ERUNTIME;  // misclassified input (cli.cpp:159-161)
-          finished = true;
-        } else {
-          t.phase = P_MAX;
-          t.eps = eps_max;
-        }
-      } else if (t.phase == P_MAX) {
+        zero_phase(s, ps, ok);
+        if (t.phase == P_DONE) slot[i] = -1;
+        continue;
+      }
+      ++t.calls;
+      bool finished = false;
+      if (t.phase == P_MAX) {
         if (ok) {
           t.lo = eps_max;
           finished = true;

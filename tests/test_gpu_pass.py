@@ -224,3 +224,21 @@ def test_many_slots_beyond_grid_limits():
     small = m.maxeps(xs, ps, w.norm, w.eps_max, 1e-4, slots=60)
     assert np.array_equal(big["calls"], small["calls"])
     assert np.array_equal(big["eps"], small["eps"], equal_nan=True)
+
+
+@pytest.mark.parametrize("name,n,slots", [("c3", 10, 4), ("c3", 6, 6)])
+def test_zero_probe_workspace_matches_full_width(models, port, monkeypatch, name, n, slots):
+    """The ε = 0 probes run up front on the narrow all-zero-Λ workspace (128 columns, tcgen05):
+    every sentence's status, predicted class, certified ε and probe count equal those of the
+    full-width pass (FG_NO_ZERO_PROBE=1), with more sentences than slots (continuous batching
+    picks the sentences up at ε_max) and with one slot per sentence."""
+    w, cfg, params, m = models(name)
+    xs, ps = zip(*[sentence(port, w, s)[1:] for s in range(n)])
+    xs, ps = np.stack(xs), np.stack(ps)
+    monkeypatch.setenv("FG_NO_ZERO_PROBE", "1")
+    full = m.maxeps(xs, ps, w.norm, w.eps_max, 1e-4, slots=slots)
+    monkeypatch.delenv("FG_NO_ZERO_PROBE")
+    fast = m.maxeps(xs, ps, w.norm, w.eps_max, 1e-4, slots=slots)
+    for k in ("status", "predicted", "calls"):
+        assert np.array_equal(full[k], fast[k]), k
+    assert np.array_equal(full["eps"], fast["eps"], equal_nan=True)
