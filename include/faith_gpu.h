@@ -214,7 +214,10 @@ fg_status fg_certify(fg_model* model, int S, const double* x, const int* positio
  * (verified_at(0) must hold, then eps_max, then midpoints while hi-lo > tol), all sentences
  * advancing together on the GPU (continuous batching over `slots` resident sentences;
  * slots <= 0 picks a default from free HBM).  status[s] = FG_ERUNTIME for a
- * misclassified input (cli.cpp:159-161). */
+ * misclassified input (cli.cpp:159-161).  When words*E > 128 and the model is not column
+ * sharded, the eps = 0 probes of all S sentences run first on a second, 128-column workspace
+ * whose Λ is identically zero (the verdict at eps = 0 does not depend on Λ); it stays
+ * allocated with the model.  FG_NO_ZERO_PROBE=1 keeps them on the full-width workspace. */
 fg_status fg_maxeps(fg_model* model, int S, const double* x, const int* positions, int words,
                     int norm, double eps_max, double tol, int slots, double* eps_out,
                     int* calls_out, int* predicted_out, int* status);
