@@ -242,3 +242,25 @@ def test_zero_probe_workspace_matches_full_width(models, port, monkeypatch, name
     for k in ("status", "predicted", "calls"):
         assert np.array_equal(full[k], fast[k]), k
     assert np.array_equal(full["eps"], fast["eps"], equal_nan=True)
+
+
+def test_zero_probe_failures_drop_their_eps_max_probe(models, port, monkeypatch):
+    """Sentences whose ε = 0 probe fails (inputs scaled up until the exp envelope raises a
+    domain error) finish after one call with the same status as on the full-width path, and
+    their tentative ε_max slot in the first full-width pass is dropped without disturbing the
+    other sentences."""
+    w, cfg, params, m = models("c3")
+    n = 6
+    xs, ps = zip(*[sentence(port, w, s)[1:] for s in range(n)])
+    xs, ps = np.stack(xs).copy(), np.stack(ps)
+    bad = [1, 4]
+    xs[bad] *= 1e4
+    monkeypatch.setenv("FG_NO_ZERO_PROBE", "1")
+    full = m.maxeps(xs, ps, w.norm, w.eps_max, 1e-4, slots=4)
+    monkeypatch.delenv("FG_NO_ZERO_PROBE")
+    fast = m.maxeps(xs, ps, w.norm, w.eps_max, 1e-4, slots=4)
+    assert all(full["status"][b] != 0 for b in bad), full["status"]
+    assert all(full["calls"][b] == 1 for b in bad)
+    for k in ("status", "predicted", "calls"):
+        assert np.array_equal(full[k], fast[k]), k
+    assert np.array_equal(full["eps"], fast["eps"], equal_nan=True)
