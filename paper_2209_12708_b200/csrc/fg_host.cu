@@ -844,6 +844,11 @@ struct Dumper {
   }
 };
 
+bool no_qk_skip() {  // comparison runs: write the layer-1 Q/K zero rows as well
+  static const bool v = std::getenv("FG_ONEHOT_DENSE_QK") != nullptr;
+  return v;
+}
+
 bool onehot_first_layer() {
   const char* e = std::getenv("FG_NO_ONEHOT");
   return !(e && e[0] == '1');
@@ -922,8 +927,10 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     // Q, K, V = propagate_affine(cur, Wq|Wk|Wv)   (one N=3E affine)
     g_tag = "affine_gemm";
     if (l == 0 && onehot) {
+      // Q/K rows at unperturbed tokens are never read in layer 1 on the gathered tcgen05 path
+      const bool gathered = !sharded && w.dots_ok && umma_dots_enabled() && !no_qk_skip();
       LAUNCH(launch_onehot_affine(QKV, w.crQKV, lw.qkv.w32.as<float>(), w.pos_all.as<int>(), w.slot_map.as<int>(), S,
-                                  L, E, 3 * E, w.W, D, w.col0, st));
+                                  L, E, 3 * E, w.W, D, w.col0, st, gathered ? 2 * E : 0));
     } else {
       LAUNCH(launch_affine_lambda(lw.qkv, w.tm_ok ? &w.tm_X : nullptr, X, w.crX, QKV, w.crQKV, nullptr, 0,
                                   (long long)S * L, D, st));

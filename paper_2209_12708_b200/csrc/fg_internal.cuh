@@ -118,7 +118,7 @@ int launch_init_input(float* lam, long long cr, double* lb, double* ub, const do
 // (exact, no GEMM), and the Λ0 residual of the first attention block as a +1 scatter.
 // launch_init_input with lam == nullptr binds lb/ub only.
 int launch_onehot_affine(float* lam, long long cr, const float* w, const int* positions, const int* slot_map, int S,
-                         int L, int E, int O, int W, int D, int col0, cudaStream_t st);
+                         int L, int E, int O, int W, int D, int col0, cudaStream_t st, int skip_o = 0);
 int launch_add_onehot(float* lam, const int* positions, const int* slot_map, int S, int L, int E, int W, int D,
                       int col0, cudaStream_t st);
 // MeanPool (graph.cpp:628-634) -> pooled f64 planes [S, E, D] (+ lb/ub [S, E]).

@@ -2463,8 +2463,12 @@ __global__ void init_input_kernel(float* lam, long long cr, double* lb, double* 
 //   out_c[s, t, o, d] = W[e][o] if t == pos[w] and d == w*E + e (global column), else 0;
 //   out_r = |W| . 0 = 0.
 // Exact (no TF32 splitting of a product with 1).  Row (s, t, o) per warp, float4 stores.
+// Rows of neurons o < skip_o at unperturbed tokens are not written (skip_o = 2E when every
+// layer-1 reader of Q/K Λ gathers the perturbed tokens only: concretize_tokens and the gathered
+// McCormick GEMMs); V rows (and everything at skip_o = 0) are written, zeros included.
 __global__ void onehot_affine_kernel(float* lam, long long cr, const float* __restrict__ w, const int* positions,
-                                     const int* slot_map, int S, int L, int E, int O, int W, int D, int col0) {
+                                     const int* slot_map, int S, int L, int E, int O, int W, int D, int col0,
+                                     int skip_o) {
   long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
   int lane = threadIdx.x & (kWarp - 1);
   long long nrows = (long long)S * L * O;
@@ -2476,6 +2480,7 @@ __global__ void onehot_affine_kernel(float* lam, long long cr, const float* __re
   int word = -1;
   for (int q = 0; q < W; ++q)
     if (positions[src * W + q] == tok) word = q;
+  if (word < 0 && o < skip_o) return;
   float* c = lam + row * D;
   float* r = c + cr;
   for (int d = lane * 4; d < D; d += 4 * kWarp) {
@@ -3176,10 +3181,10 @@ int launch_init_input(float* lam, long long cr, double* lb, double* ub, const do
 }
 
 int launch_onehot_affine(float* lam, long long cr, const float* w, const int* positions, const int* slot_map, int S,
-                         int L, int E, int O, int W, int D, int col0, cudaStream_t st) {
+                         int L, int E, int O, int W, int D, int col0, cudaStream_t st, int skip_o) {
   const long long nrows = (long long)S * L * O;
   onehot_affine_kernel<<<blocks_for(nrows, 8), 256, 0, st>>>(lam, cr, w, positions, slot_map, S, L, E, O, W, D,
-                                                             col0);
+                                                             col0, skip_o);
   return 1;
 }
 
