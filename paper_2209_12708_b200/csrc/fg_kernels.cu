@@ -408,6 +408,107 @@ __global__ void __launch_bounds__(256) elementwise_verify_kernel(
   }
 }
 
+// Narrow rows (D <= 256: one or two float4 per lane and plane): two rows per warp, their loads
+// issued together so each warp keeps twice the bytes in flight through the reductions and the
+// f64 envelope.  Per row the arithmetic (lane partial order, butterfly, envelope) is that of
+// concretize_kernel / elementwise_verify_kernel, so results are bit-identical.
+template <int Q>
+__global__ void __launch_bounds__(256) concretize_rows2_kernel(const float* __restrict__ lam, long long cr,
+                                                               const double* __restrict__ lb,
+                                                               const double* __restrict__ ub, long long rows_per_s,
+                                                               long long nrows, int D, const double* __restrict__ eps,
+                                                               double* __restrict__ lo, double* __restrict__ hi) {
+  const long long row0 = 2 * ((long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp);
+  const int lane = threadIdx.x & (kWarp - 1);
+  if (row0 >= nrows) return;
+  const bool two = row0 + 1 < nrows;
+  NormAcc<Q> acc[2];
+  for (int d = lane * 4; d < D; d += 4 * kWarp) {
+    const float* c0 = lam + row0 * D + d;
+    const float4 c0v = *reinterpret_cast<const float4*>(c0), r0v = *reinterpret_cast<const float4*>(c0 + cr);
+    float4 c1v = make_float4(0.f, 0.f, 0.f, 0.f), r1v = c1v;
+    if (two) {
+      c1v = *reinterpret_cast<const float4*>(c0 + D);
+      r1v = *reinterpret_cast<const float4*>(c0 + D + cr);
+    }
+    acc[0].add4(c0v, r0v);
+    acc[1].add4(c1v, r1v);
+  }
+  acc[0].warp_reduce();
+  acc[1].warp_reduce();
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const long long row = row0 + q;
+      if (row >= nrows) break;
+      const double e = eps[row / rows_per_s];
+      lo[row] = lb[row] - e * acc[q].fin(acc[q].l);
+      hi[row] = ub[row] + e * acc[q].fin(acc[q].u);
+    }
+  }
+}
+
+template <int Q>
+__global__ void __launch_bounds__(256) elementwise_verify_rows2_kernel(
+    int kind, float* __restrict__ lam, long long cr, double* __restrict__ lb, double* __restrict__ ub,
+    long long rows_per_s, long long nrows, int D, const double* __restrict__ eps, int* __restrict__ status, int site,
+    double* __restrict__ lo_out, double* __restrict__ hi_out) {
+  const long long row0 = 2 * ((long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp);
+  const int lane = threadIdx.x & (kWarp - 1);
+  if (row0 >= nrows) return;
+  const int nr = row0 + 1 < nrows ? 2 : 1;
+  NormAcc<Q> acc[2];
+  for (int d = lane * 4; d < D; d += 4 * kWarp) {
+    const float* c0 = lam + row0 * D + d;
+    const float4 c0v = *reinterpret_cast<const float4*>(c0), r0v = *reinterpret_cast<const float4*>(c0 + cr);
+    float4 c1v = make_float4(0.f, 0.f, 0.f, 0.f), r1v = c1v;
+    if (nr == 2) {
+      c1v = *reinterpret_cast<const float4*>(c0 + D);
+      r1v = *reinterpret_cast<const float4*>(c0 + D + cr);
+    }
+    acc[0].add4(c0v, r0v);
+    acc[1].add4(c1v, r1v);
+  }
+  acc[0].warp_reduce();
+  acc[1].warp_reduce();
+  Lines ln[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    if (q >= nr) break;
+    const long long row = row0 + q;
+    const long long s = row / rows_per_s;
+    const double xlb = lb[row], xub = ub[row];
+    const double e = eps[s];
+    const double lo = xlb - e * acc[q].fin(acc[q].l);
+    const double hi = xub + e * acc[q].fin(acc[q].u);
+    const int code = envelope(kind, lo, hi, ln[q], lane, kind == RELAX_SILU ? kWarp : 1);
+    if (lane == 0) {
+      if (code) set_status(status, (int)s, site, code);
+      if (lo_out) {
+        lo_out[row] = lo;
+        hi_out[row] = hi;
+      }
+      ub[row] = ln[q].au * (ln[q].au >= 0.0 ? xub : xlb) + ln[q].bu;
+      lb[row] = ln[q].al * (ln[q].al >= 0.0 ? xlb : xub) + ln[q].bl;
+    }
+  }
+  for (int d = lane * 4; d < D; d += 4 * kWarp) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (q >= nr) break;
+      float* c = lam + (row0 + q) * D + d;
+      const float4 cv = *reinterpret_cast<const float4*>(c), rv = *reinterpret_cast<const float4*>(c + cr);
+      float4 oc, orr;
+      compose_cr(ln[q], cv.x, rv.x, oc.x, orr.x);
+      compose_cr(ln[q], cv.y, rv.y, oc.y, orr.y);
+      compose_cr(ln[q], cv.z, rv.z, oc.z, orr.z);
+      compose_cr(ln[q], cv.w, rv.w, oc.w, orr.w);
+      *reinterpret_cast<float4*>(c) = oc;
+      *reinterpret_cast<float4*>(c + cr) = orr;
+    }
+  }
+}
+
 __global__ void relax_kernel(int kind, const double* lo, const double* hi, long long n,
                              double* al, double* bl, double* au, double* bu, int* status) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2813,6 +2914,11 @@ inline unsigned blocks_for(long long n, int per_block) {
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
+bool rows2_enabled() {  // comparison runs: FG_NO_ROWS2=1 keeps one row per warp for narrow rows
+  static const bool v = getenv("FG_NO_ROWS2") == nullptr;
+  return v;
+}
+
 #define DISPATCH_Q(q, KERNEL, ...)                        \
   switch (q) {                                            \
     case NORM_L1: KERNEL<NORM_L1> __VA_ARGS__; break;     \
@@ -2824,6 +2930,11 @@ int launch_concretize(const float* lam, long long cr, const double* lb, const do
                       long long rows_per_s, long long nrows, int D, int norm, const double* eps,
                       double* lo, double* hi, cudaStream_t st) {
   if (nrows <= 0) return 0;
+  if (rows2_enabled() && D % 4 == 0 && D <= 256) {
+    DISPATCH_Q(dual_norm(norm), concretize_rows2_kernel,
+               <<<blocks_for((nrows + 1) / 2, 8), 256, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi));
+    return 1;
+  }
   dim3 grid(blocks_for(nrows, 8)), block(256);
   DISPATCH_Q(dual_norm(norm), concretize_kernel,
              <<<grid, block, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi));
@@ -2846,6 +2957,12 @@ int launch_elementwise_verify(int kind, float* lam, long long cr, double* lb, do
                               const double* eps, int* status, int site, double* lo_out,
                               double* hi_out, cudaStream_t st, const double* lo_in, const double* hi_in) {
   if (nrows <= 0) return 0;
+  if (rows2_enabled() && !lo_in && D % 4 == 0 && D <= 256) {
+    DISPATCH_Q(dual_norm(norm), elementwise_verify_rows2_kernel,
+               <<<blocks_for((nrows + 1) / 2, 8), 256, 0, st>>>(kind, lam, cr, lb, ub, rows_per_s, nrows, D, eps,
+                                                                 status, site, lo_out, hi_out));
+    return 1;
+  }
   dim3 grid(blocks_for(nrows, 8)), block(256);
   DISPATCH_Q(dual_norm(norm), elementwise_verify_kernel,
              <<<grid, block, 0, st>>>(kind, lam, cr, lb, ub, rows_per_s, nrows, D, eps, status,
