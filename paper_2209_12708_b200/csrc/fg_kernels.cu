@@ -353,6 +353,52 @@ __global__ void __launch_bounds__(256) concretize_tokens_kernel(
   }
 }
 
+// The same in two launches: unperturbed rows copied one thread per row, perturbed rows (W per
+// sentence and feature) reduced one warp per row -- instead of a warp per row for all of them,
+// most of which only copy two doubles.
+__global__ void __launch_bounds__(256) concretize_cold_kernel(const double* __restrict__ lb,
+                                                              const double* __restrict__ ub, long long rows_per_s,
+                                                              long long nrows, double* __restrict__ lo,
+                                                              double* __restrict__ hi, const int* __restrict__ positions,
+                                                              const int* __restrict__ slot_map, int W, int width) {
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nrows) return;
+  const long long s = row / rows_per_s;
+  const int tok = (int)((row % rows_per_s) / width);
+  const int src = slot_map[s];
+  bool hot = false;
+  for (int q = 0; q < W; ++q) hot |= positions[src * W + q] == tok;
+  if (!hot) {
+    lo[row] = lb[row];
+    hi[row] = ub[row];
+  }
+}
+
+template <int Q>
+__global__ void __launch_bounds__(256) concretize_hot_kernel(
+    const float* __restrict__ lam, long long cr, const double* __restrict__ lb, const double* __restrict__ ub,
+    long long rows_per_s, int S, int D, const double* __restrict__ eps, double* __restrict__ lo,
+    double* __restrict__ hi, const int* __restrict__ positions, const int* __restrict__ slot_map, int W, int width) {
+  const long long hid = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;  // (s, q, f)
+  const int lane = threadIdx.x & (kWarp - 1);
+  if (hid >= (long long)S * W * width) return;
+  const int f = (int)(hid % width), q = (int)((hid / width) % W);
+  const long long s = hid / ((long long)W * width);
+  const int tok = positions[slot_map[s] * W + q];
+  const long long row = s * rows_per_s + (long long)tok * width + f;
+  const float* c = lam + row * D;
+  const float* r = c + cr;
+  NormAcc<Q> acc;
+  for (int d = lane * 4; d < D; d += 4 * kWarp)
+    acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
+  acc.warp_reduce();
+  if (lane == 0) {
+    const double e = eps[s];
+    lo[row] = lb[row] - e * acc.fin(acc.l);
+    hi[row] = ub[row] + e * acc.fin(acc.u);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // elementwise_verify (graph.cpp:484-501) fused: concretize -> envelope -> compose,
 // in place, one warp per neuron row.  Λ is read from HBM once (the second sweep
@@ -2981,6 +3027,15 @@ int launch_concretize_tokens(const float* lam, long long cr, const double* lb, c
                              double* lo, double* hi, const int* positions, const int* slot_map, int W, int width,
                              cudaStream_t st) {
   if (nrows <= 0) return 0;
+  if (D % 4 == 0 && getenv("FG_TOKENS_ONEPASS") == nullptr) {  // env: comparison runs
+    concretize_cold_kernel<<<blocks_for(nrows, 256), 256, 0, st>>>(lb, ub, rows_per_s, nrows, lo, hi, positions,
+                                                                   slot_map, W, width);
+    const int S = (int)(nrows / rows_per_s);
+    DISPATCH_Q(dual_norm(norm), concretize_hot_kernel,
+               <<<blocks_for((long long)S * W * width, 8), 256, 0, st>>>(lam, cr, lb, ub, rows_per_s, S, D, eps, lo,
+                                                                          hi, positions, slot_map, W, width));
+    return 2;
+  }
   DISPATCH_Q(dual_norm(norm), concretize_tokens_kernel,
              <<<blocks_for(nrows, 8), 256, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi, positions,
                                                      slot_map, W, width));
