@@ -179,6 +179,15 @@ def pass_over_sample(w, kind):
     return (cal.get(kind) or cal.get("reference") or cal.get("port") or {}).get("pass_over_sample")
 
 
+def scale_phrase(w, kind):
+    """How the sample extrapolates to a full pass, or why it does not (no calibration row)."""
+    ratio = pass_over_sample(w, kind)
+    if not ratio:
+        return (f"no single-thread full-pass calibration for {w.name} in profiles/cpu_calibration.json, "
+                "so value is null")
+    return f"full pass = sample x {ratio} (single-thread calibration, profiles/cpu_calibration.json)"
+
+
 def cpu_rate(w, wall_s, n_threads, passes_per_sentence, kind):
     """sentences/s of the reference CPU path extrapolated from the sample."""
     ratio = pass_over_sample(w, kind)
@@ -207,8 +216,8 @@ def reference_arm(args, w):
     wall = sum(walls) / len(walls)
     value, t_pass = cpu_rate(w, wall, n_threads, passes, kind)
     sample = (f"first {SAMPLE_NODES} nodes (layer-1 Q,K,V propagate_affine) of the {w.name} word-level bound pass, "
-              f"{n_threads} sentences concurrently (one per host thread); full pass = sample x "
-              f"{pass_over_sample(w, kind)} (single-thread calibration, profiles/cpu_calibration.json), "
+              f"{n_threads} sentences concurrently (one per host thread); "
+              f"{scale_phrase(w, kind)}, "
               f"{passes} passes per sentence")
     line = {"impl": "reference", "metric": "certified sentences/sec (eps binary search)", "value": value,
             "unit": "sentences/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -391,8 +400,8 @@ def main():
         line["cpu_baseline"] = {
             "value": rate, "unit": "sentences/s", "cores": n_threads, "kind": kind,
             "sample": f"first {SAMPLE_NODES} nodes of the {w.name} bound pass for {n_threads} sentences "
-                      f"concurrently ({wall_cpu:.1f} s wall); pass = sample x "
-                      f"{pass_over_sample(w, kind)}; "
+                      f"concurrently ({wall_cpu:.1f} s wall); "
+                      f"{scale_phrase(w, kind)}; "
                       f"{statistics.mean(calls):.1f} passes/sentence",
         }
     if rank == 0:
