@@ -203,6 +203,26 @@ fg_status fg_bound_pass_dump(fg_model* model, const double* x, const int* positi
                              int norm, double eps, double* logits_lo, double* logits_hi,
                              double* node_lo, double* node_hi, int* status);
 
+/* The same pass in the exact precision mode (FG_PRECISION_F64 arithmetic: f64 Λ in the
+ * reference layout, every operator in the reference's operation order, no FMA contraction) for
+ * ONE sentence, entirely on the device.  Bit-identical to graph::evaluate + concretize for the
+ * arithmetic operators; the exp/tanh/SiLU envelopes agree to an ulp or two of the device libm.
+ * node_lo/node_hi (fg_node_dump_size() each) may be NULL; when given, every node's concretized
+ * bounds are written in fo_bound_pass order (no NaN entries).  status as fg_bound_pass. */
+fg_status fg_bound_pass_exact(fg_model* model, const double* x, const int* positions, int words,
+                              int norm, double eps, double* logits_lo, double* logits_hi,
+                              double* node_lo, double* node_hi, int* status);
+
+/* Decision-exact verdicts.  fg_certify, fg_maxeps and fg_maxeps_spec decide every probe with
+ * check_robust on the fused f32-Λ pass; a probe is AMBIGUOUS when for some class j != t
+ *   |lo_t - hi_j - margin| <= kappa * ((hi_t - lo_t) + (hi_j - lo_j)) + 1e-11 * max(1, |lo_t|, |hi_j|)
+ * i.e. its margin lies within the f32-Λ error estimate (a fraction kappa of the Λ-derived bound
+ * widths) of zero.  Ambiguous probes are re-decided by fg_bound_pass_exact, so every verdict is
+ * the reference's.  kappa = 0 turns the re-decision off (raw f32 verdicts).  The default is
+ * FG_DEFAULT_KAPPA (measured f32-vs-exact margin error x 50). */
+#define FG_DEFAULT_KAPPA 1e-5
+fg_status fg_model_set_exact_resolve(fg_model* model, double kappa);
+
 /* certify(sentence, p, eps) -- cmd_verify (cli.cpp:64-133) for S sentences:
  * predicted = argmax(forward); verified = check_robust(concretize(pass), predicted, margin).
  * bounded[s] = 0 when the pass raised a domain error (cli.cpp:92-94). */
@@ -297,6 +317,8 @@ typedef struct {
   int slots;             /* sentences resident per pass */
   uint64_t launches;     /* kernels launched by the last call */
   double sentence_passes;/* sentence-passes executed (sum over passes of active slots) */
+  int exact_probes;      /* probes re-decided by the exact pass (fg_model_set_exact_resolve) */
+  double exact_ms;       /* time spent in those exact passes (included in device_ms) */
 } fg_run_stats;
 fg_status fg_last_run_stats(const fg_model* model, fg_run_stats* out);
 

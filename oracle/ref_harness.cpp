@@ -15,8 +15,13 @@
 // bit-for-bit in the reference's own whole-embedding mode.
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include "faith/bounds.hpp"
@@ -122,9 +127,11 @@ struct Walk {
   int max_nodes = 0;
   int count = 0;
   std::size_t off = 0;
+  std::function<void()> gate;  // paced walks (fo_paced_*): called before every node
 
   void dump(const LinearBounds& b) {
     if (max_nodes > 0 && ++count >= max_nodes) throw StopWalk{};
+    if (gate) gate();
     if (!node_lo) return;
     ConcreteBounds c = concretize(b, ps);
     std::memcpy(node_lo + off, c.lo.data(), c.lo.numel() * sizeof(double));
@@ -142,6 +149,7 @@ struct Walk {
   }
 
   LinearBounds run(LinearBounds cur) {
+    if (gate) gate();
     std::size_t L = s.length;
     for (const md::LayerWeights& w : s.layers) {
       LinearBounds q = rx::propagate_affine(cur, w.wq, &w.bq); dump(q);
@@ -510,6 +518,87 @@ int fo_ref_selfcheck(const fo_config* c, const double* params, const double* x, 
              same(want.uw, got.uw);
   });
   return st == FO_OK ? result : -st;
+}
+
+
+// ---- paced walks (bench.py --impl reference) ------------------------------------------------
+// A full word-level pass of the unmodified reference, run on its own thread and advanced a
+// given number of nodes per call, so that one complete pass per host core can be spread over
+// the timed steps of a benchmark run instead of being extrapolated from a prefix.
+struct fo_paced {
+  std::mutex mu;
+  std::condition_variable cv;
+  int allowed = 0, done = 0;  // gates the walk may pass / has passed (one before every node)
+  bool at_gate = false, finished = false;
+  int status = FO_OK;
+  std::vector<double> lo, hi;
+  std::thread th;
+};
+
+fo_paced* fo_paced_begin(const fo_config* c, const double* params, const double* x, const int* positions,
+                         int words, int norm, double eps) {
+  auto* p = new fo_paced();
+  md::TransformerSpec s = spec_from(c, params);
+  std::vector<double> xv(x, x + static_cast<std::size_t>(c->length) * c->embed);
+  std::vector<int> pv(positions, positions + words);
+  p->lo.resize(c->classes);
+  p->hi.resize(c->classes);
+  p->th = std::thread([p, s = std::move(s), xv = std::move(xv), pv = std::move(pv), words, norm, eps]() {
+    int st = guarded([&] {
+      std::size_t D = static_cast<std::size_t>(words) * s.embed_dim;
+      Walk walk{s, PerturbationSpec(to_norm(norm), eps, D), nullptr, nullptr};
+      walk.gate = [p] {  // the previous node is complete; wait for an allowance for the next one
+        std::unique_lock<std::mutex> lk(p->mu);
+        p->at_gate = true;
+        p->cv.notify_all();
+        p->cv.wait(lk, [p] { return p->done < p->allowed; });
+        p->at_gate = false;
+        ++p->done;
+      };
+      LinearBounds out = walk.run(word_input(s, xv.data(), pv.data(), words));
+      ConcreteBounds cb = concretize(out, walk.ps);
+      std::copy(cb.lo.data(), cb.lo.data() + cb.lo.numel(), p->lo.begin());
+      std::copy(cb.hi.data(), cb.hi.data() + cb.hi.numel(), p->hi.begin());
+    });
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->status = st;
+    p->finished = true;
+    p->cv.notify_all();
+  });
+  return p;
+}
+
+// Lets each of the n walks run `nodes` more nodes and waits until all of them have finished
+// those nodes (or the whole pass).  Returns the number of walks that finished.
+int fo_paced_step(fo_paced** walks, int n, int nodes) {
+  for (int i = 0; i < n; ++i) {
+    std::lock_guard<std::mutex> lk(walks[i]->mu);
+    walks[i]->allowed += nodes;
+    walks[i]->cv.notify_all();
+  }
+  int fin = 0;
+  for (int i = 0; i < n; ++i) {
+    fo_paced* p = walks[i];
+    std::unique_lock<std::mutex> lk(p->mu);
+    // the allowed nodes are complete when the walk waits at the gate after them (or finished)
+    p->cv.wait(lk, [p] { return p->finished || (p->at_gate && p->done >= p->allowed); });
+    fin += p->finished ? 1 : 0;
+  }
+  return fin;
+}
+
+int fo_paced_end(fo_paced* p, double* logits_lo, double* logits_hi) {
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    p->allowed = 1 << 30;
+    p->cv.notify_all();
+  }
+  p->th.join();
+  int st = p->status;
+  if (logits_lo) std::copy(p->lo.begin(), p->lo.end(), logits_lo);
+  if (logits_hi) std::copy(p->hi.begin(), p->hi.end(), logits_hi);
+  delete p;
+  return st;
 }
 
 }  // extern "C"

@@ -27,6 +27,7 @@ SOURCES = {
     "fg_shard.cu": [],
     "fg_forward.cu": [],
     "fg_graph.cu": ["-fmad=false"],
+    "fg_exact_pass.cu": ["-fmad=false"],
 }
 
 

@@ -75,5 +75,9 @@ CONFIGS = {
 SHAPE_CHECKS = {
     "c4m": Workload("c4m", 2, 8, 256, 512, 128, 1, "linf", 1e-4, 1,
                     description="c4-shaped mini: 2 layers d=256 8 heads ffn=512, seq 128, one word linf"),
+    # c5-shaped slice: the BERT-base layer (E 768, 12 heads, F 3072, 128 tokens, two words l2,
+    # D = 1536) at 2 layers, which the reference walks in about two hours on one core.
+    "c5s": Workload("c5s", 2, 12, 768, 3072, 128, 2, "l2", 1e-5, 1,
+                    description="c5-shaped slice: 2 layers d=768 12 heads ffn=3072, seq 128, two words l2"),
 }
 ALL = {**CONFIGS, **SHAPE_CHECKS}

@@ -708,6 +708,10 @@ struct fg_model {
   std::unique_ptr<Workspace> ws0;  // ε = 0 probe workspace (narrow, all-zero Λ; fg_maxeps)
   fg_run_stats stats{};
   fgh::ShardState shard;  // column sharding of the perturbation dimension (fg_model_set_column_shard)
+  DBuf params64;          // f64 weights on the device for the exact pass (uploaded on first use)
+  double kappa = FG_DEFAULT_KAPPA;  // ambiguity band of the decision-exact verdicts
+  int exact_probes = 0;   // per call: probes re-decided by the exact pass, and their time
+  double exact_ms = 0.0;
   // offsets of the layers in params (gen_synthetic order)
   size_t layer_off(int l) const {
     size_t e = cfg.embed, f = cfg.ffn;
@@ -1336,6 +1340,67 @@ int default_slots(const fg_model* m, int S, int D) {
   return std::max(1, std::min(slots, maxb));
 }
 
+// ---- decision-exact verdicts (fg_model_set_exact_resolve) -----------------------------
+// check_robust's strict test lo_t > hi_j + margin (bounds.cpp:142-157) is AMBIGUOUS on the f32-Λ
+// pass when the margin lies within the error estimate of the pass: a fraction kappa of the
+// Λ-derived widths of the two bounds (the f32 Λ / 3xTF32 error enters every bound through
+// ε·‖Λ‖ and the envelope lines built from it, so it scales with the widths) plus an f64 rounding
+// floor.  Such a probe is re-decided by the exact pass, whose arithmetic is the reference's.
+bool ambiguous_verdict(const double* lo, const double* hi, int C, int t, double margin, double kappa) {
+  if (!(kappa > 0.0)) return false;
+  for (int j = 0; j < C; ++j) {
+    if (j == t) continue;
+    const double m = lo[t] - hi[j] - margin;
+    const double band = kappa * ((hi[t] - lo[t]) + (hi[j] - lo[j])) +
+                        1e-11 * std::max({1.0, std::fabs(lo[t]), std::fabs(hi[j])});
+    if (!(std::fabs(m) > band)) return true;  // NaN-safe: a non-finite margin is ambiguous
+  }
+  return false;
+}
+
+fg_status upload_params64(fg_model* m) {
+  fg_ctx* ctx = m->ctx;
+  if (m->params64.p) return FG_OK;
+  CK(m->params64.alloc(sizeof(double) * m->params.size()));
+  CK(cudaMemcpy(m->params64.p, m->params.data(), sizeof(double) * m->params.size(), cudaMemcpyHostToDevice));
+  return FG_OK;
+}
+
+// Verdict of one probe (sentence s of the call's inputs at radius eps) from the fused pass's
+// logits bounds and status; ambiguous ones go through the exact pass.  `ps` is updated to the
+// status the decision rests on.  Returns the call status (a failure of the exact pass itself).
+fg_status decide_probe(fg_model* m, const double* x_s, const int* pos_s, int words, int norm, double eps,
+                       const double* lo, const double* hi, int pred, double margin, fg_status& ps, int& ok) {
+  const int C = m->cfg.classes;
+  ok = 0;
+  if (ps != FG_OK) return FG_OK;
+  fg_check_robust((size_t)C, lo, hi, (size_t)pred, margin, &ok);
+  if (!ambiguous_verdict(lo, hi, C, pred, margin, m->kappa)) return FG_OK;
+  fg_ctx* ctx = m->ctx;
+  if (fg_status st = upload_params64(m)) return st;
+  std::vector<double> elo(C), ehi(C);
+  int est = FG_OK;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, ctx->stream);
+  fg_status st = fgh::exact_pass(ctx, m->cfg, m->params64.as<double>(), x_s, pos_s, words, norm, eps, elo.data(),
+                                 ehi.data(), nullptr, nullptr, &est);
+  cudaEventRecord(b, ctx->stream);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (st) return st;
+  ++m->exact_probes;
+  m->exact_ms += ms;
+  ps = (fg_status)est;
+  ok = 0;
+  if (ps == FG_OK) fg_check_robust((size_t)C, elo.data(), ehi.data(), (size_t)pred, margin, &ok);
+  return FG_OK;
+}
+
 // Narrow workspace for the ε = 0 probes of fg_maxeps (see ensure_workspace's zero_d), with
 // the staged inputs of m->ws copied in; nullptr where it would not pay (D <= 128), when the
 // pass is column-sharded, under FG_NO_ZERO_PROBE=1, or when it does not fit in free HBM.
@@ -1514,7 +1579,7 @@ fg_status fg_bound_pass(fg_model* m, int S, const double* x, const int* position
   }
   cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(t0); cudaEventDestroy(t1);
   m->stats = fg_run_stats{total_ms, passes ? total_ms / passes : 0.0, passes, slots,
-                          ctx->launches - launches0, (double)S};
+                          ctx->launches - launches0, (double)S, 0, 0.0};
   return st;
 }
 
@@ -1559,14 +1624,23 @@ fg_status fg_certify(fg_model* m, int S, const double* x, const int* positions, 
   fg_status st = fg_bound_pass(m, S, x, positions, words, norm, eps, logits_lo, logits_hi, status);
   if (st) return st;
   const int C = m->cfg.classes;
+  const size_t LE = (size_t)m->cfg.length * m->cfg.embed;
+  fg_run_stats stats = m->stats;
+  m->exact_probes = 0;
+  m->exact_ms = 0.0;
   for (int s = 0; s < S; ++s) {
     predicted[s] = pred[s];
+    fg_status ps = (fg_status)status[s];
+    if ((st = decide_probe(m, x + s * LE, positions + (size_t)s * words, words, norm, eps[s],
+                           logits_lo + (size_t)s * C, logits_hi + (size_t)s * C, pred[s], margin, ps, verified[s])))
+      return st;
+    status[s] = ps;
     bounded[s] = status[s] != FG_EDOMAIN;  // cli.cpp:92-94
-    verified[s] = 0;
-    if (status[s] == FG_OK)
-      fg_check_robust((size_t)C, logits_lo + (size_t)s * C, logits_hi + (size_t)s * C, (size_t)pred[s],
-                      margin, &verified[s]);
   }
+  stats.exact_probes = m->exact_probes;
+  stats.exact_ms = m->exact_ms;
+  stats.device_ms += m->exact_ms;
+  m->stats = stats;
   return FG_OK;
 }
 
@@ -1588,6 +1662,8 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
   cudaEventCreate(&c0); cudaEventCreate(&c1); cudaEventCreate(&e0); cudaEventCreate(&e1);
   CK(cudaEventRecord(c0, ctx->stream));
   uint64_t launches0 = ctx->launches;
+  m->exact_probes = 0;
+  m->exact_ms = 0.0;
   // predicted classes on host threads, overlapped with the first passes
   std::future<std::vector<int>> fut = std::async(std::launch::async, predict_all, m, S, x);
   std::vector<int> pred;
@@ -1646,14 +1722,17 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
       sent[s].eps = eps_max;
     }
   }
-  auto decode_zero = [&]() {
+  const size_t LE = (size_t)m->cfg.length * m->cfg.embed;
+  auto decode_zero = [&]() -> fg_status {
     for (int s = 0; s < S; ++s) {
       fg_status ps = decode_status(zst[s]);
       int ok = 0;
-      if (ps == FG_OK)
-        fg_check_robust((size_t)C, &zlog[(size_t)s * 2 * C], &zlog[(size_t)s * 2 * C + C], (size_t)pred[s], 0.0, &ok);
+      if (fg_status e = decide_probe(m, x + s * LE, positions + (size_t)s * words, words, norm, 0.0,
+                                     &zlog[(size_t)s * 2 * C], &zlog[(size_t)s * 2 * C + C], pred[s], 0.0, ps, ok))
+        return e;
       zero_phase(s, ps, ok);
     }
+    return FG_OK;
   };
   while (done < S && !st) {
     for (int i = 0; i < slots; ++i) {
@@ -1670,7 +1749,7 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
     if (!have_pred) {
       pred = fut.get();
       have_pred = true;
-      if (!zst.empty()) decode_zero();
+      if (!zst.empty() && (st = decode_zero())) break;
     }
     for (int i = 0; i < slots; ++i) {
       int s = slot[i];
@@ -1683,9 +1762,10 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
       sentence_passes += 1.0;
       fg_status ps = decode_status(w.h_status[i]);
       int ok = 0;
-      if (ps == FG_OK)
-        fg_check_robust((size_t)C, w.h_logits + (size_t)i * C, w.h_logits + (size_t)slots * C + (size_t)i * C,
-                        (size_t)pred[s], 0.0, &ok);
+      if ((st = decide_probe(m, x + s * LE, positions + (size_t)s * words, words, norm, t.eps,
+                             w.h_logits + (size_t)i * C, w.h_logits + (size_t)slots * C + (size_t)i * C, pred[s],
+                             0.0, ps, ok)))
+        break;
       if (t.phase == P_ZERO) {  // verified_at(0, tolerate=false)
         zero_phase(s, ps, ok);
         if (t.phase == P_DONE) slot[i] = -1;
@@ -1727,7 +1807,7 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
   cudaEventElapsedTime(&total, c0, c1);
   cudaEventDestroy(c0); cudaEventDestroy(c1); cudaEventDestroy(e0); cudaEventDestroy(e1);
   m->stats = fg_run_stats{(double)total, passes ? pass_ms_sum / passes : 0.0, passes, slots,
-                          ctx->launches - launches0, sentence_passes};
+                          ctx->launches - launches0, sentence_passes, m->exact_probes, m->exact_ms};
   return st;
 }
 
@@ -1775,11 +1855,17 @@ fg_status fg_maxeps_spec(fg_model* m, int S, const double* x, const int* positio
   for (int s = 0; s < S; ++s) status_out[s] = FG_OK;
   int rounds = 0, done = 0;
   uint64_t launches0 = ctx->launches;
-  double dev_ms = 0.0, sentence_passes = 0.0;
+  double pass_ms_sum = 0.0, sentence_passes = 0.0;
   int passes = 0;
-  cudaEvent_t e0, e1;
+  m->exact_probes = 0;
+  m->exact_ms = 0.0;
+  const size_t LE = (size_t)m->cfg.length * m->cfg.embed;
+  cudaEvent_t e0, e1, c0, c1;  // e0/e1 per batched pass; c0/c1 span the whole call
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  cudaEventCreate(&c0);
+  cudaEventCreate(&c1);
+  cudaEventRecord(c0, ctx->stream);
   while (done < S) {
     // ---- probes of this round
     std::vector<SpecProbe> probes;
@@ -1807,8 +1893,10 @@ fg_status fg_maxeps_spec(fg_model* m, int S, const double* x, const int* positio
         level.swap(next);
       }
     }
-    // ---- evaluate this rank's share in batched passes of `slots` probes
-    std::vector<int> verdict(probes.size(), 0);
+    // ---- evaluate this rank's share in batched passes of `slots` probes.  The last word of
+    // the verdict vector carries this rank's call status, so a failure on one rank ends the
+    // call on every rank after the exchange instead of leaving the others waiting in it.
+    std::vector<int> verdict(probes.size() + 1, 0);
     std::vector<int> mine;
     for (int i = rank; i < (int)probes.size(); i += nranks) mine.push_back(i);
     for (size_t b0 = 0; b0 < mine.size(); b0 += slots) {
@@ -1820,22 +1908,27 @@ fg_status fg_maxeps_spec(fg_model* m, int S, const double* x, const int* positio
       }
       float ms = 0.f;
       if ((st = run_pass(m, norm, e0, e1, &ms))) break;
-      dev_ms += ms;
+      pass_ms_sum += ms;
       ++passes;
       sentence_passes += (double)nb;
-      for (size_t i = 0; i < nb; ++i) {
+      for (size_t i = 0; i < nb && !st; ++i) {
         const int pi = mine[b0 + i];
-        const fg_status ps = decode_status(w.h_status[i]);
+        const int s = probes[pi].sent;
+        fg_status ps = decode_status(w.h_status[i]);
         int ok = 0;
-        if (ps == FG_OK)
-          fg_check_robust((size_t)C, w.h_logits + i * C, w.h_logits + (size_t)slots * C + i * C,
-                          (size_t)pred[probes[pi].sent], 0.0, &ok);
+        st = decide_probe(m, x + s * LE, positions + (size_t)s * words, words, norm, probes[pi].eps,
+                          w.h_logits + i * C, w.h_logits + (size_t)slots * C + i * C, pred[s], 0.0, ps, ok);
         verdict[pi] = ps != FG_OK ? 10 + ps : (ok ? 2 : 1);
       }
+      if (st) break;
     }
-    if (st) break;
+    verdict.back() = st;
     if (nranks > 1 && exchange(user, verdict.data(), verdict.size()) != 0) {
       st = fail(ctx, FG_ERUNTIME, "fg_maxeps_spec: verdict exchange failed");
+      break;
+    }
+    if (verdict.back() != FG_OK) {  // this rank or another one failed (MAX over the ranks' codes)
+      if (!st) st = fail(ctx, (fg_status)verdict.back(), "fg_maxeps_spec: a pass failed on another rank");
       break;
     }
     ++rounds;
@@ -1895,12 +1988,18 @@ fg_status fg_maxeps_spec(fg_model* m, int S, const double* x, const int* positio
       }
     }
   }
+  cudaEventRecord(c1, ctx->stream);
+  cudaEventSynchronize(c1);
+  float total = 0.f;  // the whole call, host-side forward / exchanges / exact passes included
+  cudaEventElapsedTime(&total, c0, c1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  cudaEventDestroy(c0);
+  cudaEventDestroy(c1);
   for (int s = 0; s < S; ++s) predicted_out[s] = pred[s];
   *rounds_out = rounds;
-  m->stats = fg_run_stats{dev_ms, passes ? dev_ms / passes : 0.0, passes, slots, ctx->launches - launches0,
-                          sentence_passes};
+  m->stats = fg_run_stats{(double)total, passes ? pass_ms_sum / passes : 0.0, passes, slots,
+                          ctx->launches - launches0, sentence_passes, m->exact_probes, m->exact_ms};
   return st;
 }
 
@@ -2122,6 +2221,27 @@ fg_status fg_model_shard_loopback(fg_model* m, fg_loopback* g, int rank) {
   fgh::ShardState sh;
   if (fg_status s = fgh::loopback_exchange(g, rank, sh)) return fail(m->ctx, s, "column shard: bad loopback rank");
   return set_shard(m, std::move(sh));
+}
+
+fg_status fg_bound_pass_exact(fg_model* m, const double* x, const int* positions, int words, int norm, double eps,
+                              double* logits_lo, double* logits_hi, double* node_lo, double* node_hi,
+                              int* status) {
+  fg_ctx* ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
+  if (words < 1 || words > m->cfg.length) return fail(ctx, FG_EINVAL, "fg_bound_pass_exact: bad sizes");
+  for (int w = 0; w < words; ++w)
+    if (positions[w] < 0 || positions[w] >= m->cfg.length)
+      return fail(ctx, FG_EINVAL, "fg_bound_pass_exact: position out of range");
+  if (fg_status st = upload_params64(m)) return st;
+  return fgh::exact_pass(ctx, m->cfg, m->params64.as<double>(), x, positions, words, norm, eps, logits_lo,
+                         logits_hi, node_lo, node_hi, status);
+}
+
+fg_status fg_model_set_exact_resolve(fg_model* m, double kappa) {
+  if (!(kappa >= 0.0) || !std::isfinite(kappa)) return fail(m->ctx, FG_EINVAL, "fg_model_set_exact_resolve: kappa");
+  m->kappa = kappa;
+  return FG_OK;
 }
 
 fg_status fg_last_run_stats(const fg_model* m, fg_run_stats* out) {

@@ -107,6 +107,11 @@ fg_status x64_add(fg_ctx* ctx, size_t n, size_t d, const double* alw, const doub
 fg_status x64_scale(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const double* xlb, const double* xuw,
                     const double* xub, double s, double* ylw, double* ylb, double* yuw, double* yub);
 
+// The word-level pass of one sentence in the exact precision mode (fg_exact_pass.cu).
+fg_status exact_pass(fg_ctx* ctx, const fg_config& c, const double* params_dev, const double* x_host,
+                     const int* pos_host, int words, int norm, double eps, double* logits_lo, double* logits_hi,
+                     double* node_lo, double* node_hi, int* status);
+
 }  // namespace fgh
 
 #define CK(expr)                                                                             \

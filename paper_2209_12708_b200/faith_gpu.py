@@ -71,7 +71,8 @@ class Relaxation(NamedTuple):
 
 class RunStats(C.Structure):
     _fields_ = [("device_ms", C.c_double), ("pass_ms", C.c_double), ("passes", C.c_int), ("slots", C.c_int),
-                ("launches", C.c_uint64), ("sentence_passes", C.c_double)]
+                ("launches", C.c_uint64), ("sentence_passes", C.c_double), ("exact_probes", C.c_int),
+                ("exact_ms", C.c_double)]
 
 
 class FgConfig(C.Structure):
@@ -126,6 +127,8 @@ def load_library():
     L.fg_node_dump_size.argtypes = [C.POINTER(FgConfig)]
     L.fg_bound_pass.argtypes = [vp, C.c_int, _dp, _ip, C.c_int, C.c_int, _dp, _dp, _dp, _ip]
     L.fg_bound_pass_dump.argtypes = [vp, _dp, _ip, C.c_int, C.c_int, C.c_double, _dp, _dp, _dp, _dp, _ip]
+    L.fg_bound_pass_exact.argtypes = [vp, _dp, _ip, C.c_int, C.c_int, C.c_double, _dp, _dp, _dp, _dp, _ip]
+    L.fg_model_set_exact_resolve.argtypes = [vp, C.c_double]
     L.fg_certify.argtypes = [vp, C.c_int, _dp, _ip, C.c_int, C.c_int, _dp, C.c_double, _ip, _ip, _ip, _dp, _dp, _ip]
     L.fg_maxeps.argtypes = [vp, C.c_int, _dp, _ip, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _dp, _ip,
                             _ip, _ip]
@@ -589,6 +592,25 @@ class Model:
                                                     eps, _d(lo), _d(hi), _d(nlo), _d(nhi), _i(st)),
                         "fg_bound_pass_dump")
         return int(st[0]), lo, hi, nlo, nhi
+
+    def bound_pass_exact(self, x, positions, norm: str, eps: float, dump: bool = False):
+        """fg_bound_pass_exact: one sentence in the exact (reference-order f64) mode on the device
+        -> (status, logits_lo, logits_hi, node_lo, node_hi); node arrays None unless dump."""
+        x, pos = self._inputs(x, positions)
+        nlo = nhi = None
+        if dump:
+            n = int(self.lib.fg_node_dump_size(C.byref(self.cfg.fg())))
+            nlo, nhi = np.zeros(n), np.zeros(n)
+        lo, hi = np.zeros(self.cfg.classes), np.zeros(self.cfg.classes)
+        st = np.zeros(1, dtype=np.int32)
+        self.ctx._check(self.lib.fg_bound_pass_exact(self.handle, _d(x[0]), _i(pos[0]), pos.shape[1], NORM[norm],
+                                                     eps, _d(lo), _d(hi), _d(nlo), _d(nhi), _i(st)),
+                        "fg_bound_pass_exact")
+        return int(st[0]), lo, hi, nlo, nhi
+
+    def set_exact_resolve(self, kappa: float):
+        """Ambiguity band of the decision-exact verdicts (include/faith_gpu.h); 0 = raw f32 verdicts."""
+        self.ctx._check(self.lib.fg_model_set_exact_resolve(self.handle, float(kappa)), "fg_model_set_exact_resolve")
 
     def certify(self, x, positions, norm: str, eps, margin: float = 0.0):
         """cmd_verify semantics per sentence -> dict of arrays."""

@@ -68,10 +68,10 @@ def test_pass_matches_golden(models, port, path):
     s = int(os.path.basename(path).split("_s")[1].split(".")[0])
     w, cfg, params, m = models(name)
     _, x, pos = sentence(port, w, s)
-    st, lo, hi, nlo, nhi = m.bound_pass_dump(x, pos, w.norm, w.eps)
+    st, lo, hi, nlo, nhi = m.bound_pass_dump(x, pos, w.norm, float(g["eps"]))
     assert st == int(g["status"])
     assert close(lo, g["logits_lo"])[0] and close(hi, g["logits_hi"])[0], (lo, hi, g["logits_lo"], g["logits_hi"])
-    check_nodes(cfg, nlo, nhi, g["node_lo"].astype(np.float64), g["node_hi"].astype(np.float64), g["node_index"])
+    check_nodes(cfg, nlo, nhi, g["node_lo"], g["node_hi"], g["node_index"])
 
 
 # ---- against the C restatement on configs the golden set does not cover ----------

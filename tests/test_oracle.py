@@ -166,17 +166,20 @@ def test_port_matches_golden_pass(port, path):
     w = CONFIGS[name]
     if name in ("c3", "c4m") and not os.environ.get("FAITH_SLOW_TESTS"):
         pytest.skip(f"{name} reference pass takes minutes on one core (set FAITH_SLOW_TESTS=1)")
+    if name in ("c4", "c5s") and not os.environ.get("FAITH_VERY_SLOW_TESTS"):
+        pytest.skip(f"{name} reference pass takes hours on one core (set FAITH_VERY_SLOW_TESTS=1)")
     cfg = model_config(w)
     params = port.gen_model(cfg, w.model_seed)
     x = port.gen_input(cfg, w.input_seed(s))
     pos = port.gen_positions(w.position_seed(s), w.length, w.words)
     assert np.array_equal(pos, g["positions"])
-    st, lo, hi, nlo, nhi = port.bound_pass(cfg, params, x, pos, w.norm, w.eps, dump=True)
+    st, lo, hi, nlo, nhi = port.bound_pass(cfg, params, x, pos, w.norm, float(g["eps"]), dump=True)
     assert st == int(g["status"])
     assert np.array_equal(lo, g["logits_lo"]) and np.array_equal(hi, g["logits_hi"])
     idx = g["node_index"]
-    assert np.array_equal(nlo[idx].astype(np.float32), g["node_lo"])
-    assert np.array_equal(nhi[idx].astype(np.float32), g["node_hi"])
+    assert g["node_lo"].dtype == np.float64  # golden node bounds are stored bit-exact
+    assert np.array_equal(nlo[idx], g["node_lo"])
+    assert np.array_equal(nhi[idx], g["node_hi"])
 
 
 def _golden_maxeps():
