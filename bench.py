@@ -6,17 +6,23 @@ GPU (each sentence 22 bound passes unless eps_max verifies).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
 
-Multi-GPU: one process per GPU (torchrun); sentences are sharded across ranks with no
-data-path collective ("scaling": "weak"); torch.distributed only provides the barrier and
-the max-over-ranks of the device time.  `--impl reference` times the reference's own CPU
-path (oracle/_ref, the unmodified reference build; the C restatement if absent) on the
-host cores, rank 0 only.
+Multi-GPU: one process per GPU.  Under torchrun (WORLD_SIZE set) each process is one rank;
+`--gpus N` without torchrun re-launches this script under `torch.distributed.run` with N ranks.
+Sentences are sharded across ranks with no data-path collective ("scaling": "weak");
+torch.distributed only provides the barrier and the max-over-ranks of the device time.
+Verdicts are decision-exact (fg_model_set_exact_resolve, on by default): ambiguous probes are
+re-decided by the exact pass inside the timed region.  `--impl reference` times the reference's
+own CPU path (oracle/_ref, the unmodified reference build) on the host cores, rank 0 only: one
+complete bound pass per host thread, advanced node by node across the timed steps (measured,
+not extrapolated from a prefix).
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -27,17 +33,20 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: NCCL's own logging (e.g. its version banner) goes to stderr
-os.environ.setdefault("NCCL_DEBUG", "WARN")
+# stdout carries exactly one JSON line: NCCL's own logging goes to stderr (INFO, so the
+# communicator size of a multi-GPU run is visible in the log)
+os.environ.setdefault("NCCL_DEBUG", "INFO")
+os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 from paper_2209_12708_b200.configs import CONFIGS  # noqa: E402
 
-# CPU-baseline sample: the first SAMPLE_NODES nodes of the word-level bound pass (layer-1
-# Q, K, V propagate_affine).  PASS_OVER_SAMPLE = full pass time / sample time, measured
-# single-threaded on the unmodified reference build.
+# Our arm's bounded CPU sample: the first SAMPLE_NODES nodes of the word-level bound pass
+# (layer-1 Q, K, V propagate_affine), scaled to a pass with the single-thread calibration
+# profiles/cpu_calibration.json -- reported as extrapolated; the reference arm measures full passes.
 SAMPLE_NODES = 3
 CALIB_PATH = os.path.join(ROOT, "profiles", "cpu_calibration.json")
+METRIC = "certified sentences/sec (eps binary search)"
 
 
 def load_calibration(name):
@@ -60,8 +69,33 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def host_cpu() -> dict:
+    """CPU model, logical CPUs and threads per core of this host."""
+    model, tpc = "", None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Thread(s) per core:"):
+                tpc = int(ln.split(":")[1])
+    except (OSError, ValueError, subprocess.SubprocessError):
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count(), "threads_per_core": tpc}
+
+
+def search_passes(w) -> int:
+    """Bound passes of one cmd_maxeps search (cli.cpp:159-176): verified_at(0), verified_at(eps_max),
+    then one per bisection step while hi - lo > tol: 2 + ceil(log2(eps_max / tol)) whenever eps_max
+    does not verify (every c2-c5 sentence; our arm reports the measured passes_per_sentence)."""
+    return 2 + int(math.ceil(math.log2(w.eps_max / w.tol)))
+
+
 # ---------------------------------------------------------------------------
-# algorithmic work per sentence-pass
+# algorithmic work per sentence-pass (SURVEY 8(a)/(d); DESIGN.md §5)
 # ---------------------------------------------------------------------------
 def affine_flops(w) -> float:
     """Useful flops of the bound GEMMs: 4*L*C*O*D per affine (both bounds, one product each).
@@ -73,13 +107,20 @@ def affine_flops(w) -> float:
 
 
 def site_bytes(w) -> dict:
-    """Algorithmic HBM bytes per sentence-pass of the memory-bound sites (f32 Λ, 2 planes)."""
-    L, E, F, H, D = w.length, w.embed, w.ffn, w.heads, w.pert_dim
+    """Algorithmic HBM bytes per sentence-pass of the memory-bound sites: f32 Λ, two planes,
+    each Λ a site must read counted once and each Λ it produces written once.  Layer 1 is
+    sparse: Λ0 is one-hot, so only the W perturbed token rows of Q/K/V carry Λ; the layer-1
+    concretization reads those rows only and the layer-1 similarity product gathers only those
+    Q/K rows, so those are the bytes counted there."""
+    L, E, F, H, D, W = w.length, w.embed, w.ffn, w.heads, w.pert_dim, w.words
     lam = 2 * 4 * D
+    deep = w.layers - 1
     return {
-        "concretize": w.layers * L * 3 * E * lam,                 # read QKV Λ
-        "act_verify": w.layers * 2 * L * F * lam,                 # read + write FFN Λ
-        "softmax": w.layers * 2 * H * L * L * lam,                # read + write scores Λ
+        "concretize": (deep * L + W) * 3 * E * lam,                                     # read Q/K/V rows
+        "dot_similarity": (deep * 2 * L * E + 2 * W * E + w.layers * H * L * L) * lam,  # read Q, K; write scores
+        "softmax": w.layers * 2 * H * L * L * lam,                                      # read + write scores
+        "dot_weighted": w.layers * (H * L * L + 2 * L * E) * lam,                       # read P, V; write context
+        "act_verify": w.layers * 2 * L * F * lam,                                       # read + write FFN Λ
     }
 
 
@@ -140,11 +181,12 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (reference build / port), bounded sample on the host cores
+# CPU paths (reference build / port) on the host cores
 # ---------------------------------------------------------------------------
 def cpu_sample(w, n_threads: int, first_sentence: int):
-    """Runs the SAMPLE_NODES-node prefix of the bound pass for n_threads sentences concurrently
-    (one per host thread, single-threaded each like the reference).  Returns (wall_s, kind)."""
+    """Our arm's bounded sample: the SAMPLE_NODES-node prefix of the bound pass for n_threads
+    sentences concurrently (one per host thread, single-threaded each like the reference).
+    Returns (wall_s, kind)."""
     import ctypes as C
     from oracle.oracle import LIBS, NORM, ModelConfig, Oracle, _d, _i
     kind = "reference" if os.path.exists(LIBS["reference"]) else "port"
@@ -179,55 +221,129 @@ def pass_over_sample(w, kind):
     return (cal.get(kind) or cal.get("reference") or cal.get("port") or {}).get("pass_over_sample")
 
 
-def scale_phrase(w, kind):
-    """How the sample extrapolates to a full pass, or why it does not (no calibration row)."""
-    ratio = pass_over_sample(w, kind)
-    if not ratio:
-        return (f"no single-thread full-pass calibration for {w.name} in profiles/cpu_calibration.json, "
-                "so value is null")
-    return f"full pass = sample x {ratio} (single-thread calibration, profiles/cpu_calibration.json)"
+def paced_full_pass(w, n_threads: int, first_sentence: int, steps: int, warmup: int):
+    """One COMPLETE word-level bound pass of the unmodified reference per host thread, all
+    running concurrently; the walks advance a slice of nodes per timed step (fo_paced_step), so
+    the timed steps together cover exactly one full pass per thread.  Returns per-step walls."""
+    import ctypes as C
+    from oracle.oracle import NORM, ModelConfig, Oracle
+    o = Oracle("reference")
+    L = o.lib
+    L.fo_paced_begin.restype = C.c_void_p
+    L.fo_paced_begin.argtypes = [C.c_void_p] * 4 + [C.c_int, C.c_int, C.c_double]
+    L.fo_paced_step.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int]
+    L.fo_paced_end.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    cfg = ModelConfig(w.layers, w.heads, w.embed, w.ffn, w.length, w.classes, w.activation)
+    params = o.gen_model(cfg, w.model_seed)
+    fc = cfg.fo()
+    keep = []
 
+    def begin(first, n):
+        hs = []
+        for i in range(n):
+            s = first + i
+            x = o.gen_input(cfg, w.input_seed(s))
+            pos = np.ascontiguousarray(o.gen_positions(w.position_seed(s), w.length, w.words), dtype=np.int32)
+            keep.append((x, pos))
+            hs.append(L.fo_paced_begin(C.byref(fc), params.ctypes.data, x.ctypes.data, pos.ctypes.data, w.words,
+                                       NORM[w.norm], w.eps))
+        return hs, (C.c_void_p * n)(*hs)
 
-def cpu_rate(w, wall_s, n_threads, passes_per_sentence, kind):
-    """sentences/s of the reference CPU path extrapolated from the sample."""
-    ratio = pass_over_sample(w, kind)
-    if not ratio:
-        return None, None
-    t_pass = wall_s * ratio
-    return n_threads / (t_pass * passes_per_sentence), t_pass
+    nodes = w.layers * 16 + 2  # nodes of the walk (fo_bound_pass node order)
+    # warm-up steps: the first node of a separate set of walks (pages in the library / weights)
+    whs, warr = begin(first_sentence + 10_000, n_threads)
+    for k in range(warmup):
+        L.fo_paced_step(warr, n_threads, 1 if k == 0 else 0)
+    for h in whs:
+        L.fo_paced_end(h, None, None)
+    hs, arr = begin(first_sentence, n_threads)
+    walls = []
+    for k in range(steps):
+        n_k = (k + 1) * nodes // steps - k * nodes // steps
+        t0 = time.perf_counter()
+        L.fo_paced_step(arr, n_threads, n_k)
+        walls.append(time.perf_counter() - t0)
+    status = [L.fo_paced_end(h, None, None) for h in hs]
+    return walls, nodes, status
 
 
 def reference_arm(args, w):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    from oracle.oracle import LIBS
     n_threads = os.cpu_count() or 1
-    calls = load_calibration(w.name) or {}
-    passes = calls.get("passes_per_sentence", 22)
-    for i in range(args.warmup):
-        cpu_sample(w, n_threads, 10_000 + i * n_threads)
-    walls = []
-    kind = "port"
+    passes = search_passes(w)
+    cpu = host_cpu()
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        wall, kind = cpu_sample(w, n_threads, 20_000 + i * n_threads)
-        walls.append(wall)
+    if os.path.exists(LIBS["reference"]):
+        walls, nodes, status = paced_full_pass(w, n_threads, 20_000, args.steps, args.warmup)
+        kind = "reference"
+        t_pass = sum(walls)
+        value = n_threads / (t_pass * passes)
+        sample = (f"one complete {w.name} word-level bound pass (all {nodes} nodes, eps {w.eps:g}) per host thread, "
+                  f"{n_threads} sentences concurrently on the unmodified reference build, advanced in "
+                  f"{args.steps} node slices (one per timed step): full pass measured, {t_pass:.1f} s wall; "
+                  f"x {passes} passes per sentence (2 + ceil(log2(eps_max/tol)), cli.cpp:159-176); "
+                  f"pass statuses {sorted(set(status))}")
+    else:
+        walls = []
+        kind = "port"
+        for i in range(args.steps):
+            walls.append(cpu_sample(w, n_threads, 20_000 + i * n_threads)[0])
+        ratio = pass_over_sample(w, kind)
+        t_pass = statistics.mean(walls) * ratio if ratio else None
+        value = n_threads / (t_pass * passes) if t_pass else None
+        sample = (f"EXTRAPOLATED (reference build absent): first {SAMPLE_NODES} nodes on the C restatement, "
+                  f"x {ratio} (profiles/cpu_calibration.json) x {passes} passes")
     total = time.perf_counter() - t0
-    wall = sum(walls) / len(walls)
-    value, t_pass = cpu_rate(w, wall, n_threads, passes, kind)
-    sample = (f"first {SAMPLE_NODES} nodes (layer-1 Q,K,V propagate_affine) of the {w.name} word-level bound pass, "
-              f"{n_threads} sentences concurrently (one per host thread); "
-              f"{scale_phrase(w, kind)}, "
-              f"{passes} passes per sentence")
-    line = {"impl": "reference", "metric": "certified sentences/sec (eps binary search)", "value": value,
+    line = {"impl": "reference", "metric": METRIC, "value": value,
             "unit": "sentences/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": w.as_dict(),
-            "ms_per_bound_pass": None if t_pass is None else 1e3 * t_pass / 1.0,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": {"workload": w.name, **w.as_dict()},
+            "ms_per_bound_pass": None if t_pass is None else 1e3 * t_pass,
             "cpu_baseline": {"value": value, "unit": "sentences/s", "cores": n_threads, "kind": kind,
-                             "sample": sample},
+                             "sample": sample, "cpu": cpu},
             "e2e": {"value": value, "unit": "sentences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# launching N ranks without torchrun
+# ---------------------------------------------------------------------------
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run with N ranks
+    (127.0.0.1 rendezvous); rank 0's JSON line is the only stdout."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def dry_run(args, w) -> int:
+    """--dry-run: the multi-rank plumbing without a GPU (gloo): rank/world, the sentence blocks and
+    the max-over-ranks reduction; prints the JSON line's shape keys."""
+    from paper_2209_12708_b200 import dist as D
+    rank, world, _ = dist_env()
+    dist = D.init(backend="gloo")
+    assert world == args.gpus, f"world size {world} != --gpus {args.gpus}"
+    B = args.batch or {"c1": 256, "c2": 256, "c3": 64, "c4": 16, "c5": 4}[w.name]
+    ids = [list(D.sentence_block(rank, s, args.steps + args.warmup, B)) for s in range(args.steps + args.warmup)]
+    first = D.max_over_ranks([ids[0][0]], dist)[0]
+    line = {"metric": METRIC, "value": None, "n_gpus": world, "dry_run": True,
+            "config": {"workload": w.name, "global_batch": B * world, "sentences_per_step_per_gpu": B,
+                       "parallelism": f"sentence-sharded dp{world}"},
+            "max_first_sentence_over_ranks": first}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
     return 0
 
 
@@ -244,6 +360,10 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="sentences per step per GPU (default: per config)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--raw-f32-verdicts", action="store_true",
+                    help="decide every probe on the f32-Λ pass alone (kappa 0; comparison only: near ε* the "
+                         "bisection may leave the reference's path)")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (gloo, no GPU work)")
     ap.add_argument("--shard", default="sentences", choices=["sentences", "columns"],
                     help="sentences: independent sentences per GPU (weak scaling, no collective); columns: "
                          "perturbation columns of every sentence split over the GPUs, concretization partials "
@@ -255,6 +375,10 @@ def main():
     w = CONFIGS[args.config]
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args)
+    if args.dry_run:
+        return dry_run(args, w)
     if args.impl == "reference":
         return reference_arm(args, w)
 
@@ -263,6 +387,8 @@ def main():
     from paper_2209_12708_b200 import faith_gpu as F
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE {world} != --gpus {args.gpus}")
     torch.cuda.set_device(local)
     dist = D.init(backend="nccl", device_index=local)
     B = args.batch or {"c1": 256, "c2": 256, "c3": 64, "c4": 16, "c5": 4}[w.name]
@@ -270,6 +396,8 @@ def main():
     cfg = F.ModelConfig(w.layers, w.heads, w.embed, w.ffn, w.length, w.classes, w.activation)
     ctx = F.Context(local)
     model = F.Model(ctx, cfg, F.gen_synthetic(cfg, w.model_seed))
+    if args.raw_f32_verdicts:
+        model.set_exact_resolve(0.0)
     columns = args.shard == "columns"
     spec = args.speculative > 0
     if columns:
@@ -298,9 +426,8 @@ def main():
     for s in range(args.warmup):
         search(*inputs[s])
     barrier()
-    dev_ms, calls, launches, passes, pass_ms = 0.0, [], 0, 0, []
-    h2d = B * (w.length * w.embed * 8 + w.words * 4)
-    d2h = B * (8 + 4 + 4 + 4)
+    dev_ms, calls, launches, passes, pass_ms, exact_probes, exact_ms = 0.0, [], 0, 0, [], 0, 0.0
+    h2d = d2h = 0
     # fg_maxeps runs the eps = 0 probes up front on a narrow workspace (one pass for B <= 256
     # sentences) when words*embed > 128 and the pass is not column-sharded: its eps/slot staging
     # and verdict readback
@@ -315,11 +442,18 @@ def main():
             launches += st["launches"]
             passes += st["passes"]
             pass_ms.append(st["pass_ms"])
+            exact_probes += st["exact_probes"]
+            exact_ms += st["exact_ms"]
             calls.extend(r["calls"].tolist())
-            # per-pass eps/slot staging and verdict readback
+            # every step copies its batch's inputs in (x f64, positions i32) and the results out
+            # (eps f64, calls / predicted / status i32), plus per pass the eps/slot staging and
+            # the logits-bound/status readback; an exact re-decision copies one sentence in and
+            # its logits out
+            h2d += B * (w.length * w.embed * 8 + w.words * 4)
+            d2h += B * (8 + 4 + 4 + 4)
             zp = -(-B // 256) if zero_probe else 0
-            h2d += (st["passes"] + zp) * B * (8 + 4)
-            d2h += (st["passes"] + zp) * B * (2 * w.classes * 8 + 4)
+            h2d += (st["passes"] + zp) * B * (8 + 4) + st["exact_probes"] * (w.length * w.embed * 8 + w.words * 4)
+            d2h += (st["passes"] + zp) * B * (2 * w.classes * 8 + 4) + st["exact_probes"] * 2 * w.classes * 8
         barrier()
         wall = time.perf_counter() - t0
     dev_ms_max, wall_max = D.max_over_ranks([dev_ms, wall], dist, device="cuda")
@@ -330,7 +464,7 @@ def main():
     ms_pass_sentence = ms_pass_batched / B
 
     line = {
-        "metric": "certified sentences/sec (eps binary search)", "value": value, "unit": "sentences/s",
+        "metric": METRIC, "value": value, "unit": "sentences/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps,
         "higher_is_better": True, "scaling": "strong" if (columns or spec) else "weak", "vs_baseline": None,
         "dtype": "f32+f64",
@@ -342,11 +476,16 @@ def main():
                                    if columns else
                                    f"speculative bisection depth {args.speculative} over {world} GPU(s)" if spec
                                    else f"sentence-sharded dp{world}"),
+                   "verdicts": "raw f32 (kappa 0)" if args.raw_f32_verdicts else
+                               f"decision-exact (kappa {F.DEFAULT_KAPPA:g}: ambiguous probes re-decided by the "
+                               "exact pass)",
                    "l2_flush": "not needed: inputs larger than L2 (Λ working set "
                                f"{B * 0.45:.1f} GB per GPU >> 126 MB L2)"},
         "ms_per_bound_pass": {"batched_pass_ms": ms_pass_batched, "per_sentence_ms": ms_pass_sentence,
                               "batch": B},
         "passes_per_sentence": statistics.mean(calls),
+        "exact_probes_per_sentence": exact_probes / (B * args.steps),
+        "exact_ms_share": exact_ms / dev_ms if dev_ms else 0.0,
         "e2e": {"value": e2e, "unit": "sentences/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches,
@@ -358,6 +497,7 @@ def main():
         prof = model.profile_pass(w.norm, w.eps)
     if rank == 0 and prof is not None:
         pk, pk_kind = peaks()
+        tf32 = ctx.mma_peak("tf32")["tflops"]
         total = sum(ms for ms, _ in prof.values())
         gemm_ms, gemm_k = prof.get("affine_gemm", (0.0, 0))
         flops = affine_flops(w) * B / (world if columns else 1)
@@ -376,33 +516,39 @@ def main():
             "algorithmic": f"{affine_flops(w):.4g} useful flop per sentence-pass (4*L*C*O*D per GEMM affine; "
                            f"layer-1 Q/K/V is a one-hot scatter) x {B} sentences per launch set",
             "launches_per_pass": gemm_k, "share_of_pass": gemm_ms / total if total else None,
-            # the precision north_star asks for (error-compensated 3xTF32): kind::tf32 runs at half the
-            # dense bf16 rate and each useful product costs three MMAs, so its ceiling is bf16 / 6
-            "peak_3xtf32": pk["bf16_tflops"] / 6.0,
-            "frac_3xtf32": (ach / (pk["bf16_tflops"] / 6.0)) if ach else None,
+            # the precision north_star asks for (error-compensated 3xTF32): each useful product costs
+            # three kind::tf32 MMAs, so its ceiling is the measured dense TF32 rate / 3
+            "peak_tf32_measured": tf32,
+            "peak_tf32_source": "fg_selftest_mma_peak: tcgen05.mma kind::tf32 M128 N256, one CTA per SM, "
+                                "SMEM-resident operands, this run",
+            "peak_3xtf32": tf32 / 3.0,
+            "frac_3xtf32": (ach / (tf32 / 3.0)) if ach else None,
         }
         mem = {}
         for site, nbytes in site_bytes(w).items():
             if site in prof and prof[site][0] > 0:
                 gbs = nbytes * B / (world if columns else 1) / (prof[site][0] / 1e3) / 1e9
-                mem[site] = {"GB/s": gbs, "frac_hbm": gbs / pk["hbm_gbs"], "ms": prof[site][0]}
+                mem[site] = {"GB/s": gbs, "frac_hbm": gbs / pk["hbm_gbs"], "ms": prof[site][0],
+                             "algorithmic_GB": nbytes * B / 1e9}
         line["kernels"] = {k: {"ms_per_pass": v[0], "launches": v[1]} for k, v in sorted(prof.items())}
-        mem["_note"] = ("GB/s = algorithmic bytes (each Λ read once, written once) / site time; a site that "
-                        "reads what the previous kernel just wrote (concretize after the Q/K/V GEMM) partly "
-                        "hits the 126 MB L2, so its rate can exceed the HBM peak; DRAM bytes per launch are in "
-                        "profiles/r1c_ncu_launches_c3.txt")
+        mem["_note"] = ("GB/s = algorithmic bytes (each Λ a site reads counted once, each Λ it writes once; "
+                        "layer-1 Q/K/V rows only where Λ is non-zero) / site time of one eager profiled pass; "
+                        "DRAM bytes per launch are in the committed ncu launch list (profiles/)")
         line["hbm_sites"] = mem
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_threads = os.cpu_count() or 1
         wall_cpu, kind = cpu_sample(w, n_threads, 900_000)
-        rate, t_pass = cpu_rate(w, wall_cpu, n_threads, statistics.mean(calls), kind)
+        ratio = pass_over_sample(w, kind)
+        t_pass = wall_cpu * ratio if ratio else None
+        rate = n_threads / (t_pass * statistics.mean(calls)) if t_pass else None
+        cal = load_calibration(w.name) or {}
         line["cpu_baseline"] = {
-            "value": rate, "unit": "sentences/s", "cores": n_threads, "kind": kind,
-            "sample": f"first {SAMPLE_NODES} nodes of the {w.name} bound pass for {n_threads} sentences "
-                      f"concurrently ({wall_cpu:.1f} s wall); "
-                      f"{scale_phrase(w, kind)}; "
-                      f"{statistics.mean(calls):.1f} passes/sentence",
+            "value": rate, "unit": "sentences/s", "cores": n_threads, "kind": kind, "cpu": host_cpu(),
+            "sample": f"EXTRAPOLATED: first {SAMPLE_NODES} nodes of the {w.name} bound pass for {n_threads} sentences "
+                      f"concurrently ({wall_cpu:.1f} s wall) x {ratio} (full pass / sample, single-thread, "
+                      f"{cal.get('host', 'build container')}: profiles/cpu_calibration.json) x "
+                      f"{statistics.mean(calls):.1f} passes/sentence; bench.py --impl reference measures full passes",
         }
     if rank == 0:
         print(json.dumps(line), flush=True)

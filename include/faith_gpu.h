@@ -214,12 +214,14 @@ fg_status fg_bound_pass_exact(fg_model* model, const double* x, const int* posit
                               double* node_lo, double* node_hi, int* status);
 
 /* Decision-exact verdicts.  fg_certify, fg_maxeps and fg_maxeps_spec decide every probe with
- * check_robust on the fused f32-Λ pass; a probe is AMBIGUOUS when for some class j != t
- *   |lo_t - hi_j - margin| <= kappa * ((hi_t - lo_t) + (hi_j - lo_j)) + 1e-11 * max(1, |lo_t|, |hi_j|)
- * i.e. its margin lies within the f32-Λ error estimate (a fraction kappa of the Λ-derived bound
- * widths) of zero.  Ambiguous probes are re-decided by fg_bound_pass_exact, so every verdict is
- * the reference's.  kappa = 0 turns the re-decision off (raw f32 verdicts).  The default is
- * FG_DEFAULT_KAPPA (measured f32-vs-exact margin error x 50). */
+ * check_robust on the fused f32-Λ pass; a probe is AMBIGUOUS when for some class j != t its
+ * margin m = lo_t - hi_j - margin lies in the error band of that pass,
+ *   -kappa/10 * W - f <= m <= kappa * W + f,   W = (hi_t - lo_t) + (hi_j - lo_j),
+ *   f = 1e-11 * max(1, |lo_t|, |hi_j|)
+ * (one-sided: the fused pass's tcgen05 accumulation truncates toward zero, so its widths come
+ * out slightly small and its margins large; measured (m_f32 - m_exact) / W in [+8.2e-7, +5.1e-6]
+ * at c3).  Ambiguous probes are re-decided by fg_bound_pass_exact, so
+ * every verdict is the reference's.  kappa = 0 turns the re-decision off (raw f32 verdicts). */
 #define FG_DEFAULT_KAPPA 1e-5
 fg_status fg_model_set_exact_resolve(fg_model* model, double kappa);
 
@@ -307,6 +309,12 @@ fg_status fg_profile_pass(fg_model* model, int norm, double eps, int max_sites, 
  * O % 128, C % 32, D % 128); ms_* = CUDA-event time of one launch. */
 fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_t seed, double* err_umma,
                              double* err_simt, double* ms_umma, double* ms_simt);
+
+/* Dense tensor-pipe peak on this device (the roofline denominator of the 3xTF32 GEMMs): one CTA
+ * per SM issuing tcgen05.mma M=128 N=256 back to back on SMEM-resident operands, `iters` x 4
+ * MMAs each.  kind 0 = kind::tf32, 1 = kind::f16 with bf16 operands.  ms = CUDA-event time,
+ * tflops = 2*M*N*K*MMAs / time. */
+fg_status fg_selftest_mma_peak(fg_ctx* ctx, int kind, int iters, double* ms, double* tflops);
 
 /* Timing of the last fg_maxeps / fg_bound_pass call, measured with CUDA events on the
  * library's stream (device time), and pass counts. */

@@ -49,6 +49,77 @@ __global__ void x_affine_lam_kernel(const double* __restrict__ xlw, const double
   ylw[rj * d + k] = yl + ln;
 }
 
+// The same Λ rows, JT outputs per thread: thread = (row r, outputs j0..j0+JT-1, column k).
+// Every output still accumulates its four partial sums over i = 0..c-1 in order, so the
+// result is bit-identical to x_affine_lam_kernel; the block stages kIC input rows of both Λ
+// planes (its 128 columns) and the matching kIC x JT weights in shared memory per step, so
+// the loads are issued together and each x value feeds JT outputs (the one-output kernel
+// re-reads each Λ row from L2 once per output).  Terms with w == 0 are skipped: both of their
+// products are signed zeros, and adding a signed zero never changes a partial sum here (a sum
+// that starts at +0.0 can never become -0.0 in round-to-nearest), so skipping them is exact.
+// The sign tests read shared memory and are warp-uniform (all threads share j).
+constexpr int kIC = 16;
+template <int JT>
+__global__ void __launch_bounds__(kXThreads) x_affine_lam_tiled_kernel(
+    const double* __restrict__ xlw, const double* __restrict__ xuw, const double* __restrict__ w,
+    double* __restrict__ ylw, double* __restrict__ yuw, long long rows, int c, int o, int d) {
+  __shared__ double su[kIC][kXThreads], sl[kIC][kXThreads], sw[kIC][JT];
+  const int kb = (d + kXThreads - 1) / kXThreads;
+  const int jtiles = o / JT;
+  const long long blk = blockIdx.x;
+  const int kc = (int)(blk % kb);
+  const long long rjt = blk / kb;
+  const int jt = (int)(rjt % jtiles);
+  const long long r = rjt / jtiles;
+  const int k = kc * kXThreads + threadIdx.x;
+  if (r >= rows) return;
+  const bool live = k < d;
+  const int j0 = jt * JT;
+  double yu[JT], un[JT], yl[JT], ln[JT];
+#pragma unroll
+  for (int t = 0; t < JT; ++t) yu[t] = un[t] = yl[t] = ln[t] = 0.0;
+  const double* xu_p = xuw + r * c * (long long)d + k;
+  const double* xl_p = xlw + r * c * (long long)d + k;
+  for (int i0 = 0; i0 < c; i0 += kIC) {
+    const int ni = min(kIC, c - i0);
+    __syncthreads();
+#pragma unroll
+    for (int ii = 0; ii < kIC; ++ii) {
+      const bool in = live && ii < ni;
+      su[ii][threadIdx.x] = in ? xu_p[(long long)(i0 + ii) * d] : 0.0;
+      sl[ii][threadIdx.x] = in ? xl_p[(long long)(i0 + ii) * d] : 0.0;
+    }
+    for (int e = threadIdx.x; e < kIC * JT; e += kXThreads) {
+      const int ii = e / JT, t = e % JT;
+      sw[ii][t] = ii < ni ? w[(long long)(i0 + ii) * o + j0 + t] : 0.0;
+    }
+    __syncthreads();
+    for (int ii = 0; ii < ni; ++ii) {
+      const double xu = su[ii][threadIdx.x], xl = sl[ii][threadIdx.x];
+      double wv[JT];
+#pragma unroll
+      for (int t = 0; t < JT; ++t) wv[t] = sw[ii][t];
+#pragma unroll
+      for (int t = 0; t < JT; ++t) {
+        if (wv[t] > 0.0) {  // wp = w, wn = 0
+          yu[t] += wv[t] * xu;
+          yl[t] += wv[t] * xl;
+        } else if (wv[t] < 0.0) {  // wp = 0, wn = w
+          un[t] += wv[t] * xl;
+          ln[t] += wv[t] * xu;
+        }
+      }
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int t = 0; t < JT; ++t) {
+    const long long rj = r * o + j0 + t;
+    yuw[rj * d + k] = yu[t] + un[t];
+    ylw[rj * d + k] = yl[t] + ln[t];
+  }
+}
+
 // propagate_affine biases: y_ub = (ub_pos + ub_neg) + b, y_lb likewise.
 __global__ void x_affine_bias_kernel(const double* __restrict__ xlb, const double* __restrict__ xub,
                                      const double* __restrict__ w, const double* __restrict__ bias,
@@ -99,6 +170,55 @@ __global__ void x_concretize_kernel(const double* __restrict__ lw, const double*
       const double a = fabs(u[k]);
       su = (su < a) ? a : su;
     }
+  }
+  lo[i] = lb[i] - eps * sl;
+  hi[i] = ub[i] + eps * su;
+}
+
+// The same reduction with coalesced loads: a block of kXThreads neurons stages its rows
+// kCC columns at a time through shared memory (each warp loads whole column chunks of
+// consecutive rows), then every thread continues its own row's sum in order k = 0..d-1.
+constexpr int kCC = 16;
+__global__ void __launch_bounds__(kXThreads) x_concretize_staged_kernel(
+    const double* __restrict__ lw, const double* __restrict__ lb, const double* __restrict__ uw,
+    const double* __restrict__ ub, long long n, int d, int q, double eps, double* __restrict__ lo,
+    double* __restrict__ hi) {
+  __shared__ double tl[kXThreads][kCC + 1], tu[kXThreads][kCC + 1];
+  const long long i0 = (long long)blockIdx.x * kXThreads;
+  const long long i = i0 + threadIdx.x;
+  double sl = 0.0, su = 0.0;
+  for (int k0 = 0; k0 < d; k0 += kCC) {
+    const int kw = min(kCC, d - k0);
+    for (int e = threadIdx.x; e < kXThreads * kCC; e += kXThreads) {
+      const int rr = e / kCC, cc = e % kCC;
+      const long long row = i0 + rr;
+      const bool in = row < n && cc < kw;
+      tl[rr][cc] = in ? lw[row * d + k0 + cc] : 0.0;
+      tu[rr][cc] = in ? uw[row * d + k0 + cc] : 0.0;
+    }
+    __syncthreads();
+    if (q == NORM_L1) {
+      for (int cc = 0; cc < kw; ++cc) sl += fabs(tl[threadIdx.x][cc]);
+      for (int cc = 0; cc < kw; ++cc) su += fabs(tu[threadIdx.x][cc]);
+    } else if (q == NORM_L2) {
+      for (int cc = 0; cc < kw; ++cc) sl += tl[threadIdx.x][cc] * tl[threadIdx.x][cc];
+      for (int cc = 0; cc < kw; ++cc) su += tu[threadIdx.x][cc] * tu[threadIdx.x][cc];
+    } else {
+      for (int cc = 0; cc < kw; ++cc) {
+        const double a = fabs(tl[threadIdx.x][cc]);
+        sl = (sl < a) ? a : sl;
+      }
+      for (int cc = 0; cc < kw; ++cc) {
+        const double a = fabs(tu[threadIdx.x][cc]);
+        su = (su < a) ? a : su;
+      }
+    }
+    __syncthreads();
+  }
+  if (i >= n) return;
+  if (q == NORM_L2) {
+    sl = sqrt(sl);
+    su = sqrt(su);
   }
   lo[i] = lb[i] - eps * sl;
   hi[i] = ub[i] + eps * su;
@@ -310,7 +430,11 @@ int launch_x_affine(const double* xlw, const double* xlb, const double* xuw, con
   int n = 0;
   if (rows * o <= 0) return 0;
   if (d > 0) {
-    x_affine_lam_kernel<<<row_blocks(rows * o, d), kXThreads, 0, st>>>(xlw, xuw, w, ylw, yuw, rows, c, o, d);
+    if (o % 8 == 0)
+      x_affine_lam_tiled_kernel<8><<<row_blocks(rows * (o / 8), d), kXThreads, 0, st>>>(xlw, xuw, w, ylw, yuw, rows,
+                                                                                         c, o, d);
+    else
+      x_affine_lam_kernel<<<row_blocks(rows * o, d), kXThreads, 0, st>>>(xlw, xuw, w, ylw, yuw, rows, c, o, d);
     ++n;
   }
   x_affine_bias_kernel<<<blocks_for(rows * o, 128), 128, 0, st>>>(xlb, xub, w, bias, ylb, yub, rows, c, o);
@@ -321,7 +445,10 @@ int launch_x_concretize(const double* lw, const double* lb, const double* uw, co
                         int d, int norm, double eps, double* lo, double* hi, cudaStream_t st) {
   const int q = norm == NORM_L1 ? NORM_LINF : (norm == NORM_L2 ? NORM_L2 : NORM_L1);  // dual (bounds.cpp:9-19)
   if (n <= 0) return 0;
-  x_concretize_kernel<<<blocks_for(n, 128), 128, 0, st>>>(lw, lb, uw, ub, n, d, q, eps, lo, hi);
+  if (d >= kCC)
+    x_concretize_staged_kernel<<<blocks_for(n, kXThreads), kXThreads, 0, st>>>(lw, lb, uw, ub, n, d, q, eps, lo, hi);
+  else
+    x_concretize_kernel<<<blocks_for(n, 128), 128, 0, st>>>(lw, lb, uw, ub, n, d, q, eps, lo, hi);
   return 1;
 }
 

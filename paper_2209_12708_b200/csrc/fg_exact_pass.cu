@@ -139,8 +139,8 @@ fg_status exact_pass(fg_ctx* ctx, const fg_config& c, const double* params, cons
   CK(cudaMemsetAsync(cur.lw.p, 0, sizeof(double) * L * E * D, ctx->stream));
   CK(cudaMemsetAsync(cur.uw.p, 0, sizeof(double) * L * E * D, ctx->stream));
   DBuf dx, dpos;
-  CK(dx.alloc(sizeof(double) * L * E));
-  CK(dpos.alloc(sizeof(int) * words));
+  CK(dx.alloc_async(sizeof(double) * L * E, ctx->stream));
+  CK(dpos.alloc_async(sizeof(int) * words, ctx->stream));
   CK(cudaMemcpyAsync(dx.p, x_host, sizeof(double) * L * E, cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(dpos.p, pos_host, sizeof(int) * words, cudaMemcpyHostToDevice, ctx->stream));
   x_bind_input_kernel<<<nblocks((long long)L * E, 256), 256, 0, ctx->stream>>>(
@@ -225,7 +225,7 @@ fg_status exact_pass(fg_ctx* ctx, const fg_config& c, const double* params, cons
   if (fg_status st = wk.dump(logits)) return st;
   // sink finiteness (graph.cpp:663-671) over lb, ub, lw, uw
   DBuf flag;
-  CK(flag.alloc(sizeof(int)));
+  CK(flag.alloc_async(sizeof(int), ctx->stream));
   CK(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx->stream));
   x_finite_kernel<<<1, 64, 0, ctx->stream>>>(logits.plb(), (long long)C, flag.as<int>());
   x_finite_kernel<<<1, 64, 0, ctx->stream>>>(logits.pub(), (long long)C, flag.as<int>());

@@ -43,37 +43,57 @@ inline fg_status fail(fg_ctx* ctx, fg_status code, const std::string& msg) {
   return code;
 }
 
-// RAII device allocation
+// RAII device allocation.  alloc(): cudaMalloc.  alloc_async(): stream-ordered from the
+// device's default memory pool (cudaMallocAsync / cudaFreeAsync on that stream): no device-wide
+// synchronisation on free, so the exact-mode paths (many short-lived f64 tensors) do not stall.
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+  bool pooled = false;
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), stream(o.stream), pooled(o.pooled) {
     o.p = nullptr;
     o.bytes = 0;
+    o.pooled = false;
   }
   DBuf& operator=(DBuf&& o) noexcept {
     if (this != &o) {
       reset();
       p = o.p;
       bytes = o.bytes;
+      stream = o.stream;
+      pooled = o.pooled;
       o.p = nullptr;
       o.bytes = 0;
+      o.pooled = false;
     }
     return *this;
   }
   ~DBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled) cudaFreeAsync(p, stream);
+      else cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
+    pooled = false;
   }
   cudaError_t alloc(size_t b) {
     reset();
     bytes = b ? b : 16;
     return cudaMalloc(&p, bytes);
+  }
+  cudaError_t alloc_async(size_t b, cudaStream_t st) {
+    reset();
+    bytes = b ? b : 16;
+    stream = st;
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    pooled = e == cudaSuccess;
+    return e;
   }
   template <class T>
   T* as() const {

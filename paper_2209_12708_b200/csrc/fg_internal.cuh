@@ -188,6 +188,8 @@ bool umma_tmap_wop(void* tm, const float* base, int K, int N, int P2, int P3, in
 // when given and M % 256 == 0 the CTA-pair (cta_group::2, M = 256) kernel runs.
 int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, LamGemm p, int bn,
                     cudaStream_t st, const void* tm2_whi = nullptr, const void* tm2_wlo = nullptr);
+// dense tcgen05 peak microbenchmark: kind 0 = kind::tf32, 1 = kind::f16 (bf16); returns CTAs launched
+int launch_mma_peak(int kind, int iters, cudaStream_t st);
 int launch_ref_affine_f64(const float* W, const float* X, long long x_cr, double* Y, int C, int O, int D,
                           long long rows, cudaStream_t st);
 

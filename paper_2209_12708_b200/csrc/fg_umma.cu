@@ -610,6 +610,82 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
   return -1;
 }
 
+// Dense tensor-pipe peak microbenchmark (fg_selftest_mma_peak; the roofline denominator of the
+// 3xTF32 GEMMs): one CTA per SM, one thread issuing back-to-back tcgen05.mma M=128 N=256 on
+// SMEM-resident operands (no loads), 4 K-steps per 128 B operand row, committed every 64 MMAs.
+// kind::tf32 (K = 8 per MMA) or kind::f16 with bf16 operands (K = 16 per MMA).
+template <int KIND>
+__global__ void __launch_bounds__(128, 1) mma_peak_kernel(int iters) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* a = smem;                 // 128 rows x 128 B
+  uint8_t* b = smem + 128 * 128;     // 256 rows x 128 B
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 384 * 128);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+  for (int i = threadIdx.x; i < 384 * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *slot;
+  if (threadIdx.x == 0) {
+    // D f32; A/B tf32 (kind::tf32: format 2) or bf16 (kind::f16: format 1); K-major; N = 256, M = 128
+    const uint32_t fmt = KIND == 0 ? 2u : 1u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(256 >> 3) << 17) |
+                           ((uint32_t)(128 >> 4) << 24);
+    uint32_t phase = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const uint64_t ad = kmajor_sw128_desc(smem_u32(a) + ks * 32), bd = kmajor_sw128_desc(smem_u32(b) + ks * 32);
+        if (KIND == 0)
+          umma_tf32(tmem, ad, bd, idesc, (it | ks) != 0);
+        else
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+              "l"(ad), "l"(bd), "r"(idesc), "r"((uint32_t)((it | ks) != 0)));
+      }
+      if ((it & 15) == 15 || it == iters - 1) {
+        umma_commit(bar);
+        mbar_wait(bar, phase);
+        phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
+int launch_mma_peak(int kind, int iters, cudaStream_t st) {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int bytes = 384 * 128 + 64 + 1024;
+  auto k0 = mma_peak_kernel<0>;
+  auto k1 = mma_peak_kernel<1>;
+  cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (kind == 0) k0<<<g_num_sms, 128, bytes, st>>>(iters);
+  else k1<<<g_num_sms, 128, bytes, st>>>(iters);
+  return g_num_sms;
+}
+
 // f64 reference of the affine plane GEMM for fg_selftest_affine (test facility, not on the pass).
 __global__ void ref_affine_f64_kernel(const float* A, const float* X, long long x_cr, double* Y, int C, int O,
                                       int D, long long rows) {

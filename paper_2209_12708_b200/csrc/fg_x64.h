@@ -40,10 +40,10 @@ struct XB {
 inline fg_status xb_alloc(fg_ctx* ctx, XB& b, size_t n, size_t d) {
   b.n = n;
   b.d = d;
-  CK(b.lw.alloc(sizeof(double) * n * d));
-  CK(b.uw.alloc(sizeof(double) * n * d));
-  CK(b.lb.alloc(sizeof(double) * n));
-  CK(b.ub.alloc(sizeof(double) * n));
+  CK(b.lw.alloc_async(sizeof(double) * n * d, ctx->stream));
+  CK(b.uw.alloc_async(sizeof(double) * n * d, ctx->stream));
+  CK(b.lb.alloc_async(sizeof(double) * n, ctx->stream));
+  CK(b.ub.alloc_async(sizeof(double) * n, ctx->stream));
   return FG_OK;
 }
 
@@ -86,8 +86,8 @@ inline fg_status x_status(fg_ctx* ctx, int* dstatus, const char* what) {
 
 // concretize on the device, result stays on the device
 inline fg_status x_conc(fg_ctx* ctx, const XB& x, int norm, double eps, DBuf& lo, DBuf& hi) {
-  CK(lo.alloc(sizeof(double) * x.n));
-  CK(hi.alloc(sizeof(double) * x.n));
+  CK(lo.alloc_async(sizeof(double) * x.n, ctx->stream));
+  CK(hi.alloc_async(sizeof(double) * x.n, ctx->stream));
   XL(launch_x_concretize(x.plw(), x.plb(), x.puw(), x.pub(), (long long)x.n, (int)x.d, norm, eps,
                          lo.as<double>(), hi.as<double>(), ctx->stream));
   return FG_OK;
@@ -97,8 +97,8 @@ inline fg_status x_conc(fg_ctx* ctx, const XB& x, int norm, double eps, DBuf& lo
 inline fg_status x_relax_compose(fg_ctx* ctx, int kind, const XB& x, const DBuf& lo, const DBuf& hi, XB& y,
                           const char* what) {
   DBuf lines, st;
-  CK(lines.alloc(sizeof(double) * 4 * x.n));
-  CK(st.alloc(sizeof(int)));
+  CK(lines.alloc_async(sizeof(double) * 4 * x.n, ctx->stream));
+  CK(st.alloc_async(sizeof(int), ctx->stream));
   XL(launch_fill_int(st.as<int>(), kStatusClear, 1, ctx->stream));
   double* l = lines.as<double>();
   XL(launch_relax(kind, lo.as<double>(), hi.as<double>(), (long long)x.n, l, l + x.n, l + 2 * x.n, l + 3 * x.n,

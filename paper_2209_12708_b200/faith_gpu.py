@@ -26,6 +26,8 @@ FG_OK, FG_EINVAL, FG_EDOMAIN, FG_ERANGE, FG_ERUNTIME, FG_ECUDA, FG_ENOMEM = rang
 NORM = {"l1": 0, "l2": 1, "linf": 2}
 RELAX = {"relu": 0, "tanh": 1, "silu": 2, "exp": 3, "recip": 4}
 DOT = {"similarity": 0, "weighted_values": 1}
+# ambiguity band of the decision-exact verdicts (FG_DEFAULT_KAPPA, include/faith_gpu.h)
+DEFAULT_KAPPA = 1e-5
 STATUS_NAME = {0: "ok", 1: "invalid_argument", 2: "domain_error", 3: "out_of_range", 4: "runtime_error",
                5: "cuda_error", 6: "out_of_memory"}
 
@@ -141,6 +143,7 @@ def load_library():
     L.fg_profile_pass.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_char_p, _dp, _ip, _ip]
     L.fg_selftest_affine.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _dp, _dp, _dp, _dp]
     L.fg_ctx_set_precision.argtypes = [vp, C.c_int]
+    L.fg_selftest_mma_peak.argtypes = [vp, C.c_int, C.c_int, _dp, _dp]
     L.fg_ctx_precision.argtypes = [vp]
     L.fg_dot_batched.argtypes = [vp, C.c_int, sz, sz, sz, sz, sz] + [_dp] * 8 + [C.c_int, C.c_double] + [_dp] * 4
     L.fg_softmax_axis.argtypes = [vp, sz, sz, sz, sz] + [_dp] * 4 + [C.c_int, C.c_double] + [_dp] * 4
@@ -230,6 +233,13 @@ class Context:
                 "ms_simt": float(out[3][0])}
 
     # ---- bounds.hpp ------------------------------------------------------------------
+    def mma_peak(self, kind: str = "tf32", iters: int = 20000) -> dict:
+        """fg_selftest_mma_peak: measured dense tcgen05 throughput (kind "tf32" or "bf16")."""
+        ms, tf = np.zeros(1), np.zeros(1)
+        self._check(self.lib.fg_selftest_mma_peak(self.handle, {"tf32": 0, "bf16": 1}[kind], iters, _d(ms), _d(tf)),
+                    "fg_selftest_mma_peak")
+        return {"ms": float(ms[0]), "tflops": float(tf[0])}
+
     def concretize(self, b, norm: str, eps: float):
         """faith::concretize (bounds.cpp:122-140) -> (lo, hi)."""
         b = _bounds(b)

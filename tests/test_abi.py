@@ -59,3 +59,10 @@ def test_check_robust_is_host_side_and_strict():
         F.Context.check_robust([0.4, 0.1], [0.6, 0.39], 2)
     with pytest.raises(F.InvalidArgument):
         F.Context.check_robust([0.4, 0.1], [0.6, 0.39], 0, -1.0)
+
+
+def test_default_kappa_matches_header():
+    import re
+    text = open(F.HEADER).read()
+    m = re.search(r"#define FG_DEFAULT_KAPPA\s+([0-9.eE+-]+)", text)
+    assert m and float(m.group(1)) == F.DEFAULT_KAPPA

@@ -163,3 +163,23 @@ def test_column_range_rules():
     with pytest.raises(ValueError):
         D.column_range(1536, 0, 16 * 7)
     assert D.reduce_op("l1") == "max" and D.reduce_op("l2") == "sum" and D.reduce_op("linf") == "sum"
+
+
+def test_bench_spawns_ranks_itself():
+    """`bench.py --gpus 2` outside torchrun re-launches itself under torch.distributed.run with two
+    ranks (here with --dry-run: gloo, no GPU work); rank 0 prints one JSON line for the job."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                           "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["config"]["global_batch"] == 128
+    # rank 1's first sentence block starts after rank 0's steps (disjoint, rank-major)
+    assert rec["max_first_sentence_over_ranks"] == (2 + 3) * 64

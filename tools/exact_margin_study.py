@@ -44,7 +44,7 @@ def margin_part(ctx, n):
     m.set_exact_resolve(0.0)
     r = m.maxeps(np.stack(xs), np.stack(ps), w.norm, w.eps_max, w.tol)
     preds = r["predicted"]
-    ratios, exact_ms, worst = [], [], None
+    ratios, signed, exact_ms, worst = [], [], [], None
     for s in range(n):
         e0 = float(r["eps"][s])
         if not np.isfinite(e0) or e0 <= 0:
@@ -68,6 +68,7 @@ def margin_part(ctx, n):
                 wd = (hi[0][t] - lo[0][t]) + (hi[0][j] - lo[0][j])
                 q = abs(m32 - m64) / wd if wd > 0 else 0.0
                 ratios.append(q)
+                signed.append((m32 - m64) / wd if wd > 0 else 0.0)
                 if worst is None or q > worst[0]:
                     worst = (q, s, eps, m32, m64, wd)
                 if (m32 > 0) != (m64 > 0):
@@ -75,7 +76,8 @@ def margin_part(ctx, n):
                           f"ratio {q:.3e}", flush=True)
     ratios = np.array(ratios)
     out = {"probes": int(ratios.size), "ratio_max": float(ratios.max()), "ratio_p99": float(np.quantile(ratios, 0.99)),
-           "ratio_median": float(np.median(ratios)), "worst": worst, "exact_ms_median": float(np.median(exact_ms)),
+           "ratio_median": float(np.median(ratios)), "signed_min": float(np.min(signed)),
+           "signed_max": float(np.max(signed)), "worst": worst, "exact_ms_median": float(np.median(exact_ms)),
            "exact_ms_max": float(np.max(exact_ms))}
     print("MARGIN", json.dumps(out), flush=True)
 
