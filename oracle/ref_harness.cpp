@@ -151,31 +151,50 @@ struct Walk {
   LinearBounds run(LinearBounds cur) {
     if (gate) gate();
     std::size_t L = s.length;
+    // Every value is released after its last consumer, as graph::evaluate does
+    // (graph.cpp:655-660), so the deep / wide shapes (c5) fit in host memory.
+    auto drop = [](LinearBounds& b) { b = LinearBounds(); };
     for (const md::LayerWeights& w : s.layers) {
-      LinearBounds q = rx::propagate_affine(cur, w.wq, &w.bq); dump(q);
-      LinearBounds k = rx::propagate_affine(cur, w.wk, &w.bk); dump(k);
-      LinearBounds v = rx::propagate_affine(cur, w.wv, &w.bv); dump(v);
-      LinearBounds scores = rx::propagate_dot_product(q, k, ps, rx::DotLayout::PairwiseSimilarity,
-                                                      s.num_heads);
-      dump(scores);
-      LinearBounds scaled =
-          rx::propagate_scale(scores, 1.0 / std::sqrt(static_cast<double>(s.head_dim())));
-      dump(scaled);
-      // expand_softmax (graph.cpp:209-244), evaluated node by node.
-      ConcreteBounds cs = concretize(scaled, ps);
-      LinearBounds e = rx::compose_elementwise(scaled, rx::relax_exp(cs)); dump(e);
-      LinearBounds sm = rx::propagate_sum_axis(e, 3); dump(sm);
-      ConcreteBounds css = concretize(sm, ps);
-      LinearBounds r = rx::compose_elementwise(sm, rx::relax_recip(css)); dump(r);
-      LinearBounds probs = rx::propagate_mul_broadcast(e, r, 3, ps); dump(probs);
+      LinearBounds v, probs;
+      {
+        LinearBounds q = rx::propagate_affine(cur, w.wq, &w.bq); dump(q);
+        LinearBounds k = rx::propagate_affine(cur, w.wk, &w.bk); dump(k);
+        v = rx::propagate_affine(cur, w.wv, &w.bv); dump(v);
+        LinearBounds scores = rx::propagate_dot_product(q, k, ps, rx::DotLayout::PairwiseSimilarity,
+                                                        s.num_heads);
+        dump(scores);
+        drop(q);
+        drop(k);
+        LinearBounds scaled =
+            rx::propagate_scale(scores, 1.0 / std::sqrt(static_cast<double>(s.head_dim())));
+        dump(scaled);
+        drop(scores);
+        // expand_softmax (graph.cpp:209-244), evaluated node by node.
+        ConcreteBounds cs = concretize(scaled, ps);
+        LinearBounds e = rx::compose_elementwise(scaled, rx::relax_exp(cs)); dump(e);
+        drop(scaled);
+        LinearBounds sm = rx::propagate_sum_axis(e, 3); dump(sm);
+        ConcreteBounds css = concretize(sm, ps);
+        LinearBounds r = rx::compose_elementwise(sm, rx::relax_recip(css)); dump(r);
+        probs = rx::propagate_mul_broadcast(e, r, 3, ps); dump(probs);
+      }
       LinearBounds ctx = rx::propagate_dot_product(probs, v, ps, rx::DotLayout::WeightedValues,
                                                    s.num_heads);
       dump(ctx);
+      drop(probs);
+      drop(v);
       LinearBounds attn = rx::propagate_affine(ctx, w.wo, &w.bo); dump(attn);
+      drop(ctx);
       LinearBounds res1 = rx::propagate_add(cur, attn); dump(res1);
-      LinearBounds f1 = rx::propagate_affine(res1, w.w1, &w.b1); dump(f1);
-      LinearBounds act = elementwise(f1, s.activation); dump(act);
+      drop(cur);
+      drop(attn);
+      LinearBounds act;
+      {
+        LinearBounds f1 = rx::propagate_affine(res1, w.w1, &w.b1); dump(f1);
+        act = elementwise(f1, s.activation); dump(act);
+      }
       LinearBounds f2 = rx::propagate_affine(act, w.w2, &w.b2); dump(f2);
+      drop(act);
       cur = rx::propagate_add(res1, f2); dump(cur);
     }
     LinearBounds pooled = rx::propagate_scale(rx::propagate_sum_axis(cur, 1),
@@ -529,7 +548,7 @@ struct fo_paced {
   std::mutex mu;
   std::condition_variable cv;
   int allowed = 0, done = 0;  // gates the walk may pass / has passed (one before every node)
-  bool at_gate = false, finished = false;
+  bool at_gate = false, finished = false, cancel = false;
   int status = FO_OK;
   std::vector<double> lo, hi;
   std::thread th;
@@ -551,14 +570,19 @@ fo_paced* fo_paced_begin(const fo_config* c, const double* params, const double*
         std::unique_lock<std::mutex> lk(p->mu);
         p->at_gate = true;
         p->cv.notify_all();
-        p->cv.wait(lk, [p] { return p->done < p->allowed; });
+        p->cv.wait(lk, [p] { return p->cancel || p->done < p->allowed; });
         p->at_gate = false;
+        if (p->cancel) throw StopWalk{};
         ++p->done;
       };
-      LinearBounds out = walk.run(word_input(s, xv.data(), pv.data(), words));
-      ConcreteBounds cb = concretize(out, walk.ps);
-      std::copy(cb.lo.data(), cb.lo.data() + cb.lo.numel(), p->lo.begin());
-      std::copy(cb.hi.data(), cb.hi.data() + cb.hi.numel(), p->hi.begin());
+      try {
+        LinearBounds out = walk.run(word_input(s, xv.data(), pv.data(), words));
+        ConcreteBounds cb = concretize(out, walk.ps);
+        std::copy(cb.lo.data(), cb.lo.data() + cb.lo.numel(), p->lo.begin());
+        std::copy(cb.hi.data(), cb.hi.data() + cb.hi.numel(), p->hi.begin());
+      } catch (const StopWalk&) {
+        throw std::runtime_error("paced walk cancelled");
+      }
     });
     std::lock_guard<std::mutex> lk(p->mu);
     p->status = st;
@@ -587,10 +611,13 @@ int fo_paced_step(fo_paced** walks, int n, int nodes) {
   return fin;
 }
 
-int fo_paced_end(fo_paced* p, double* logits_lo, double* logits_hi) {
+// Lets the walk run to completion (finish != 0) or stops it at its next node (finish == 0:
+// status FO_ERUNTIME); joins the thread and returns the walk's status.
+int fo_paced_end(fo_paced* p, int finish, double* logits_lo, double* logits_hi) {
   {
     std::lock_guard<std::mutex> lk(p->mu);
     p->allowed = 1 << 30;
+    p->cancel = finish == 0;
     p->cv.notify_all();
   }
   p->th.join();

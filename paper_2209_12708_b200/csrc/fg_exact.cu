@@ -280,6 +280,25 @@ struct XOps {  // device pointers of two operands, their concretizations and the
 };
 
 // propagate_dot_product (relax.cpp:573-654), batch b: thread = (output neuron, column k).
+// Λ part of one McCormick term (x_term's row additions) with the operand rows already loaded:
+// the same additions in the same order, with the "skip when the coefficient is 0" of
+// relax.cpp:545-566 as a select, so all loads can be issued before any coefficient is known.
+__device__ __forceinline__ void x_term_rows(double lx, double ly, double uy, double xl, double xu, double yl,
+                                            double yu, double& olw, double& ouw) {
+  const double a = ly * ((ly >= 0.0) ? xl : xu);  // lower plane: cx = ly, cy = lx
+  olw = (ly != 0.0) ? olw + a : olw;
+  const double b = lx * ((lx >= 0.0) ? yl : yu);
+  olw = (lx != 0.0) ? olw + b : olw;
+  const double c = uy * ((uy >= 0.0) ? xu : xl);  // upper plane: cx = uy, cy = lx
+  ouw = (uy != 0.0) ? ouw + c : ouw;
+  const double e = lx * ((lx >= 0.0) ? yu : yl);
+  ouw = (lx != 0.0) ? ouw + e : ouw;
+}
+
+// propagate_dot_product (relax.cpp:573-654): thread = (output neuron, column k); the k == 0
+// thread of each output also accumulates the biases (in a second loop: same per-output order).
+// Both candidate rows of every operand are loaded unconditionally and the term loop is unrolled,
+// so the row loads of several terms are in flight together.
 __global__ void x_dot_kernel(XOps p, int layout, long long batch, int len, int e, int heads, int d) {
   const int kb = d > 0 ? (d + kXThreads - 1) / kXThreads : 1;
   const long long oidx = blockIdx.x / kb;
@@ -291,37 +310,49 @@ __global__ void x_dot_kernel(XOps p, int layout, long long batch, int len, int e
   const bool bias = kk == 0;
   const int k = kk < d ? kk : -1;
   if (k < 0 && !bias) return;
-  double olb = 0.0, oub = 0.0, olw = 0.0, ouw = 0.0;
+  // term t: x row xi0 + t*xs, y row yi0 + t*ys
+  long long xi0, yi0, xs, ys;
+  int nt;
   if (sim) {  // scores[b, h, i, j] = sum_t q[b, i, h*hd + t] k[b, j, h*hd + t]
     const int j = (int)(oidx % len);
     const int i = (int)((oidx / len) % len);
     const int h = (int)((oidx / ((long long)len * len)) % heads);
     const long long bi = oidx / ((long long)heads * len * len);
-    for (int t = 0; t < hd; ++t) {
-      const long long xi = (bi * len + i) * e + (long long)h * hd + t;
-      const long long yi = (bi * len + j) * e + (long long)h * hd + t;
-      x_term(p.alw, p.alb, p.auw, p.aub, p.blw, p.blb, p.buw, p.bub, xi, yi, p.alo[xi], p.blo[yi], p.bhi[yi],
-             d, k, bias, olb, oub, olw, ouw);
-    }
+    xi0 = (bi * len + i) * e + (long long)h * hd;
+    yi0 = (bi * len + j) * e + (long long)h * hd;
+    xs = ys = 1;
+    nt = hd;
   } else {  // ctx[b, i, h*hd + t] = sum_j s[b, h, i, j] v[b, j, h*hd + t]
     const int f = (int)(oidx % e);
     const int i = (int)((oidx / e) % len);
     const long long bi = oidx / ((long long)len * e);
     const int h = f / hd;
-    for (int j = 0; j < len; ++j) {
-      const long long xi = ((bi * heads + h) * len + i) * len + j;
-      const long long yi = (bi * len + j) * e + f;
-      x_term(p.alw, p.alb, p.auw, p.aub, p.blw, p.blb, p.buw, p.bub, xi, yi, p.alo[xi], p.blo[yi], p.bhi[yi],
-             d, k, bias, olb, oub, olw, ouw);
-    }
-  }
-  if (bias) {
-    p.ylb[oidx] = olb;
-    p.yub[oidx] = oub;
+    xi0 = ((bi * heads + h) * len + i) * len;
+    yi0 = (bi * len) * e + f;
+    xs = 1;
+    ys = e;
+    nt = len;
   }
   if (k >= 0) {
+    double olw = 0.0, ouw = 0.0;
+#pragma unroll 4
+    for (int t = 0; t < nt; ++t) {
+      const long long xi = xi0 + t * xs, yi = yi0 + t * ys;
+      x_term_rows(p.alo[xi], p.blo[yi], p.bhi[yi], p.alw[xi * d + k], p.auw[xi * d + k], p.blw[yi * d + k],
+                  p.buw[yi * d + k], olw, ouw);
+    }
     p.ylw[oidx * d + k] = olw;
     p.yuw[oidx * d + k] = ouw;
+  }
+  if (bias) {
+    double olb = 0.0, oub = 0.0, dl = 0.0, du = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      const long long xi = xi0 + t * xs, yi = yi0 + t * ys;
+      x_term(p.alw, p.alb, p.auw, p.aub, p.blw, p.blb, p.buw, p.bub, xi, yi, p.alo[xi], p.blo[yi], p.bhi[yi], d,
+             -1, true, olb, oub, dl, du);
+    }
+    p.ylb[oidx] = olb;
+    p.yub[oidx] = oub;
   }
 }
 

@@ -267,6 +267,8 @@ bool umma_affine_enabled() {
 // Λ bound GEMM of one affine over `rows` token rows: tcgen05 3xTF32 when the shape and
 // the input tensor map allow it, the FP32 SIMT kernel otherwise.
 // tcgen05 descriptor of the affine: batch (token row, plane); Λ map (d, C, rows, 2).
+constexpr double kTruncPerMma = 0.57;  // mean relative shortening per accumulating MMA, units of 2^-24
+
 LamGemm affine_lam(const DevAffine& a, float* out, long long out_cr, const float* res, long long res_cr,
                    long long rows, int D) {
   LamGemm g{};
@@ -281,6 +283,12 @@ LamGemm affine_lam(const DevAffine& a, float* out, long long out_cr, const float
   g.res = res;
   g.res_c[0] = (long long)a.O * D; g.res_c[1] = res_cr; g.ldn_res = D;
   g.alpha = 1.0f;
+  // Radius plane r' = |W| r: a sum of non-negative products, which tcgen05's accumulation (it
+  // truncates toward zero at every MMA instruction) shortens by a near-constant fraction --
+  // measured 0.57 * 2^-24 per accumulating MMA (3 per 8-deep K step in 3xTF32; c3 W1: -3.3e-6
+  // relative, tools/error_by_node.py).  The epilogue scales it back by that expected amount.
+  g.alpha_r_dim1 = 2;  // b[1] = plane (0 = centre, 1 = radius)
+  g.alpha_r = (float)(1.0 + kTruncPerMma * (3.0 * a.C / 8.0) * 0x1p-24);
   return g;
 }
 

@@ -170,6 +170,10 @@ struct LamGemm {
   float* out;
   const float* res;
   float alpha;
+  // tiles whose batch coordinate b[alpha_r_dim1 - 1] == 1 (the radius plane of an affine) are
+  // scaled by alpha_r instead of alpha; alpha_r_dim1 = 0 (zero-initialised LamGemm): alpha everywhere
+  int alpha_r_dim1;
+  float alpha_r;
   int accumulate;
   int tiles_m, tiles_n, num_tiles;  // set by launch_lam_gemm
   int epi_groups;                   // epilogue warp groups draining tiles (1 or 2; launch_lam_gemm)

@@ -421,8 +421,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
         float* oc = chunk_out(c);
         float o[32];
+        const float al = (p.alpha_r_dim1 > 0 && b[p.alpha_r_dim1 - 1] == 1) ? p.alpha_r : p.alpha;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) o[j] = p.alpha * __uint_as_float(v[j]);
+        for (int j = 0; j < 32; ++j) o[j] = al * __uint_as_float(v[j]);
         if (has_x) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) o[j] += xv[j];

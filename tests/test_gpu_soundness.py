@@ -1,7 +1,8 @@
 """Size-independent properties of the fused pass at the BASELINE configs' full sizes, checked with
 the GPU f64 forward (fg_forward_batch) as the oracle of the exact function:
-  * soundness: logits of sampled perturbed inputs (word-level ε-ball, helpers.sample_in_ball =
-    proj/tests/helpers.hpp:16-54) lie inside the GPU bounds (slack 1e-6*max(1,|v|); f32 Λ);
+  * soundness: logits of 10^4 sampled perturbed inputs per case (word-level ε-ball,
+    helpers.sample_in_ball = proj/tests/helpers.hpp:16-54, a quarter on the sphere) lie inside
+    the GPU bounds with the reference's own slack 1e-7*max(1,|v|) (acceptance.cpp:97);
   * exactness at ε = 0: the bounds collapse onto the exact forward (acceptance.cpp:111-131);
   * the GPU forward equals the host forward (model.cpp:487-571) to 1e-12."""
 import numpy as np
@@ -38,7 +39,7 @@ def test_gpu_forward_equals_host_forward(name):
 # the random-init model's forward-mode bounds are finite (exp overflow, EDOMAIN) yet not
 # degenerate at f64 resolution (lo > hi from the cancelling chords, EINVAL) -- the reference's
 # algorithm certifies only eps = 0 there; its eps = 0 collapse is checked below.
-@pytest.mark.parametrize("name,samples", [("c2", 2000), ("c3", 2000), ("c4", 600)])
+@pytest.mark.parametrize("name,samples", [("c2", 10_000), ("c3", 10_000), ("c4", 10_000)])
 def test_sampled_soundness_full_size(name, samples):
     w, cfg, m = _model(name)
     rng = np.random.default_rng(11)
@@ -56,11 +57,15 @@ def test_sampled_soundness_full_size(name, samples):
         assert st[0] == 0
         assert np.all(hi[0] - lo[0] > 0)
         deltas = sample_in_ball(rng, w.norm, eps, w.words * E, samples)
-        xp = np.repeat(x.reshape(1, cfg.length, E), samples, axis=0)
-        for wi, p in enumerate(pos):
-            xp[:, p, :] += deltas[:, wi * E:(wi + 1) * E]
-        logits = m.forward_batch(xp.reshape(samples, -1))
-        slack = 1e-6 * np.maximum(1.0, np.abs(logits))
+        chunks = []
+        for i in range(0, samples, 1000):  # bounded host memory at c4 (L*E = 65536 doubles per input)
+            d = deltas[i:i + 1000]
+            xp = np.repeat(x.reshape(1, cfg.length, E), len(d), axis=0)
+            for wi, p in enumerate(pos):
+                xp[:, p, :] += d[:, wi * E:(wi + 1) * E]
+            chunks.append(m.forward_batch(xp.reshape(len(d), -1)))
+        logits = np.concatenate(chunks)
+        slack = 1e-7 * np.maximum(1.0, np.abs(logits))
         below = np.max(lo[0] - logits - slack)
         above = np.max(logits - hi[0] - slack)
         assert below <= 0.0 and above <= 0.0, (name, s, below, above)
