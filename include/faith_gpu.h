@@ -216,13 +216,12 @@ fg_status fg_bound_pass_exact(fg_model* model, const double* x, const int* posit
 /* Decision-exact verdicts.  fg_certify, fg_maxeps and fg_maxeps_spec decide every probe with
  * check_robust on the fused f32-Λ pass; a probe is AMBIGUOUS when for some class j != t its
  * margin m = lo_t - hi_j - margin lies in the error band of that pass,
- *   -kappa/10 * W - f <= m <= kappa * W + f,   W = (hi_t - lo_t) + (hi_j - lo_j),
+ *   -kappa * W - f <= m <= kappa / 8 * W + f,   W = (hi_t - lo_t) + (hi_j - lo_j),
  *   f = 1e-11 * max(1, |lo_t|, |hi_j|)
- * (one-sided: the fused pass's tcgen05 accumulation truncates toward zero, so its widths come
- * out slightly small and its margins large; measured (m_f32 - m_exact) / W in [+8.2e-7, +5.1e-6]
- * at c3).  Ambiguous probes are re-decided by fg_bound_pass_exact, so
- * every verdict is the reference's.  kappa = 0 turns the re-decision off (raw f32 verdicts). */
-#define FG_DEFAULT_KAPPA 1e-5
+ * (asymmetric like the measured error (m_f32 - m_exact) / W: [-1.7e-6, +1.9e-7] at c3,
+ * DESIGN.md section 6).  Ambiguous probes are re-decided by fg_bound_pass_exact, so every
+ * verdict is the reference's.  kappa = 0 turns the re-decision off (raw f32 verdicts). */
+#define FG_DEFAULT_KAPPA 4.5e-6
 fg_status fg_model_set_exact_resolve(fg_model* model, double kappa);
 
 /* certify(sentence, p, eps) -- cmd_verify (cli.cpp:64-133) for S sentences:
@@ -306,9 +305,10 @@ fg_status fg_profile_pass(fg_model* model, int norm, double eps, int max_sites, 
 /* Self-test of the affine bound GEMM (propagate_affine's Λ contraction) on random data:
  * tcgen05 3xTF32 kernel and FP32 SIMT kernel vs an f64 device reference.  err_* =
  * max|Y - Y_ref| / max|Y_ref| (err_umma = -1 if the shape is not tcgen05-eligible:
- * O % 128, C % 32, D % 128); ms_* = CUDA-event time of one launch. */
+ * O % 128, C % 32, D % 128); ms_* = CUDA-event time of one launch; bias_umma[2] (may be NULL) =
+ * median signed relative error of the tcgen05 centre / radius planes (radius inputs >= 0). */
 fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_t seed, double* err_umma,
-                             double* err_simt, double* ms_umma, double* ms_simt);
+                             double* err_simt, double* ms_umma, double* ms_simt, double* bias_umma);
 
 /* Dense tensor-pipe peak on this device (the roofline denominator of the 3xTF32 GEMMs): one CTA
  * per SM issuing tcgen05.mma M=128 N=256 back to back on SMEM-resident operands, `iters` x 4

@@ -27,7 +27,7 @@ NORM = {"l1": 0, "l2": 1, "linf": 2}
 RELAX = {"relu": 0, "tanh": 1, "silu": 2, "exp": 3, "recip": 4}
 DOT = {"similarity": 0, "weighted_values": 1}
 # ambiguity band of the decision-exact verdicts (FG_DEFAULT_KAPPA, include/faith_gpu.h)
-DEFAULT_KAPPA = 1e-5
+DEFAULT_KAPPA = 4.5e-6
 STATUS_NAME = {0: "ok", 1: "invalid_argument", 2: "domain_error", 3: "out_of_range", 4: "runtime_error",
                5: "cuda_error", 6: "out_of_memory"}
 
@@ -141,7 +141,7 @@ def load_library():
     L.fg_gen_input.argtypes = [C.POINTER(FgConfig), C.c_uint64, _dp]
     L.fg_gen_positions.argtypes = [C.c_uint64, C.c_int, C.c_int, _ip]
     L.fg_profile_pass.argtypes = [vp, C.c_int, C.c_double, C.c_int, C.c_char_p, _dp, _ip, _ip]
-    L.fg_selftest_affine.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _dp, _dp, _dp, _dp]
+    L.fg_selftest_affine.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, _dp, _dp, _dp, _dp, _dp]
     L.fg_ctx_set_precision.argtypes = [vp, C.c_int]
     L.fg_selftest_mma_peak.argtypes = [vp, C.c_int, C.c_int, _dp, _dp]
     L.fg_ctx_precision.argtypes = [vp]
@@ -226,11 +226,12 @@ class Context:
 
     def selftest_affine(self, rows: int, c: int, o: int, d: int, seed: int = 1) -> dict:
         """tcgen05 3xTF32 and FP32 SIMT affine GEMMs vs an f64 reference (fg_selftest_affine)."""
-        out = [np.zeros(1) for _ in range(4)]
+        out = [np.zeros(1) for _ in range(4)] + [np.zeros(2)]
         self._check(self.lib.fg_selftest_affine(self.handle, rows, c, o, d, seed, *map(_d, out)),
                     "fg_selftest_affine")
         return {"err_umma": float(out[0][0]), "err_simt": float(out[1][0]), "ms_umma": float(out[2][0]),
-                "ms_simt": float(out[3][0])}
+                "ms_simt": float(out[3][0]), "bias_umma_centre": float(out[4][0]),
+                "bias_umma_radius": float(out[4][1])}
 
     # ---- bounds.hpp ------------------------------------------------------------------
     def mma_peak(self, kind: str = "tf32", iters: int = 20000) -> dict:

@@ -9,7 +9,7 @@
    the deep configs' candidate golden radii.
 3. cost: exact-pass time per sentence; maxeps with and without the exact re-decision.
 
-  python tools/exact_margin_study.py [--sentences 24] [--parts margin,nodes,maxeps]
+  python tools/exact_margin_study.py [--sentences 24] [--parts margin,nodes,maxeps] [--configs c1,c2,c3]
 """
 import argparse
 import json
@@ -38,8 +38,8 @@ def sent(w, cfg, s):
     return F.gen_input(cfg, w.input_seed(s)), F.gen_positions(w.position_seed(s), w.length, w.words)
 
 
-def margin_part(ctx, n):
-    w, cfg, m = load(ctx, "c3")
+def margin_part(ctx, n, name="c3"):
+    w, cfg, m = load(ctx, name)
     xs, ps = zip(*[sent(w, cfg, s) for s in range(n)])
     m.set_exact_resolve(0.0)
     r = m.maxeps(np.stack(xs), np.stack(ps), w.norm, w.eps_max, w.tol)
@@ -79,7 +79,7 @@ def margin_part(ctx, n):
            "ratio_median": float(np.median(ratios)), "signed_min": float(np.min(signed)),
            "signed_max": float(np.max(signed)), "worst": worst, "exact_ms_median": float(np.median(exact_ms)),
            "exact_ms_max": float(np.max(exact_ms))}
-    print("MARGIN", json.dumps(out), flush=True)
+    print("MARGIN", name, json.dumps(out), flush=True)
 
 
 def nodes_part(ctx):
@@ -134,13 +134,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sentences", type=int, default=24)
     ap.add_argument("--parts", default="nodes,margin,maxeps")
+    ap.add_argument("--configs", default="c3")
     a = ap.parse_args()
     ctx = F.Context(0)
     parts = a.parts.split(",")
     if "nodes" in parts:
         nodes_part(ctx)
     if "margin" in parts:
-        margin_part(ctx, a.sentences)
+        for name in a.configs.split(","):
+            margin_part(ctx, a.sentences, name)
     if "maxeps" in parts:
         maxeps_part(ctx, 64)
 
