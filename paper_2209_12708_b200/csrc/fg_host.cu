@@ -356,11 +356,11 @@ fg_status fg_ctx_create(int device, fg_ctx** out) {
     return FG_ECUDA;
   }
   // The exact-mode paths allocate their f64 tensors stream-ordered from the default pool
-  // (DBuf::alloc_async); keep up to 4 GiB cached across calls instead of returning it at every
-  // synchronisation.
+  // (DBuf::alloc_async); the pool keeps what it has mapped across calls instead of returning
+  // it to the driver at every synchronisation (re-mapping GBs per exact pass cost 100s of ms).
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t keep = 4ull << 30;
+    uint64_t keep = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   *out = ctx;

@@ -598,9 +598,9 @@ __global__ void __launch_bounds__(kBiasCols) affine_bias_kernel(
   __shared__ double2 xs[kBiasRows][kBiasChunk];  // (lb, ub) of the CTA's rows
   const int j = blockIdx.x * kBiasCols + threadIdx.x;
   const long long r0 = (long long)blockIdx.y * kBiasRows;
-  double ub_pos[kBiasRows], ub_neg[kBiasRows], lb_pos[kBiasRows], lb_neg[kBiasRows];
+  double ub_acc[kBiasRows], lb_acc[kBiasRows];
 #pragma unroll
-  for (int r = 0; r < kBiasRows; ++r) ub_pos[r] = ub_neg[r] = lb_pos[r] = lb_neg[r] = 0.0;
+  for (int r = 0; r < kBiasRows; ++r) ub_acc[r] = lb_acc[r] = 0.0;
   for (int i0 = 0; i0 < C; i0 += kBiasChunk) {
     const int n = min(kBiasChunk, C - i0);
     __syncthreads();
@@ -612,20 +612,19 @@ __global__ void __launch_bounds__(kBiasCols) affine_bias_kernel(
     }
     __syncthreads();
     if (j < O) {
-      // i ascending per (row, j): the reference's accumulation order (relax.cpp:280-287);
-      // unrolled so several weight loads are in flight per thread
+      // sign-selected operand, one f64 FMA per bound: y_ub += w * (w > 0 ? ub : lb),
+      // y_lb += w * (w > 0 ? lb : ub) -- the sum of relax.cpp:280-287 (whose four separate
+      // sign-half sums the exact mode, fg_exact.cu, keeps bit for bit) at a quarter of the FP64
+      // instructions; unrolled so several weight loads are in flight per thread
 #pragma unroll 8
       for (int i = 0; i < n; ++i) {
         const double wv = w[(long long)(i0 + i) * O + j];
-        const double wp = (wv < 0.0) ? 0.0 : wv;
-        const double wn = (0.0 < wv) ? 0.0 : wv;
+        const bool pos = wv > 0.0;
 #pragma unroll
         for (int r = 0; r < kBiasRows; ++r) {
           const double2 x = xs[r][i];
-          ub_pos[r] += wp * x.y;
-          ub_neg[r] += wn * x.x;
-          lb_pos[r] += wp * x.x;
-          lb_neg[r] += wn * x.y;
+          ub_acc[r] = __fma_rn(wv, pos ? x.y : x.x, ub_acc[r]);
+          lb_acc[r] = __fma_rn(wv, pos ? x.x : x.y, lb_acc[r]);
         }
       }
     }
@@ -637,8 +636,8 @@ __global__ void __launch_bounds__(kBiasCols) affine_bias_kernel(
     const long long row = r0 + r;
     if (row >= nrows) break;
     const long long t = row * O + j;
-    double yub = ub_pos[r] + ub_neg[r] + bv;
-    double ylb = lb_pos[r] + lb_neg[r] + bv;
+    double yub = ub_acc[r] + bv;
+    double ylb = lb_acc[r] + bv;
     if (res_lb) {  // propagate_add(res, y) (relax.cpp:666-667)
       yub = res_ub[t] + yub;
       ylb = res_lb[t] + ylb;
