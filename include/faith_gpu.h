@@ -218,10 +218,10 @@ fg_status fg_bound_pass_exact(fg_model* model, const double* x, const int* posit
  * margin m = lo_t - hi_j - margin lies in the error band of that pass,
  *   -kappa * W - f <= m <= kappa / 8 * W + f,   W = (hi_t - lo_t) + (hi_j - lo_j),
  *   f = 1e-11 * max(1, |lo_t|, |hi_j|)
- * (asymmetric like the measured error (m_f32 - m_exact) / W: [-1.7e-6, +1.9e-7] at c3,
- * DESIGN.md section 6).  Ambiguous probes are re-decided by fg_bound_pass_exact, so every
+ * (asymmetric like the measured error (m_f32 - m_exact) / W: [-3.0e-6, -7.5e-7] at c3,
+ * [-1.3e-6, -8.9e-7] at c2 -- the fused pass is conservative -- DESIGN.md section 6).  Ambiguous probes are re-decided by fg_bound_pass_exact, so every
  * verdict is the reference's.  kappa = 0 turns the re-decision off (raw f32 verdicts). */
-#define FG_DEFAULT_KAPPA 4.5e-6
+#define FG_DEFAULT_KAPPA 6e-6
 fg_status fg_model_set_exact_resolve(fg_model* model, double kappa);
 
 /* certify(sentence, p, eps) -- cmd_verify (cli.cpp:64-133) for S sentences:

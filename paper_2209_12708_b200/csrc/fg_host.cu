@@ -1366,9 +1366,11 @@ int default_slots(const fg_model* m, int S, int D) {
 // bound through ε·‖Λ‖ and the envelope lines built from it) plus an f64 rounding floor.  The
 // band is asymmetric because the error is: measured (m_f32 - m_exact) / W over 576 probes per
 // config straddling each sentence's ε* (tools/exact_margin_study.py) lies in
-// [-1.7e-6, +1.9e-7] at c3, [-2.5e-7, -5.4e-8] at c2, +-7.7e-9 at c1 (FP32 SIMT), so a probe is
-// ambiguous when  -kappa * W - f <= m <= kappa / 8 * W + f  (kappa = 4.5e-6: 2.6x / 3x the
-// extremes).  Such a probe is re-decided by the exact pass, whose arithmetic is the reference's.
+// [-3.0e-6, -7.5e-7] at c3, [-1.3e-6, -8.9e-7] at c2 (the truncation compensation of the
+// affine GEMMs and the 2^-20 norm pad make the fused pass conservative) and +-7.7e-9 at c1
+// (FP32 SIMT), so a probe is ambiguous when  -kappa * W - f <= m <= kappa / 8 * W + f
+// (kappa = 6e-6: 2x the extreme).  Such a probe is re-decided by the exact pass, whose
+// arithmetic is the reference's.
 bool ambiguous_verdict(const double* lo, const double* hi, int C, int t, double margin, double kappa) {
   if (!(kappa > 0.0)) return false;
   for (int j = 0; j < C; ++j) {

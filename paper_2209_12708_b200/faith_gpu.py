@@ -27,7 +27,7 @@ NORM = {"l1": 0, "l2": 1, "linf": 2}
 RELAX = {"relu": 0, "tanh": 1, "silu": 2, "exp": 3, "recip": 4}
 DOT = {"similarity": 0, "weighted_values": 1}
 # ambiguity band of the decision-exact verdicts (FG_DEFAULT_KAPPA, include/faith_gpu.h)
-DEFAULT_KAPPA = 4.5e-6
+DEFAULT_KAPPA = 6e-6
 STATUS_NAME = {0: "ok", 1: "invalid_argument", 2: "domain_error", 3: "out_of_range", 4: "runtime_error",
                5: "cuda_error", 6: "out_of_memory"}
 
