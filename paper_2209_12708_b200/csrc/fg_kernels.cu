@@ -832,15 +832,11 @@ void wv_bias(const NView& pv, const NView& v, const NView& out, int S, int H, in
 
 // ---------------------------------------------------------------------------
 // Softmax chain (graph.cpp:237-240 -> relax.cpp:363-394, 705-742, 396-424, 744-775),
-// one CTA per (sentence, score row), in place:
-//   phase 1: per key j (warp per row): norms -> exp envelope -> e bounds/norms;
-//   phase 2: column-owned sums  Σ_j e_j  -> norms -> recip envelope -> r;
-//   phase 3: McCormick e_j * r written back as probs, with probs lo/hi.
-// Scores Λ is read twice (the second read of the CTA's own rows hits L2) and
-// written once.
+// per (sentence, score row), in place: exp envelope per key -> Σ_j e_j -> recip envelope ->
+// McCormick e_j * r written back as probs with their lo/hi.  Kernels: softmax2 (general D),
+// softmax3 (D split over a CTA cluster), softmax4 / softmax5 / softmax6 (streaming at full
+// width; launch_softmax picks by shape).
 // ---------------------------------------------------------------------------
-constexpr int kSmThreads = 256;
-constexpr int kSmGroup = 8;  // rows reduced together in phase 3
 
 template <int Q>
 __device__ __forceinline__ double block_reduce(double v, double* scratch) {
@@ -2355,223 +2351,6 @@ int softmax3_cluster(int n, int D, int nbuf, int tile_kb) {
   return best;
 }
 
-template <int Q, int CH>
-__global__ void __launch_bounds__(kSmThreads) softmax_kernel(NView sc, int rows_per_s, int n, int D,
-                                                             const double* __restrict__ eps,
-                                                             int* __restrict__ status, int site_exp,
-                                                             int site_recip) {
-  extern __shared__ double sm[];
-  double* a_lo = sm;
-  double* a_up = sm + n;
-  double* e_lb = sm + 2 * n;
-  double* e_ub = sm + 3 * n;
-  double* e_lo = sm + 4 * n;
-  double* e_hi = sm + 5 * n;
-  double* red = sm + 6 * n;              // 32 doubles
-  double* grp = red + 32;                // [nwarps][2*kSmGroup]
-  double* scal = grp + 8 * 2 * kSmGroup;  // scalars
-
-  const int s = blockIdx.x / rows_per_s;
-  const int row = blockIdx.x % rows_per_s;
-  const long long nb = (long long)s * sc.s_stride + (long long)row * n;  // first neuron
-  float* cb = sc.lam + nb * D;
-  float* rb = cb + sc.cr;
-  const double e = eps[s];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-
-  // ---- phase 1: exp envelope per key (ExpVerify node)
-  int err_exp = 0;
-  for (int j = warp; j < n; j += nwarps) {
-    NormAcc<Q> acc;
-    const float* c = cb + (long long)j * D;
-    const float* r = rb + (long long)j * D;
-    for (int d = lane * 4; d < D; d += 128)
-      acc.add4(*reinterpret_cast<const float4*>(c + d), *reinterpret_cast<const float4*>(r + d));
-    acc.warp_reduce();
-    if (lane == 0) {
-      double nl = acc.fin(acc.l), nu = acc.fin(acc.u);
-      double xlb = sc.lb[nb + j], xub = sc.ub[nb + j];
-      double lo = xlb - e * nl, hi = xub + e * nu;
-      Lines ln;
-      int code = envelope(RELAX_EXP, lo, hi, ln);
-      if (code) err_exp = err_exp ? min(err_exp, code) : code;
-      a_lo[j] = ln.al;
-      a_up[j] = ln.au;
-      double ub2 = ln.au * (ln.au >= 0.0 ? xub : xlb) + ln.bu;
-      double lb2 = ln.al * (ln.al >= 0.0 ? xlb : xub) + ln.bl;
-      e_ub[j] = ub2;
-      e_lb[j] = lb2;
-      // ||a v||_q = |a| ||v||_q: norms of the composed rows without re-reading them
-      double nel = fabs(ln.al) * (ln.al >= 0.0 ? nl : nu);
-      double neu = fabs(ln.au) * (ln.au >= 0.0 ? nu : nl);
-      e_lo[j] = lb2 - e * nel;
-      e_hi[j] = ub2 + e * neu;
-    }
-  }
-  if (lane == 0 && err_exp) set_status(status, s, site_exp, err_exp);
-  __syncthreads();
-
-  // ---- phase 2: SumReduce over keys, column-owned (thread owns CH float4 chunks)
-  double su[CH][4], sl[CH][4];
-#pragma unroll
-  for (int q = 0; q < CH; ++q)
-#pragma unroll
-    for (int t = 0; t < 4; ++t) su[q][t] = sl[q][t] = 0.0;
-  for (int j = 0; j < n; ++j) {
-    double au = a_up[j], al = a_lo[j];
-    const float* c = cb + (long long)j * D;
-    const float* r = rb + (long long)j * D;
-#pragma unroll
-    for (int q = 0; q < CH; ++q) {
-      int d = (threadIdx.x + q * blockDim.x) * 4;
-      if (d < D) {
-        float4 cv = *reinterpret_cast<const float4*>(c + d);
-        float4 rv = *reinterpret_cast<const float4*>(r + d);
-        float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          double u = (double)cc[t] + (double)rr[t], l = (double)cc[t] - (double)rr[t];
-          su[q][t] += au * (au >= 0.0 ? u : l);
-          sl[q][t] += al * (al >= 0.0 ? l : u);
-        }
-      }
-    }
-  }
-  // norms of the sum rows
-  double pu = 0.0, pl = 0.0;
-#pragma unroll
-  for (int q = 0; q < CH; ++q) {
-    int d = (threadIdx.x + q * blockDim.x) * 4;
-    if (d < D)
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        if (Q == NORM_L1) { pu += fabs(su[q][t]); pl += fabs(sl[q][t]); }
-        else if (Q == NORM_L2) { pu += su[q][t] * su[q][t]; pl += sl[q][t] * sl[q][t]; }
-        else { pu = fmax(pu, fabs(su[q][t])); pl = fmax(pl, fabs(sl[q][t])); }
-      }
-  }
-  double nsu = block_reduce<Q>(pu, red);
-  double nsl = block_reduce<Q>(pl, red);
-  if (threadIdx.x == 0) {
-    double slb = 0.0, sub = 0.0;  // propagate_sum_axis order (relax.cpp:728-731)
-    for (int j = 0; j < n; ++j) {
-      slb += e_lb[j];
-      sub += e_ub[j];
-    }
-    NormAcc<Q> fin;
-    double lo = slb - e * fin.fin(nsl), hi = sub + e * fin.fin(nsu);
-    Lines ln;
-    int code = envelope(RELAX_RECIP, lo, hi, ln);  // RecipVerify node
-    if (code) set_status(status, s, site_recip, code);
-    scal[0] = ln.al;
-    scal[1] = ln.au;
-    scal[2] = ln.al * (ln.al >= 0.0 ? slb : sub) + ln.bl;  // r lb
-    scal[3] = ln.au * (ln.au >= 0.0 ? sub : slb) + ln.bu;  // r ub
-  }
-  __syncthreads();
-  const double r_al = scal[0], r_au = scal[1], r_lb = scal[2], r_ub = scal[3];
-  // r rows (compose_elementwise of the sum) and their norms
-  pu = pl = 0.0;
-#pragma unroll
-  for (int q = 0; q < CH; ++q)
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      double u = su[q][t], l = sl[q][t];
-      double ru = r_au * (r_au >= 0.0 ? u : l);
-      double rl = r_al * (r_al >= 0.0 ? l : u);
-      su[q][t] = ru;
-      sl[q][t] = rl;
-      int d = (threadIdx.x + q * blockDim.x) * 4;
-      if (d < D) {
-        if (Q == NORM_L1) { pu += fabs(ru); pl += fabs(rl); }
-        else if (Q == NORM_L2) { pu += ru * ru; pl += rl * rl; }
-        else { pu = fmax(pu, fabs(ru)); pl = fmax(pl, fabs(rl)); }
-      }
-    }
-  double nru = block_reduce<Q>(pu, red);
-  double nrl = block_reduce<Q>(pl, red);
-  NormAcc<Q> fin;
-  const double r_lo = r_lb - e * fin.fin(nrl);
-  const double r_hi = r_ub + e * fin.fin(nru);
-
-  // ---- phase 3: MulBroadcast (McCormick e_j * r), groups of kSmGroup keys
-  for (int j0 = 0; j0 < n; j0 += kSmGroup) {
-    double gu[kSmGroup], gl[kSmGroup];
-#pragma unroll
-    for (int g = 0; g < kSmGroup; ++g) gu[g] = gl[g] = 0.0;
-#pragma unroll
-    for (int g = 0; g < kSmGroup; ++g) {
-      int j = j0 + g;
-      if (j >= n) break;
-      double au = a_up[j], al = a_lo[j];
-      double lx = e_lo[j], ly = r_lo, uy = r_hi;
-      float* c = cb + (long long)j * D;
-      float* r = rb + (long long)j * D;
-#pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        int d = (threadIdx.x + q * blockDim.x) * 4;
-        if (d < D) {
-          float4 cv = *reinterpret_cast<const float4*>(c + d);
-          float4 rv = *reinterpret_cast<const float4*>(r + d);
-          float cc[4] = {cv.x, cv.y, cv.z, cv.w}, rr[4] = {rv.x, rv.y, rv.z, rv.w};
-          float oc[4], orr[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            double u = (double)cc[t] + (double)rr[t], l = (double)cc[t] - (double)rr[t];
-            double eu = au * (au >= 0.0 ? u : l);
-            double el = al * (al >= 0.0 ? l : u);
-            double pl2 = 0.0, pu2 = 0.0;
-            // lower plane: cx = ly, cy = lx (relax.cpp:542-553)
-            if (ly != 0.0) pl2 += ly * (ly >= 0.0 ? el : eu);
-            if (lx != 0.0) pl2 += lx * (lx >= 0.0 ? sl[q][t] : su[q][t]);
-            // upper plane: cx = uy, cy = lx (relax.cpp:556-567)
-            if (uy != 0.0) pu2 += uy * (uy >= 0.0 ? eu : el);
-            if (lx != 0.0) pu2 += lx * (lx >= 0.0 ? su[q][t] : sl[q][t]);
-            oc[t] = (float)(0.5 * (pu2 + pl2));
-            orr[t] = (float)(0.5 * (pu2 - pl2));
-            if (Q == NORM_L1) { gu[g] += fabs(pu2); gl[g] += fabs(pl2); }
-            else if (Q == NORM_L2) { gu[g] += pu2 * pu2; gl[g] += pl2 * pl2; }
-            else { gu[g] = fmax(gu[g], fabs(pu2)); gl[g] = fmax(gl[g], fabs(pl2)); }
-          }
-          *reinterpret_cast<float4*>(c + d) = make_float4(oc[0], oc[1], oc[2], oc[3]);
-          *reinterpret_cast<float4*>(r + d) = make_float4(orr[0], orr[1], orr[2], orr[3]);
-        }
-      }
-    }
-    // reduce the group's 2*kSmGroup partial norms across the CTA
-#pragma unroll
-    for (int g = 0; g < kSmGroup; ++g) {
-      if (Q == NORM_LINF) { gu[g] = warp_max(gu[g]); gl[g] = warp_max(gl[g]); }
-      else { gu[g] = warp_sum(gu[g]); gl[g] = warp_sum(gl[g]); }
-    }
-    if (lane == 0)
-#pragma unroll
-      for (int g = 0; g < kSmGroup; ++g) {
-        grp[warp * 2 * kSmGroup + g] = gu[g];
-        grp[warp * 2 * kSmGroup + kSmGroup + g] = gl[g];
-      }
-    __syncthreads();
-    if (threadIdx.x < kSmGroup && j0 + threadIdx.x < n) {
-      int g = threadIdx.x, j = j0 + g;
-      double nu = grp[g], nl = grp[kSmGroup + g];
-      for (int w = 1; w < nwarps; ++w) {
-        nu = qcombine<Q>(nu, grp[w * 2 * kSmGroup + g]);
-        nl = qcombine<Q>(nl, grp[w * 2 * kSmGroup + kSmGroup + g]);
-      }
-      double lx = e_lo[j], ly = r_lo, uy = r_hi;
-      double olb = 0.0, oub = 0.0;
-      term_bias(lx, ly, uy, e_lb[j], e_ub[j], r_lb, r_ub, olb, oub);
-      long long o = nb + j;
-      sc.lb[o] = olb;
-      sc.ub[o] = oub;
-      if (sc.lo) {
-        sc.lo[o] = olb - e * fin.fin(nl);
-        sc.hi[o] = oub + e * fin.fin(nu);
-      }
-    }
-    __syncthreads();
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Input binding, mean pooling, classifier head
@@ -3184,13 +2963,12 @@ int launch_dot_weighted(const NView& p, const NView& v, const NView& out, int S,
 int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int norm,
                    const double* eps, int* status, int site_exp, int site_recip,
                    cudaStream_t st) {
-  const char* ver = getenv("FG_SOFTMAX");  // "1" / "2": older multi-read kernels (comparison runs)
-  const char* pe = getenv("FG_SM3_PERSIST");
-  const char* te = getenv("FG_SM3_TILE_KB");
-  const int nbuf = (pe && pe[0] == '1') ? 2 : 1;
-  const bool legacy = ver && (ver[0] == '1' || ver[0] == '2' || ver[0] == '3');
-  static const bool no6 = getenv("FG_SM6_OFF") != nullptr;
-  if (!legacy && !no6 && (D == 64 || D == 128) && n % (512 / D) == 0) {  // narrow rows: G keys per warp step
+  // Shape-based choice (each measured best for its shapes): narrow rows (D 64 / 128)
+  // -> softmax6, several keys per warp step; D 256 / 512 -> softmax4, streaming at full width;
+  // wide rows (D > 512, multiple of 128) -> softmax5, Σ partials in SMEM; any other D that fits
+  // a cluster -> softmax3 (columns split over a CTA cluster); otherwise softmax2.
+  constexpr int nbuf = 1;
+  if ((D == 64 || D == 128) && n % (512 / D) == 0) {  // narrow rows: G keys per warp step
     constexpr int NC6 = 4;
     const size_t smem = softmax6_smem(n, D, NC6);
     static size_t attr6[2][3] = {};
@@ -3221,14 +2999,11 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
 #undef SM6
     return 1;
   }
-  static const bool force5 = getenv("FG_SM5_ALL") != nullptr;  // comparison runs
-  if (!legacy && D % 128 == 0 && (D > 512 || force5)) {  // wide rows (c5): streaming kernel, Σ partials in SMEM
+  if (D % 128 == 0 && D > 512) {  // wide rows (c5): streaming kernel, Σ partials in SMEM
     constexpr int NC5 = 2;
-    static const int ns_env = getenv("FG_SM5_NS") ? atoi(getenv("FG_SM5_NS")) : 0;
     // one stage per consumer warp and three CTAs per SM measured best on c5 (40 ms per pass vs 50 ms
     // with two stages per warp at two CTAs per SM, 148 ms for the cluster kernel)
-    int ns = ns_env >= NC5 && ns_env % NC5 == 0 ? ns_env : NC5;
-    while (ns > NC5 && softmax5_smem(n, D, NC5, ns) > (ns_env ? 220 : 110) * 1024) ns -= NC5;  // ... 2 CTAs/SM
+    const int ns = NC5;
     const size_t smem = softmax5_smem(n, D, NC5, ns);
     if (smem <= 227 * 1024) {
       static size_t attr5[2][3] = {};
@@ -3259,10 +3034,8 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
   // streaming kernel (full D per CTA) where a key row is wide enough to amortise its per-key
   // envelope and reductions (measured: D = 512 3.3 vs 7.2 ms per c3 pass; D = 128 2.06 vs 1.98 ms
   // per c2 pass for the cluster kernel, which stays the choice there)
-  static const bool force4 = getenv("FG_SM4_ALL") != nullptr;
-  if (!legacy && (D == 256 || D == 512 || (force4 && D == 128))) {
-    static const int nc_env = getenv("FG_SM4_NC") ? atoi(getenv("FG_SM4_NC")) : 0;
-    const int NCsel = nc_env == 8 ? 8 : 4;  // default: 4 consumer warps, 4 CTAs per SM
+  if (D == 256 || D == 512) {
+    const int NCsel = 4;  // 4 consumer warps, 4 CTAs per SM (8 warps measured slower)
     const size_t smem = softmax4_smem(n, D, NCsel);
     static size_t attr4[3][3][3] = {};
     static int grid4[3][3][3] = {};
@@ -3298,8 +3071,8 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
 #undef SM4
     return 1;
   }
-  const int cs = softmax3_cluster(n, D, nbuf, te ? atoi(te) : 64);
-  if (cs > 0 && !(ver && (ver[0] == '1' || ver[0] == '2'))) {
+  const int cs = softmax3_cluster(n, D, nbuf, 64);
+  if (cs > 0) {
     const size_t smem = softmax3_smem(n, D / cs, cs, nbuf);
     const int lpk = softmax3_lpk(D / cs);
     static size_t attr_set[3] = {0, 0, 0};
@@ -3323,12 +3096,6 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      if (nbuf == 2) {  // persistent: as many clusters as fit at once (at most one per row)
-        int mc = 0;
-        if (cudaOccupancyMaxActiveClusters(&mc, (void*)kern, &cfg) != cudaSuccess || mc <= 0) mc = 148 / cs;
-        const int ncl = mc < nrows ? mc : nrows;
-        cfg.gridDim = dim3((unsigned)(ncl * cs));
-      }
       cudaLaunchKernelEx(&cfg, kern, sc, rows_per_s, nrows, n, D, cs, lpk, nbuf, eps, status, site_exp, site_recip);
     };
     if (q == NORM_L1) launch(softmax3_kernel<NORM_L1>);
@@ -3336,7 +3103,7 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
     else launch(softmax3_kernel<NORM_LINF>);
     return 1;
   }
-  if (!(ver && ver[0] == '1')) {
+  {
     const int nw = D <= 512 ? 16 : 8;
     size_t smem = (6 * (size_t)n + 2 * (size_t)D + 40) * sizeof(double) + (size_t)nw * 2 * D * sizeof(float);
     // at most two CTAs per SM: their rows (n*D*8 bytes each) stay in L2 between phases 1 and 3
@@ -3357,28 +3124,6 @@ int launch_softmax(const NView& sc, int S, int rows_per_s, int n, int D, int nor
     else launch(softmax2_kernel<NORM_LINF>);
     return 1;
   }
-  int threads = D / 4;
-  if (threads < 64) threads = 64;
-  if (threads > kSmThreads) threads = kSmThreads;
-  threads = (threads + 31) / 32 * 32;
-  int ch = (D / 4 + threads - 1) / threads;
-  size_t smem = (6 * (size_t)n + 32 + 8 * 2 * kSmGroup + 8) * sizeof(double);
-  dim3 grid(S * rows_per_s), block(threads);
-  int q = dual_norm(norm);
-#define SM_LAUNCH(QQ, CC)                                                              \
-  softmax_kernel<QQ, CC><<<grid, block, smem, st>>>(sc, rows_per_s, n, D, eps, status, \
-                                                     site_exp, site_recip)
-  if (ch <= 1) {
-    if (q == NORM_L1) SM_LAUNCH(NORM_L1, 1); else if (q == NORM_L2) SM_LAUNCH(NORM_L2, 1); else SM_LAUNCH(NORM_LINF, 1);
-  } else if (ch == 2) {
-    if (q == NORM_L1) SM_LAUNCH(NORM_L1, 2); else if (q == NORM_L2) SM_LAUNCH(NORM_L2, 2); else SM_LAUNCH(NORM_LINF, 2);
-  } else if (ch <= 4) {
-    if (q == NORM_L1) SM_LAUNCH(NORM_L1, 4); else if (q == NORM_L2) SM_LAUNCH(NORM_L2, 4); else SM_LAUNCH(NORM_LINF, 4);
-  } else {
-    return -1;  // D > 4096 unsupported
-  }
-#undef SM_LAUNCH
-  return 1;
 }
 
 int launch_init_input(float* lam, long long cr, double* lb, double* ub, const double* x,

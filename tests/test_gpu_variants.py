@@ -32,8 +32,7 @@ def run(name, n, slots, **env):
 EXACT = [{"FG_NO_GRAPH": "1"}, {"FG_NO_ROWS2": "1"}, {"FG_ONEHOT_DENSE_QK": "1"}, {"FG_NO_ZERO_PROBE": "1"},
          {"FG_MEANPOOL_SCALAR": "1"}, {"FG_TOKENS_ONEPASS": "1"}]
 CLOSE = [{"FG_NO_UMMA": "1"}, {"FG_NO_UMMA_DOTS": "1"}, {"FG_NO_UMMA_AFFINE": "1"}, {"FG_2CTA": "1"},
-         {"FG_EPI_GROUPS": "1"}, {"FG_NO_ONEHOT": "1"}, {"FG_SOFTMAX": "3"}, {"FG_SM6_OFF": "1"},
-         {"FG_SM4_NC": "8"}, {"FG_SM5_ALL": "1"}]
+         {"FG_EPI_GROUPS": "1"}, {"FG_NO_ONEHOT": "1"}]
 
 
 @pytest.fixture(scope="module")
