@@ -60,6 +60,12 @@ typedef int fg_status;
 #define FG_RELAX_SILU 2
 #define FG_RELAX_EXP 3
 #define FG_RELAX_RECIP 4
+/* Extension (no reference counterpart): the envelopes of the LayerNorm bound chain.
+ * sqrt on [lo, hi], lo >= 0 (else domain error): lower = chord, upper = tangent at the midpoint;
+ * square: lower = tangent at the midpoint, upper = chord.  Usable wherever a relaxation kind is
+ * (fg_relax, fg_elementwise_verify); Context.propagate_layernorm chains them. */
+#define FG_RELAX_SQRT 5
+#define FG_RELAX_SQUARE 6
 
 /* faith::relax::DotLayout (relax.hpp:79) */
 #define FG_DOT_SIMILARITY 0

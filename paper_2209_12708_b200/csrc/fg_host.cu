@@ -443,7 +443,7 @@ fg_status fg_affine(fg_ctx* ctx, size_t rows, size_t c, size_t o, size_t d, cons
 fg_status fg_relax(fg_ctx* ctx, int kind, size_t n, const double* lo, const double* hi,
                    double* a_low, double* b_low, double* a_up, double* b_up) {
   cudaSetDevice(ctx->device);
-  if (kind < 0 || kind > FG_RELAX_RECIP) return fail(ctx, FG_EINVAL, "relax: unknown kind");
+  if (kind < 0 || kind > FG_RELAX_SQUARE) return fail(ctx, FG_EINVAL, "relax: unknown kind");
   DBuf dlo, dhi, out;
   CK(dlo.alloc(sizeof(double) * n));
   CK(dhi.alloc(sizeof(double) * n));
@@ -496,7 +496,7 @@ fg_status fg_elementwise_verify(fg_ctx* ctx, int kind, size_t n, size_t d, const
                                 double* yub) {
   if (!eps_ok(eps)) return fail(ctx, FG_EINVAL, "PerturbationSpec: epsilon must be finite and >= 0");
   cudaSetDevice(ctx->device);
-  if (kind < 0 || kind > FG_RELAX_RECIP) return fail(ctx, FG_EINVAL, "elementwise_verify: unknown kind");
+  if (kind < 0 || kind > FG_RELAX_SQUARE) return fail(ctx, FG_EINVAL, "elementwise_verify: unknown kind");
   if (ctx->precision == FG_PRECISION_F64)
     return fgh::x64_elementwise_verify(ctx, kind, n, d, xlw, xlb, xuw, xub, norm, eps, ylw, ylb, yuw, yub);
   OpBounds x;
@@ -1384,11 +1384,20 @@ bool ambiguous_verdict(const double* lo, const double* hi, int C, int t, double 
   return false;
 }
 
+// First exact re-decision of a model: upload the f64 weights and map the stream-ordered pool up
+// to the exact pass's working set (about eight FFN-sized f64 tensors, capped at 4 GiB), so the
+// first ambiguous probe of a search does not pay for mapping fresh memory.
 fg_status upload_params64(fg_model* m) {
   fg_ctx* ctx = m->ctx;
   if (m->params64.p) return FG_OK;
   CK(m->params64.alloc(sizeof(double) * m->params.size()));
   CK(cudaMemcpy(m->params64.p, m->params.data(), sizeof(double) * m->params.size(), cudaMemcpyHostToDevice));
+  const fg_config& c = m->cfg;
+  const size_t ffn = (size_t)c.length * c.ffn * (size_t)c.embed * 2 * sizeof(double) * 2;  // 2 words, lw + uw
+  DBuf warm;
+  CK(warm.alloc_async(std::min<size_t>(8 * ffn, 4ull << 30), ctx->stream));
+  warm.reset();
+  CK(cudaStreamSynchronize(ctx->stream));
   return FG_OK;
 }
 

@@ -24,7 +24,11 @@ constexpr int kCodeInval = 1;
 constexpr int kCodeDomain = 2;
 
 enum Norm { NORM_L1 = 0, NORM_L2 = 1, NORM_LINF = 2 };
-enum Relax { RELAX_RELU = 0, RELAX_TANH = 1, RELAX_SILU = 2, RELAX_EXP = 3, RELAX_RECIP = 4 };
+enum Relax {
+  RELAX_RELU = 0, RELAX_TANH = 1, RELAX_SILU = 2, RELAX_EXP = 3, RELAX_RECIP = 4,
+  // extension (no reference counterpart): the LayerNorm bound chain's envelopes
+  RELAX_SQRT = 5, RELAX_SQUARE = 6
+};
 
 // A neuron-indexed view into a batched bound tensor.
 //   neuron(s, row, f) = s*s_stride + row*row_stride + col0 + f

@@ -248,6 +248,36 @@ __device__ int envelope(int kind, double lo, double hi, Lines& r, int lane = 0, 
       }
       return 0;
     }
+    case RELAX_SQRT: {  // extension: concave on [0, inf) -> lower chord, upper tangent at the midpoint
+      if (lo < 0.0) return kCodeDomain;
+      const double m = 0.5 * (lo + hi);
+      if (m == 0.0) return 0;  // lo = hi = 0: the zero lines are exact
+      const double sm = sqrt(m);
+      r.au = 0.5 / sm;
+      r.bu = 0.5 * sm;  // sqrt(m) - m / (2 sqrt(m))
+      if (lo == hi) {
+        r.al = r.au;
+        r.bl = r.bu;
+      } else {
+        chord(lo, hi, sqrt(lo), sqrt(hi), r.al, r.bl);
+      }
+      if (!isfinite(r.au) || !isfinite(r.bu) || !isfinite(r.al) || !isfinite(r.bl)) return kCodeDomain;
+      return 0;
+    }
+    case RELAX_SQUARE: {  // extension: convex -> lower tangent at the midpoint, upper chord
+      const double m = 0.5 * (lo + hi);
+      r.al = 2.0 * m;
+      r.bl = -m * m;
+      if (lo == hi) {
+        r.au = r.al;
+        r.bu = r.bl;
+      } else {
+        r.au = lo + hi;  // chord of x^2: slope (hi^2 - lo^2) / (hi - lo), intercept -lo * hi
+        r.bu = -lo * hi;
+      }
+      if (!isfinite(r.al) || !isfinite(r.bl) || !isfinite(r.au) || !isfinite(r.bu)) return kCodeDomain;
+      return 0;
+    }
     case RELAX_SILU: {  // relax.cpp:426-468
       if (lo == hi) {
         double a = silu_derivative(lo);

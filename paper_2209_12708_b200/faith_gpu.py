@@ -24,7 +24,8 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "faith_gpu.h")
 
 FG_OK, FG_EINVAL, FG_EDOMAIN, FG_ERANGE, FG_ERUNTIME, FG_ECUDA, FG_ENOMEM = range(7)
 NORM = {"l1": 0, "l2": 1, "linf": 2}
-RELAX = {"relu": 0, "tanh": 1, "silu": 2, "exp": 3, "recip": 4}
+RELAX = {"relu": 0, "tanh": 1, "silu": 2, "exp": 3, "recip": 4,
+         "sqrt": 5, "square": 6}  # extension: LayerNorm bound chain (no reference counterpart)
 DOT = {"similarity": 0, "weighted_values": 1}
 # ambiguity band of the decision-exact verdicts (FG_DEFAULT_KAPPA, include/faith_gpu.h)
 DEFAULT_KAPPA = 6e-6
@@ -398,6 +399,34 @@ class Context:
         self._check(self.lib.fg_mul_broadcast(self.handle, outer, n, inner, d, *map(_d, x), *map(_d, r),
                                               NORM[norm], eps, *map(_d, y)), "propagate_mul_broadcast")
         return LinearBounds(*y)
+
+    def propagate_layernorm(self, x, gamma, beta, norm: str, eps: float, delta: float = 1e-5) -> LinearBounds:
+        """EXTENSION (no reference counterpart: the reference model has no LayerNorm,
+        proj/include/faith/model.hpp:22-24).  Linear bounds of
+        y = (x - mean(x)) / sqrt(var(x) + delta) * gamma + beta over the last axis of x [n, E],
+        as a chain of the reference's own bound operators plus the sqrt / square envelopes:
+          c = propagate_affine(x, I - 1/E)               (centring: exact, linear)
+          s = ElementwiseVerify(square, c)               (convex: tangent below, chord above)
+          v = propagate_affine(s, 1/E column, + delta)   (variance + delta)
+          r = ElementwiseVerify(sqrt, v)                 (concave: chord below, tangent above)
+          q = ElementwiseVerify(recip, r)                (relax.cpp:396-424)
+          z = propagate_mul_broadcast(c, q, axis 1)      (McCormick, relax.cpp:744-775)
+          y = propagate_affine(z, diag(gamma), beta)
+        Sound by construction (every step is); checked by sampling in tests/test_gpu_layernorm.py."""
+        x = _bounds(x)
+        if x.lb.ndim != 2:
+            raise InvalidArgument("propagate_layernorm: x must have neuron shape [n, E]")
+        E = x.lb.shape[1]
+        gamma, beta = _f64(gamma).ravel(), _f64(beta).ravel()
+        if gamma.size != E or beta.size != E or not (delta > 0.0):
+            raise InvalidArgument("propagate_layernorm: gamma / beta length or delta")
+        c = self.propagate_affine(x, np.eye(E) - 1.0 / E)
+        sq = self.elementwise_verify("square", c, norm, eps)
+        v = self.propagate_affine(sq, np.full((E, 1), 1.0 / E), np.array([delta]))
+        r = self.elementwise_verify("sqrt", v, norm, eps)
+        q = self.elementwise_verify("recip", r, norm, eps)
+        z = self.propagate_mul_broadcast(c, q, 1, norm, eps)
+        return self.propagate_affine(z, np.diag(gamma), beta)
 
     def relax_bilinear(self, xlo, xhi, ylo, yhi) -> tuple:
         """faith::relax::relax_bilinear (relax.cpp:499-523) -> (lo_x, lo_y, lo_c, up_x, up_y, up_c)."""
