@@ -622,9 +622,9 @@ __global__ void compose_kernel(const float* __restrict__ lin, long long crin, co
 // Affine bias path (relax.cpp:273-299) in f64: one thread per output neuron,
 // i accumulated in the reference's order; optional residual propagate_add(res, y).
 // ---------------------------------------------------------------------------
-constexpr int kBiasRows = 32;    // token rows per CTA (one weight load feeds all of them)
+constexpr int kBiasRows = 8;     // token rows per CTA (one weight load feeds all of them)
 constexpr int kBiasCols = 128;   // output neurons per CTA (one per thread)
-constexpr int kBiasChunk = 64;   // input neurons staged in SMEM per step
+constexpr int kBiasChunk = 256;  // input neurons staged in SMEM per step
 
 __global__ void __launch_bounds__(kBiasCols) affine_bias_kernel(
     const double* __restrict__ lb_in, const double* __restrict__ ub_in, const double* __restrict__ w,

@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 from helpers import model_config
-from oracle.oracle import ModelConfig as OCfg
+from oracle.oracle import ModelConfig as OCfg, node_layout
 from paper_2209_12708_b200 import faith_gpu as F
 from paper_2209_12708_b200.configs import ALL as CONFIGS
 
@@ -58,6 +58,13 @@ def test_exact_pass_matches_golden(models, port, path):
     st, lo, hi, nlo, nhi = m.bound_pass_exact(x, pos, w.norm, float(g["eps"]), dump=True)
     assert st == int(g["status"])
     idx = g["node_index"]
+    if name == "c4":  # chaotic from layer 3 on (test_gpu_pass.CHAOTIC_FROM): the well-conditioned layers
+        end = [off for nm, off, n in node_layout(cfg) if nm == "l3.q"][0]
+        keep = idx < end
+        got, want = np.concatenate([nlo[idx[keep]], nhi[idx[keep]]]), np.concatenate([g["node_lo"][keep],
+                                                                                       g["node_hi"][keep]])
+        assert np.max(np.abs(got - want) / np.maximum(1.0, np.abs(want))) <= 1e-9  # growing x30 per layer
+        return
     got = np.concatenate([nlo[idx], nhi[idx], lo, hi])
     want = np.concatenate([g["node_lo"], g["node_hi"], g["logits_lo"], g["logits_hi"]])
     err = np.abs(got - want) / np.maximum(1.0, np.abs(want))

@@ -61,6 +61,16 @@ def models(ctx, port):
 
 
 # ---- golden vectors from the reference build ------------------------------------
+# c4 (6 layers, E 512, F 2048 on random-init weights) is numerically chaotic at any radius where
+# its bounds are finite: a difference in the last bit grows ~x30 per layer from layer 3 on
+# (tools/golden_layer_errors.py; the reference-order exact pass, whose only difference from the
+# reference is the device libm's exp in the last ulp, drifts 6e-3 from it by the logits, more than
+# the f32 pass's 2e-3).  Layers below CHAOTIC_FROM are held to the 1e-4 bar; from there on the
+# test pins the conditioning itself: a 1-ulp change of the input moves the exact pass's logits by
+# more than 1e-4 -- no f64 implementation but the reference's own binary can match those digits.
+CHAOTIC_FROM = {"c4": 5}
+
+
 @pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "*_pass_s*.npz"))), ids=os.path.basename)
 def test_pass_matches_golden(models, port, path):
     g = np.load(path)
@@ -68,10 +78,26 @@ def test_pass_matches_golden(models, port, path):
     s = int(os.path.basename(path).split("_s")[1].split(".")[0])
     w, cfg, params, m = models(name)
     _, x, pos = sentence(port, w, s)
-    st, lo, hi, nlo, nhi = m.bound_pass_dump(x, pos, w.norm, float(g["eps"]))
+    eps = float(g["eps"])
+    st, lo, hi, nlo, nhi = m.bound_pass_dump(x, pos, w.norm, eps)
     assert st == int(g["status"])
-    assert close(lo, g["logits_lo"])[0] and close(hi, g["logits_hi"])[0], (lo, hi, g["logits_lo"], g["logits_hi"])
-    check_nodes(cfg, nlo, nhi, g["node_lo"], g["node_hi"], g["node_index"])
+    first_chaotic = CHAOTIC_FROM.get(name)
+    if first_chaotic is None:
+        assert close(lo, g["logits_lo"])[0] and close(hi, g["logits_hi"])[0], (lo, hi, g["logits_lo"],
+                                                                                g["logits_hi"])
+        check_nodes(cfg, nlo, nhi, g["node_lo"], g["node_hi"], g["node_index"])
+        return
+    idx = g["node_index"]
+    end = [off for nm, off, n in node_layout(cfg) if nm == f"l{first_chaotic}.q"][0]
+    keep = idx < end
+    check_nodes(cfg, nlo, nhi, g["node_lo"][keep], g["node_hi"][keep], idx[keep])
+    # the remaining digits are conditioning-limited: bounded drift, and the exact pass moves by
+    # more than the 1e-4 bar under a 1-ulp input change
+    assert close(lo, g["logits_lo"], 1e-2)[0] and close(hi, g["logits_hi"], 1e-2)[0]
+    st0, elo, ehi, _, _ = m.bound_pass_exact(x, pos, w.norm, eps)
+    st1, flo, fhi, _, _ = m.bound_pass_exact(x * (1.0 + 2.0 ** -52), pos, w.norm, eps)
+    assert st0 == st1 == int(g["status"])
+    assert not (close(flo, elo)[0] and close(fhi, ehi)[0]), "expected a chaotic tail at this radius"
 
 
 # ---- against the C restatement on configs the golden set does not cover ----------
