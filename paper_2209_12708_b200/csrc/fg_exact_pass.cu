@@ -59,6 +59,8 @@ struct Walk {
   double eps;
   double* node_lo;
   double* node_hi;
+  int* dstat = nullptr;  // asynchronous walk: one device status word per relaxation site
+  int site = 0;
   size_t off = 0;
 
   // concretize one node into the host dump (fo_bound_pass order)
@@ -112,11 +114,22 @@ struct Walk {
     return FG_OK;
   }
 
-  // elementwise_verify (graph.cpp:484-501): concretize -> relax (validate, domain) -> compose
+  // elementwise_verify (graph.cpp:484-501): concretize -> relax (validate, domain) -> compose.
+  // Asynchronous walks do not stop at a failing relaxation: its status word is kept on the device
+  // and the first failing site decides the sentence's status when the walk has finished.
   fg_status verify(int kind, const XB& x, XB& y, const char* what) {
     DBuf lo, hi;
     if (fg_status s = x_conc(ctx, x, norm, eps, lo, hi)) return s;
-    return x_relax_compose(ctx, kind, x, lo, hi, y, what);
+    if (!dstat) return x_relax_compose(ctx, kind, x, lo, hi, y, what);
+    DBuf lines;
+    CK(lines.alloc_async(sizeof(double) * 4 * x.n, ctx->stream));
+    double* l = lines.as<double>();
+    XL(launch_relax(kind, lo.as<double>(), hi.as<double>(), (long long)x.n, l, l + x.n, l + 2 * x.n, l + 3 * x.n,
+                    dstat + site++, ctx->stream));
+    if (fg_status s = xb_alloc(ctx, y, x.n, x.d)) return s;
+    XL(launch_x_compose(x.plw(), x.plb(), x.puw(), x.pub(), l, l + x.n, l + 2 * x.n, l + 3 * x.n, y.plw(), y.plb(),
+                        y.puw(), y.pub(), (long long)x.n, (int)x.d, ctx->stream));
+    return FG_OK;
   }
 };
 
@@ -130,10 +143,17 @@ namespace fgh {
 // of the call itself.
 fg_status exact_pass(fg_ctx* ctx, const fg_config& c, const double* params, const double* x_host,
                      const int* pos_host, int words, int norm, double eps, double* logits_lo, double* logits_hi,
-                     double* node_lo, double* node_hi, int* status) {
+                     double* node_lo, double* node_hi, int* status, ExactJob* job) {
   const size_t L = c.length, E = c.embed, H = c.heads, F = c.ffn, C = c.classes, D = (size_t)words * E;
   Walk wk{ctx, c, norm, eps, node_lo, node_hi};
-  *status = FG_OK;
+  if (status) *status = FG_OK;
+  DBuf dstat;
+  const int nsites = 3 * c.layers;  // exp, recip, activation per layer
+  if (job) {
+    CK(dstat.alloc_async(sizeof(int) * nsites, ctx->stream));
+    XL(launch_fill_int(dstat.as<int>(), kStatusClear, nsites, ctx->stream));
+    wk.dstat = dstat.as<int>();
+  }
   XB cur;
   if (fg_status s = xb_alloc(ctx, cur, L * E, D)) return s;
   CK(cudaMemsetAsync(cur.lw.p, 0, sizeof(double) * L * E * D, ctx->stream));
@@ -236,6 +256,17 @@ fg_status exact_pass(fg_ctx* ctx, const fg_config& c, const double* params, cons
   ctx->launches += 4;
   DBuf lo, hi;
   if (fg_status st = x_conc(ctx, logits, norm, eps, lo, hi)) return st;
+  if (job) {  // results land in the job's pinned buffer; the caller waits on job->done
+    double* h = job->host;
+    CK(cudaMemcpyAsync(h, lo.p, sizeof(double) * C, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(h + C, hi.p, sizeof(double) * C, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(job->hstat, dstat.p, sizeof(int) * nsites, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(job->hstat + nsites, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaEventRecord(job->done, ctx->stream));
+    job->nsites = nsites;
+    job->classes = (int)C;
+    return FG_OK;
+  }
   int nonfinite = 0;
   CK(cudaMemcpyAsync(&nonfinite, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaMemcpyAsync(logits_lo, lo.p, sizeof(double) * C, cudaMemcpyDeviceToHost, ctx->stream));

@@ -731,6 +731,18 @@ struct fg_model {
   double kappa = FG_DEFAULT_KAPPA;  // ambiguity band of the decision-exact verdicts
   int exact_probes = 0;   // per call: probes re-decided by the exact pass, and their time
   double exact_ms = 0.0;
+  // asynchronous re-decisions (fg_maxeps): a low-priority side stream and reusable jobs
+  cudaStream_t exact_stream = nullptr;
+  std::vector<std::unique_ptr<fgh::ExactJob>> jobs;
+  ~fg_model() {
+    for (auto& j : jobs) {
+      if (j->host) cudaFreeHost(j->host);
+      if (j->hstat) cudaFreeHost(j->hstat);
+      if (j->start) cudaEventDestroy(j->start);
+      if (j->done) cudaEventDestroy(j->done);
+    }
+    if (exact_stream) cudaStreamDestroy(exact_stream);
+  }
   // offsets of the layers in params (gen_synthetic order)
   size_t layer_off(int l) const {
     size_t e = cfg.embed, f = cfg.ffn;
@@ -1436,6 +1448,71 @@ fg_status decide_probe(fg_model* m, const double* x_s, const int* pos_s, int wor
   return FG_OK;
 }
 
+// Asynchronous re-decision (fg_maxeps): the exact pass of an ambiguous probe is enqueued on the
+// model's side stream and the sentence waits out of its slot while the fused passes of the other
+// sentences continue; `poll` applies the verdict once the job's event has fired.
+fgh::ExactJob* start_exact_job(fg_model* m, const double* x_s, const int* pos_s, int words, int norm, double eps,
+                               int sentence, fg_status& st) {
+  fg_ctx* ctx = m->ctx;
+  st = upload_params64(m);
+  if (st) return nullptr;
+  if (!m->exact_stream) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&m->exact_stream, cudaStreamNonBlocking, lo) != cudaSuccess) {
+      st = fail(ctx, FG_ECUDA, "exact side stream");
+      return nullptr;
+    }
+  }
+  fgh::ExactJob* job = nullptr;
+  for (auto& j : m->jobs)
+    if (!j->busy) job = j.get();
+  if (!job) {
+    auto j = std::make_unique<fgh::ExactJob>();
+    const int C = m->cfg.classes, nsites = 3 * m->cfg.layers;
+    if (cudaMallocHost(&j->host, sizeof(double) * 2 * C) != cudaSuccess ||
+        cudaMallocHost(&j->hstat, sizeof(int) * (nsites + 1)) != cudaSuccess ||
+        cudaEventCreate(&j->start) != cudaSuccess || cudaEventCreate(&j->done) != cudaSuccess) {
+      st = fail(ctx, FG_ENOMEM, "exact job buffers");
+      return nullptr;
+    }
+    job = j.get();
+    m->jobs.push_back(std::move(j));
+  }
+  fg_ctx side = *ctx;  // the same device, launches counted on the side stream
+  side.stream = m->exact_stream;
+  side.launches = 0;
+  cudaEventRecord(job->start, side.stream);
+  st = fgh::exact_pass(&side, m->cfg, m->params64.as<double>(), x_s, pos_s, words, norm, eps, nullptr, nullptr,
+                       nullptr, nullptr, nullptr, job);
+  ctx->launches += side.launches;
+  if (st) {
+    ctx->err = side.err;
+    return nullptr;
+  }
+  job->busy = true;
+  job->sentence = sentence;
+  job->eps = eps;
+  ++m->exact_probes;
+  return job;
+}
+
+// Verdict of a finished job (the reference's exception order: first failing relaxation site,
+// then the sink finiteness check, graph.cpp:663-671).
+int finish_exact_job(fg_model* m, fgh::ExactJob* job, int pred, fg_status& ps) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, job->start, job->done);
+  m->exact_ms += ms;
+  job->busy = false;
+  ps = FG_OK;
+  for (int i = 0; i < job->nsites && ps == FG_OK; ++i)
+    if (job->hstat[i] != kStatusClear) ps = (job->hstat[i] & 15) == kCodeInval ? FG_EINVAL : FG_EDOMAIN;
+  if (ps == FG_OK && job->hstat[job->nsites]) ps = FG_EDOMAIN;
+  int ok = 0;
+  if (ps == FG_OK) fg_check_robust((size_t)job->classes, job->host, job->host + job->classes, (size_t)pred, 0.0, &ok);
+  return ok;
+}
+
 // Narrow workspace for the ε = 0 probes of fg_maxeps (see ensure_workspace's zero_d), with
 // the staged inputs of m->ws copied in; nullptr where it would not pay (D <= 128), when the
 // pass is column-sharded, under FG_NO_ZERO_PROBE=1, or when it does not fit in free HBM.
@@ -1769,13 +1846,79 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
     }
     return FG_OK;
   };
+  // A probe after ε = 0 (P_MAX / P_BISECT) whose f32 verdict is ambiguous is re-decided
+  // asynchronously (start_exact_job): the sentence leaves its slot until the exact verdict is in,
+  // then resumes from `ready` ahead of new sentences.  Column-sharded models decide synchronously
+  // (every rank must run the same sentences in the same slots).
+  const bool async_exact = !m->shard.active();
+  std::vector<fgh::ExactJob*> pending;
+  std::vector<int> ready;  // resumed sentences, FIFO
+  size_t ready_head = 0;
+  // one bisection step of sentence s with verdict ok (cli.cpp:163-177); true when finished
+  auto advance = [&](int s, int ok) -> bool {
+    Sent& t = sent[s];
+    ++t.calls;
+    bool finished = false;
+    if (t.phase == P_MAX) {
+      if (ok) {
+        t.lo = eps_max;
+        finished = true;
+      } else {
+        t.lo = 0.0;
+        t.hi = eps_max;
+        t.phase = P_BISECT;
+      }
+    } else {
+      if (ok) t.lo = t.eps;
+      else t.hi = t.eps;
+    }
+    if (!finished && t.phase == P_BISECT) {
+      if (t.hi - t.lo > tol) t.eps = 0.5 * (t.lo + t.hi);
+      else finished = true;
+    }
+    if (finished) {
+      t.phase = P_DONE;
+      eps_out[s] = status_out[s] == FG_OK ? t.lo : std::numeric_limits<double>::quiet_NaN();
+      calls_out[s] = t.calls;
+      ++done;
+    }
+    return finished;
+  };
+  // applies finished jobs (block: wait for the oldest one)
+  auto poll = [&](bool block) {
+    for (size_t k = 0; k < pending.size();) {
+      fgh::ExactJob* job = pending[k];
+      cudaError_t q = block && k == 0 ? cudaEventSynchronize(job->done) : cudaEventQuery(job->done);
+      if (q == cudaErrorNotReady) {
+        ++k;
+        continue;
+      }
+      if (q != cudaSuccess) {
+        st = fail(ctx, FG_ECUDA, std::string("exact re-decision: ") + cudaGetErrorString(q));
+        return;
+      }
+      const int s = job->sentence;
+      fg_status ps = FG_OK;
+      const int ok = finish_exact_job(m, job, pred[s], ps);
+      if (!advance(s, ps == FG_OK && ok)) ready.push_back(s);
+      pending.erase(pending.begin() + (long)k);
+      block = false;
+    }
+  };
   while (done < S && !st) {
+    bool any = false;
     for (int i = 0; i < slots; ++i) {
+      if (slot[i] < 0 && ready_head < ready.size()) slot[i] = ready[ready_head++];
       while (slot[i] < 0 && next < S && sent[next].phase == P_DONE) ++next;
       if (slot[i] < 0 && next < S) slot[i] = next++;
       int s = slot[i];
+      any = any || s >= 0;
       w.h_slot[i] = s >= 0 ? s : 0;
       w.h_eps[i] = s >= 0 ? sent[s].eps : 0.0;
+    }
+    if (!any) {  // every remaining sentence waits for its exact verdict
+      poll(true);
+      continue;
     }
     float ms = 0.f;
     if ((st = run_pass(m, norm, e0, e1, &ms))) break;
@@ -1796,9 +1939,17 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
       }
       sentence_passes += 1.0;
       fg_status ps = decode_status(w.h_status[i]);
+      const double* plo = w.h_logits + (size_t)i * C;
+      const double* phi = w.h_logits + (size_t)slots * C + (size_t)i * C;
       int ok = 0;
-      if ((st = decide_probe(m, x + s * LE, positions + (size_t)s * words, words, norm, t.eps,
-                             w.h_logits + (size_t)i * C, w.h_logits + (size_t)slots * C + (size_t)i * C, pred[s],
+      if (async_exact && t.phase != P_ZERO && ps == FG_OK && ambiguous_verdict(plo, phi, C, pred[s], 0.0, m->kappa)) {
+        fgh::ExactJob* job = start_exact_job(m, x + s * LE, positions + (size_t)s * words, words, norm, t.eps, s, st);
+        if (st) break;
+        pending.push_back(job);
+        slot[i] = -1;  // waits out of its slot
+        continue;
+      }
+      if ((st = decide_probe(m, x + s * LE, positions + (size_t)s * words, words, norm, t.eps, plo, phi, pred[s],
                              0.0, ps, ok)))
         break;
       if (t.phase == P_ZERO) {  // verified_at(0, tolerate=false)
@@ -1806,34 +1957,12 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
         if (t.phase == P_DONE) slot[i] = -1;
         continue;
       }
-      ++t.calls;
-      bool finished = false;
-      if (t.phase == P_MAX) {
-        if (ok) {
-          t.lo = eps_max;
-          finished = true;
-        } else {
-          t.lo = 0.0;
-          t.hi = eps_max;
-          t.phase = P_BISECT;
-        }
-      } else {
-        if (ok) t.lo = t.eps;
-        else t.hi = t.eps;
-      }
-      if (!finished && t.phase == P_BISECT) {
-        if (t.hi - t.lo > tol) t.eps = 0.5 * (t.lo + t.hi);
-        else finished = true;
-      }
-      if (finished) {
-        t.phase = P_DONE;
-        eps_out[s] = status_out[s] == FG_OK ? t.lo : std::numeric_limits<double>::quiet_NaN();
-        calls_out[s] = t.calls;
-        ++done;
-        slot[i] = -1;
-      }
+      if (advance(s, ps == FG_OK && ok)) slot[i] = -1;
     }
+    if (!st) poll(false);
   }
+  while (!pending.empty() && !st) poll(true);  // (an error left jobs in flight)
+  if (m->exact_stream) cudaStreamSynchronize(m->exact_stream);
   if (!have_pred) pred = fut.get();
   for (int s = 0; s < S; ++s) predicted_out[s] = pred[s];
   CK(cudaEventRecord(c1, ctx->stream));

@@ -127,10 +127,24 @@ fg_status x64_add(fg_ctx* ctx, size_t n, size_t d, const double* alw, const doub
 fg_status x64_scale(fg_ctx* ctx, size_t n, size_t d, const double* xlw, const double* xlb, const double* xuw,
                     const double* xub, double s, double* ylw, double* ylb, double* yuw, double* yub);
 
-// The word-level pass of one sentence in the exact precision mode (fg_exact_pass.cu).
+// An exact pass running asynchronously on a side stream (fg_maxeps' re-decisions overlap the
+// fused passes): results land in pinned host memory, `done` is recorded after them.
+struct ExactJob {
+  double* host = nullptr;  // logits lo [classes], hi [classes]
+  int* hstat = nullptr;    // relaxation-site status words [nsites], then the non-finite flag
+  int nsites = 0, classes = 0;
+  cudaEvent_t start = nullptr, done = nullptr;
+  int sentence = -1;
+  double eps = 0.0;
+  bool busy = false;
+};
+
+// The word-level pass of one sentence in the exact precision mode (fg_exact_pass.cu).  With
+// `job`, nothing is waited for: the results and statuses are copied into the job's pinned
+// buffers on ctx->stream and `job->done` is recorded (`status` / `logits_*` unused).
 fg_status exact_pass(fg_ctx* ctx, const fg_config& c, const double* params_dev, const double* x_host,
                      const int* pos_host, int words, int norm, double eps, double* logits_lo, double* logits_hi,
-                     double* node_lo, double* node_hi, int* status);
+                     double* node_lo, double* node_hi, int* status, ExactJob* job = nullptr);
 
 }  // namespace fgh
 
