@@ -46,7 +46,8 @@ if "ops" in parts:
     for precision in ("f32", "f64"):
         ctx.set_precision(precision)
         lw = rng.uniform(-1, 1, (5, 3))
-        x = (lw, rng.normal(size=5), lw.copy(), rng.normal(size=5) + 2.0)
+        lb = rng.normal(size=5)
+        x = (lw, lb, lw.copy(), lb + 2.0)  # consistent bounds (lb <= ub)
         ctx.concretize(x, "l2", 0.1)
         ctx.propagate_affine(x, rng.normal(size=(5, 4)), rng.normal(size=4))
         ctx.elementwise_verify("relu", x, "linf", 0.05)
