@@ -311,7 +311,7 @@ fg_status fg_profile_pass(fg_model* model, int norm, double eps, int max_sites, 
 /* Self-test of the affine bound GEMM (propagate_affine's Λ contraction) on random data:
  * tcgen05 3xTF32 kernel and FP32 SIMT kernel vs an f64 device reference.  err_* =
  * max|Y - Y_ref| / max|Y_ref| (err_umma = -1 if the shape is not tcgen05-eligible:
- * O % 128, C % 32, D % 128); ms_* = CUDA-event time of one launch; bias_umma[2] (may be NULL) =
+ * O % 32, C % 32, D % 128 or D = 64 with an even row count -- token rows folded in pairs); ms_* = CUDA-event time of one launch; bias_umma[2] (may be NULL) =
  * median signed relative error of the tcgen05 centre / radius planes (radius inputs >= 0). */
 fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_t seed, double* err_umma,
                              double* err_simt, double* ms_umma, double* ms_simt, double* bias_umma);

@@ -275,6 +275,7 @@ LamGemm affine_lam(const DevAffine& a, float* out, long long out_cr, const float
   LamGemm g{};
   g.M = D; g.N = a.O; g.K = a.C; g.K0 = a.C;
   g.nb[0] = (int)rows; g.nb[1] = 2; g.nb[2] = 1; g.nb[3] = 1;
+  if (D == 64) g.fold1 = 1;  // two token rows per 128-lane tile
   g.kdim = 1;
   g.lam_c[1][0] = 1;  // c2 = token row
   g.lam_c[2][1] = 1;  // c3 = plane
@@ -298,7 +299,7 @@ LamGemm affine_lam(const DevAffine& a, float* out, long long out_cr, const float
 int launch_affine_lambda(const DevAffine& a, const TensorMap* tm_in, const float* in, long long in_cr,
                          float* out, long long out_cr, const float* res, long long res_cr, long long rows,
                          int D, cudaStream_t st) {
-  if (a.umma && tm_in && umma_affine_enabled() && D % 128 == 0) {
+  if (a.umma && tm_in && umma_affine_enabled() && (D % 128 == 0 || (D == 64 && rows % 2 == 0))) {
     return launch_lam_gemm(tm_in->bytes, a.tm_hi.bytes, a.tm_lo.bytes,
                            affine_lam(a, out, out_cr, res, res_cr, rows, D), a.bn, st,
                            a.umma2 ? a.tm2_hi.bytes : nullptr, a.umma2 ? a.tm2_lo.bytes : nullptr);
@@ -674,6 +675,7 @@ struct Workspace {
   bool dots2_ok = false;
   int bn_sim = 0, bn_simx = 0, bn_wvx = 0;
   bool dots_ok = false;
+  bool wv_fold = false;  // D = 64: only the P.V product on tcgen05, its query / feature rows folded in pairs
   long long crX = 0, crQKV = 0, crF = 0, crSC = 0;
   DBuf X_b, R1_b, QKV_b, SC_b, CTX_b, F_b;  // f64 lb/ub(/lo/hi) blocks
   DBuf pooled, pooled_b, coef;
@@ -812,7 +814,10 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot, Workspace* wsp =
   w.W = W;
   w.Ntot = Ntot;
   const long long rows = (long long)S * L;
-  const bool dok = umma_available() && D % 128 == 0;
+  // tcgen05 needs 128 TMEM lanes of perturbation columns: D % 128 == 0, or D = 64 with token
+  // rows folded in pairs (affine GEMMs only; the McCormick GEMMs' folded coordinates are
+  // gathered in layer 1, so they keep the FP32 SIMT path at D = 64)
+  const bool dok = umma_available() && (D % 128 == 0 || (D == 64 && rows % 2 == 0));
   w.tm_ok = dok && lam_map(w.tm_X, w.X.as<float>(), w.crX, D, (int)E, rows, 1) &&
             lam_map(w.tm_R1, w.R1.as<float>(), w.crX, D, (int)E, rows, 1) &&
             lam_map(w.tm_CTX, w.CTX.as<float>(), w.crX, D, (int)E, rows, 1) &&
@@ -822,7 +827,14 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot, Workspace* wsp =
   w.bn_simx = umma_pick_bn((int)(2 * L)); // Q.K^T x-side: both output planes in N = 2L
   w.bn_wvx = umma_pick_bn((int)(2 * hd)); // P.V x-side: N = 2hd
   w.dots_ok = false;
-  if (w.tm_ok && w.bn_sim > 0 && w.bn_simx > 0 && w.bn_wvx > 0 && hd % 32 == 0 && L % 32 == 0) {
+  w.wv_fold = false;
+  // D = 64 (c1): the similarity product's folded coordinate (the query token) is gathered in layer
+  // 1 and its y-side contracts over hd (16 at c1, < one 32-deep K step), so it stays FP32 SIMT;
+  // the P.V product folds pairs of query tokens (x-side) / head features (y-side)
+  const bool wv_only = w.tm_ok && D == 64 && w.bn_sim > 0 && w.bn_wvx > 0 && L % 32 == 0 && (2 * hd) % 32 == 0 &&
+                       hd % 2 == 0 && L % 2 == 0;
+  if (wv_only || (w.tm_ok && D % 128 == 0 && w.bn_sim > 0 && w.bn_simx > 0 && w.bn_wvx > 0 && hd % 32 == 0 &&
+                  L % 32 == 0)) {
     const long long SH = (long long)S * H;
     bool ok = lam_map(w.tm_QKVk, w.QF.as<float>(), w.crQKV, D, (int)(3 * E), rows, 1) &&
               lam_map(w.tm_QKVrow, w.QF.as<float>(), w.crQKV, D, (int)(3 * E), rows, 2) &&
@@ -833,13 +845,14 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot, Workspace* wsp =
       CK(w.cf_wv_x[part].alloc(sizeof(float) * SH * 2 * hd * 2 * L));
       CK(w.cf_wv_y[part].alloc(sizeof(float) * SH * 2 * L * L));
       // x-side coefficient arrays [SH][2 planes][rows][K] are read as [SH][2*rows][K]
-      ok = ok && umma_tmap_wop(w.tm_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), (int)(2 * hd), (int)(2 * L), 1, (int)SH, w.bn_simx) &&
-           umma_tmap_wop(w.tm_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), (int)hd, (int)L, 2, (int)SH, w.bn_sim) &&
+      ok = ok && (wv_only || (umma_tmap_wop(w.tm_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), (int)(2 * hd), (int)(2 * L), 1, (int)SH, w.bn_simx) &&
+                              umma_tmap_wop(w.tm_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), (int)hd, (int)L, 2, (int)SH, w.bn_sim))) &&
            umma_tmap_wop(w.tm_wv_x[part].bytes, w.cf_wv_x[part].as<float>(), (int)(2 * L), (int)(2 * hd), 1, (int)SH, w.bn_wvx) &&
            umma_tmap_wop(w.tm_wv_y[part].bytes, w.cf_wv_y[part].as<float>(), (int)L, (int)L, 2, (int)SH, w.bn_sim);
     }
-    w.dots_ok = ok;
-    bool ok2 = ok && w.bn_sim >= 64 && w.bn_simx >= 64 && w.bn_wvx >= 64;
+    w.dots_ok = ok && !wv_only;
+    w.wv_fold = ok && wv_only;
+    bool ok2 = w.dots_ok && w.bn_sim >= 64 && w.bn_simx >= 64 && w.bn_wvx >= 64;
     for (int part = 0; part < 2 && ok2; ++part)
       ok2 = umma_tmap_wop(w.tm2_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), (int)(2 * hd), (int)(2 * L), 1, (int)SH, w.bn_simx / 2) &&
             umma_tmap_wop(w.tm2_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), (int)hd, (int)L, 2, (int)SH, w.bn_sim / 2) &&
@@ -1079,7 +1092,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     // ctx = DotProduct(probs, v)
     NView cx{CTX, w.crX, CTX_lb, CTX_ub, nullptr, nullptr, (long long)L * E, E, 0};
     g_tag = "dot_weighted";
-    if (w.dots_ok && umma_dots_enabled()) {
+    if ((w.dots_ok || w.wv_fold) && umma_dots_enabled()) {
       LAUNCH(launch_wv_coef_split(sc, v, S, H, L, hd, w.cf_wv_x[0].as<float>(), w.cf_wv_x[1].as<float>(),
                                   w.cf_wv_y[0].as<float>(), w.cf_wv_y[1].as<float>(), st));
       LAUNCH(launch_wv_bias(sc, v, cx, S, H, L, hd, st));
@@ -1096,6 +1109,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gx.ldn_out = D;
       gx.n_split = hd; gx.split_stride = w.crX;
       gx.alpha = 1.0f;
+      if (w.wv_fold) gx.fold1 = 3;  // pairs of query tokens i
       LAUNCH(launch_lam_gemm(w.tm_SC.bytes, w.tm_wv_x[0].bytes, w.tm_wv_x[1].bytes, gx, w.bn_wvx, st,
                              w.dots2_ok ? w.tm2_wv_x[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_x[1].bytes : nullptr));
       // y-side: ctx[s,i,h*hd+k,:] += sum_j lx[i,j] V_p[j, 2E + h*hd + k]   (K along token rows)
@@ -1113,6 +1127,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gy.out_c[3] = w.crX; gy.ldn_out = (long long)E * D;
       gy.alpha = 1.0f;
       gy.accumulate = 1;
+      if (w.wv_fold) gy.fold1 = 3;  // pairs of head features k
       LAUNCH(launch_lam_gemm(w.tm_QKVrow.bytes, w.tm_wv_y[0].bytes, w.tm_wv_y[1].bytes, gy, w.bn_sim, st,
                              w.dots2_ok ? w.tm2_wv_y[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_y[1].bytes : nullptr));
     } else {
@@ -2303,7 +2318,7 @@ fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_
   CK(cudaMemsetAsync(Y2.p, 0, sizeof(float) * 2 * nout, ctx->stream));
   CK(cudaStreamSynchronize(0));  // the legacy-stream uploads (weights, X) have landed
   TensorMap tm;
-  bool have_tm = D % 128 == 0 && lam_map(tm, X.as<float>(), nin, D, C, rows, 1);
+  bool have_tm = (D % 128 == 0 || (D == 64 && rows % 2 == 0)) && lam_map(tm, X.as<float>(), nin, D, C, rows, 1);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

@@ -186,6 +186,10 @@ struct LamGemm {
   const int* gather;
   const int* gather_slot;
   int gather_ld;
+  // M folding for D = 64 (M = 64 < the 128 TMEM lanes): when fold1 > 0, consecutive pairs of
+  // batch coordinate b[fold1 - 1] (e.g. two token rows) fill the upper / lower 64 lanes of one
+  // 128-row tile; the Λ tensor map then has a 64-wide box (umma_tmap_lam with dims[0] = 64)
+  int fold1;
 };
 bool umma_available();
 int umma_pick_bn(int N);  // 256 / 128 / 64, or 0 when N is not a multiple of 64

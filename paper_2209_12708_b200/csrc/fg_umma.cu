@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     b[1] = batch % p.nb[1];
     b[0] = batch / p.nb[1];
     if (p.gather) b[2] = p.gather[p.gather_slot[b[0]] * p.gather_ld + b[2]];
+    if (p.fold1) b[p.fold1 - 1] *= 2;  // the pair (b, b + 1) of the folded coordinate
     m0 = mt * (PAIR ? 2 : 1) * kBM + (int)rank * kBM;  // this CTA's first d-row
     n0 = nt * BN;
   };
@@ -286,8 +287,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             kl -= p.K0;
             plane = 1;
           }
-          tma_load_4d(smem + RL::kRawOff + r * RL::kL, &tm_lam, &rawfull[r], m0, lc1 + (p.kdim == 1 ? kl : 0),
-                      lc2 + (p.kdim == 2 ? kl : 0), lc3 + plane);
+          if (p.fold1) {  // two 64-row halves: batch coordinate b and b + 1
+            const int f = p.fold1 - 1;
+            for (int half = 0; half < 2; ++half) {
+              const int h1 = lc1 + half * p.lam_c[0][f], h2 = lc2 + half * p.lam_c[1][f],
+                        h3 = lc3 + half * p.lam_c[2][f];
+              tma_load_4d(smem + RL::kRawOff + r * RL::kL + half * (RL::kL / 2), &tm_lam, &rawfull[r], 0,
+                          h1 + (p.kdim == 1 ? kl : 0), h2 + (p.kdim == 2 ? kl : 0), h3 + plane);
+            }
+          } else {
+            tma_load_4d(smem + RL::kRawOff + r * RL::kL, &tm_lam, &rawfull[r], m0, lc1 + (p.kdim == 1 ? kl : 0),
+                        lc2 + (p.kdim == 2 ? kl : 0), lc3 + plane);
+          }
         }
       }
     }
@@ -351,8 +362,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* st = smem + s * RL::kOp;
         const float* raw = reinterpret_cast<const float*>(smem + RL::kRawOff + r * RL::kL);
         float v[kBK];
+        if (p.fold1) {  // raw = two [k][64] halves
+          const float* rh = raw + (d >> 6) * (kBK * 64) + (d & 63);
 #pragma unroll
-        for (int k = 0; k < kBK; ++k) v[k] = raw[k * kBM + d];
+          for (int k = 0; k < kBK; ++k) v[k] = rh[k * 64];
+        } else {
+#pragma unroll
+          for (int k = 0; k < kBK; ++k) v[k] = raw[k * kBM + d];
+        }
         // raw tile consumed: order these generic-proxy reads before the Λ producer's next TMA
         // (async-proxy) write into the same buffer, then release it
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -394,7 +411,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int b[4], m0, n0;
       decode(t, b, m0, n0);
       const int acc = it & 1;
-      const int dd = m0 + q * 32 + lane;
+      int dd = m0 + q * 32 + lane;
+      if (p.fold1) {  // lanes 64..127 hold the second of the folded pair (warp-uniform: q >> 1)
+        b[p.fold1 - 1] += q >> 1;
+        dd &= 63;
+      }
       float* out_b = p.out + lin5l(p.out_c, b) + dd;
       const float* res = p.res ? p.res + lin5l(p.res_c, b) + (long long)n0 * p.ldn_res + dd : nullptr;
       auto chunk_out = [&](int c) -> float* {
@@ -412,6 +433,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int NCH = BN / 32;
       float pa[32], pb[32];
       auto load_x = [&](int c, float (&dst)[32]) {
+        if (p.accumulate && (p.n_split & 31)) {  // plane boundary inside the chunk (see finish)
+          const int nb0 = n0 + c * 32;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            dst[j] = out_b[(long long)((nb0 + j) / p.n_split) * p.split_stride +
+                           (long long)((nb0 + j) % p.n_split) * p.ldn_out];
+          return;
+        }
         const float* xs = chunk_x(c);
 #pragma unroll
         for (int j = 0; j < 32; ++j) dst[j] = xs[j * xld];
@@ -433,8 +462,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) o[j] += rc[j * p.ldn_res];
         }
+        if (p.n_split & 31) {  // a plane boundary inside the chunk (n_split < 32, e.g. hd = 16)
+          const int nb0 = n0 + c * 32;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) __stcs(oc + j * p.ldn_out, o[j]);
+          for (int j = 0; j < 32; ++j)
+            __stcs(out_b + (long long)((nb0 + j) / p.n_split) * p.split_stride +
+                       (long long)((nb0 + j) % p.n_split) * p.ldn_out,
+                   o[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) __stcs(oc + j * p.ldn_out, o[j]);
+        }
       };
       if (has_x) {
         load_x(0, pa);
@@ -533,7 +571,9 @@ bool umma_tmap_lam(void* tm, const float* base, const unsigned long long dims[4]
   if (!enc || (kdim != 1 && kdim != 2)) return false;
   cuuint64_t dm[4] = {dims[0], dims[1], dims[2], dims[3]};
   cuuint64_t sd[3] = {strides_bytes[0], strides_bytes[1], strides_bytes[2]};
-  cuuint32_t box[4] = {kBM, kdim == 1 ? (cuuint32_t)kBK : 1u, kdim == 2 ? (cuuint32_t)kBK : 1u, 1};
+  // D = 64 (M folding, LamGemm::fold1): a 64-wide box, two loads fill one 128-row tile
+  const cuuint32_t bm = dims[0] == 64 ? 64u : (cuuint32_t)kBM;
+  cuuint32_t box[4] = {bm, kdim == 1 ? (cuuint32_t)kBK : 1u, kdim == 2 ? (cuuint32_t)kBK : 1u, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(static_cast<CUtensorMap*>(tm), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dm, sd,
              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -570,6 +610,13 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
       groups = (e && e[0] == '1') ? 1 : 2;
     }
     p.epi_groups = groups;
+  }
+  if (p.fold1) {  // D = 64: pairs of coordinate fold1 - 1 fill one 128-row tile
+    if (p.M != 64 || p.nb[p.fold1 - 1] % 2 || p.gather || p.K % kBK || p.K0 % kBK || bn <= 0 || p.N % bn)
+      return -1;
+    p.nb[p.fold1 - 1] /= 2;
+    p.M = kBM;
+    tm2_whi = tm2_wlo = nullptr;
   }
   if (p.M % kBM || p.K % kBK || p.K0 % kBK || bn <= 0 || p.N % bn) return -1;
   if (tm2_whi && tm2_wlo && p.M % (2 * kBM) == 0 && bn >= 64 && umma_pair_enabled()) {

@@ -13,6 +13,8 @@ SHAPES = [
     (2, 128, 384, 128),    # c2 QKV
     (1, 768, 256, 1536),   # c5-like N
     (5, 96, 128, 384),     # odd tile counts (3 k-blocks, 3 N tiles of 128)
+    (64, 64, 192, 64),     # c1 QKV: D = 64, token rows folded in pairs into the 128 TMEM lanes
+    (32, 128, 64, 64),     # c1 W2 (K = 128): folded
 ]
 
 
@@ -27,5 +29,15 @@ def test_umma_affine_matches_f64(ctx, rows, c, o, d):
 
 
 def test_umma_ineligible_shape_reports(ctx):
-    r = ctx.selftest_affine(2, 30, 64, 64)
+    r = ctx.selftest_affine(2, 30, 64, 64)  # C % 32 != 0
     assert r["err_umma"] == -1.0 and r["err_simt"] < 2e-6
+    r = ctx.selftest_affine(3, 64, 64, 64)  # D = 64 with an odd number of rows cannot fold
+    assert r["err_umma"] == -1.0
+
+
+def test_umma_bias_compensated(ctx):
+    """The epilogue's truncation compensation leaves the tcgen05 planes unbiased: the median
+    signed relative error of both planes stays well below the uncompensated 2-3e-6."""
+    for c in (256, 512):
+        r = ctx.selftest_affine(32, c, 256, 256, seed=c)
+        assert abs(r["bias_umma_centre"]) < 1e-6 and abs(r["bias_umma_radius"]) < 1e-6, r
