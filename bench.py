@@ -488,6 +488,8 @@ def main():
         "passes_per_sentence": statistics.mean(calls),
         "exact_probes_per_sentence": exact_probes / (B * args.steps),
         "exact_ms_share": exact_ms / dev_ms if dev_ms else 0.0,
+        "ambiguity_band": {"lo": st["band_lo"], "hi": st["band_hi"], "calibration_samples": st["band_samples"],
+                           "unit": "fraction of the two logits bounds' widths"},
         "e2e": {"value": e2e, "unit": "sentences/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches,

@@ -221,12 +221,15 @@ fg_status fg_bound_pass_exact(fg_model* model, const double* x, const int* posit
 
 /* Decision-exact verdicts.  fg_certify, fg_maxeps and fg_maxeps_spec decide every probe with
  * check_robust on the fused f32-Λ pass; a probe is AMBIGUOUS when for some class j != t its
- * margin m = lo_t - hi_j - margin lies in the error band of that pass,
- *   -kappa * W - f <= m <= kappa / 8 * W + f,   W = (hi_t - lo_t) + (hi_j - lo_j),
- *   f = 1e-11 * max(1, |lo_t|, |hi_j|)
- * (asymmetric like the measured error (m_f32 - m_exact) / W: [-3.0e-6, -7.5e-7] at c3,
- * [-1.3e-6, -8.9e-7] at c2 -- the fused pass is conservative -- DESIGN.md section 6).  Ambiguous probes are re-decided by fg_bound_pass_exact, so every
- * verdict is the reference's.  kappa = 0 turns the re-decision off (raw f32 verdicts). */
+ * margin m = lo_t - hi_j - margin lies in the model's error band of that pass,
+ *   band_lo * W - f <= m <= band_hi * W + f,   W = (hi_t - lo_t) + (hi_j - lo_j),
+ *   f = 1e-11 * max(1, |lo_t|, |hi_j|).
+ * The band starts at [-kappa, kappa / 8] and is calibrated per model: every re-decided probe
+ * gives a sample of (m_f32 - m_exact) / W, and after 16 samples the band is twice the observed
+ * extremes (where a verdict can flip: [min(err, 0), max(err, 0)] * W) plus 1e-7, never wider
+ * than the default, widened again by any later sample outside it.
+ * Ambiguous probes are re-decided by fg_bound_pass_exact, so every verdict is the reference's.
+ * kappa = 0 turns the re-decision off (raw f32 verdicts); setting kappa restarts calibration. */
 #define FG_DEFAULT_KAPPA 6e-6
 fg_status fg_model_set_exact_resolve(fg_model* model, double kappa);
 
@@ -333,6 +336,8 @@ typedef struct {
   double sentence_passes;/* sentence-passes executed (sum over passes of active slots) */
   int exact_probes;      /* probes re-decided by the exact pass (fg_model_set_exact_resolve) */
   double exact_ms;       /* time spent in those exact passes (included in device_ms) */
+  double band_lo, band_hi; /* the model's ambiguity band after the call (units of W) */
+  int band_samples;      /* re-decided probes it was calibrated on so far */
 } fg_run_stats;
 fg_status fg_last_run_stats(const fg_model* model, fg_run_stats* out);
 

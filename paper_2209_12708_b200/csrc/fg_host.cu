@@ -730,7 +730,12 @@ struct fg_model {
   fg_run_stats stats{};
   fgh::ShardState shard;  // column sharding of the perturbation dimension (fg_model_set_column_shard)
   DBuf params64;          // f64 weights on the device for the exact pass (uploaded on first use)
-  double kappa = FG_DEFAULT_KAPPA;  // ambiguity band of the decision-exact verdicts
+  double kappa = FG_DEFAULT_KAPPA;  // ambiguity band of the decision-exact verdicts (outer limit)
+  // per-model calibrated band [band_lo, band_hi] (units of the widths W), from the measured
+  // (m_f32 - m_exact) / W of this model's own re-decided probes (see ambiguous_verdict)
+  double band_lo = -FG_DEFAULT_KAPPA, band_hi = FG_DEFAULT_KAPPA / 8;
+  double err_min = 0.0, err_max = 0.0;
+  int err_samples = 0;
   int exact_probes = 0;   // per call: probes re-decided by the exact pass, and their time
   double exact_ms = 0.0;
   // asynchronous re-decisions (fg_maxeps): a low-priority side stream and reusable jobs
@@ -1398,22 +1403,56 @@ int default_slots(const fg_model* m, int S, int D) {
 // (FP32 SIMT), so a probe is ambiguous when  -kappa * W - f <= m <= kappa / 8 * W + f
 // (kappa = 6e-6: 2x the extreme).  Such a probe is re-decided by the exact pass, whose
 // arithmetic is the reference's.
-bool ambiguous_verdict(const double* lo, const double* hi, int C, int t, double margin, double kappa) {
-  if (!(kappa > 0.0)) return false;
+// The class j != t with the smallest margin and that margin / widths.
+int closest_class(const double* lo, const double* hi, int C, int t, double margin, double* m_out, double* w_out) {
+  int jb = -1;
   for (int j = 0; j < C; ++j) {
     if (j == t) continue;
     const double m = lo[t] - hi[j] - margin;
+    if (jb < 0 || m < *m_out) {
+      jb = j;
+      *m_out = m;
+      *w_out = (hi[t] - lo[t]) + (hi[j] - lo[j]);
+    }
+  }
+  return jb;
+}
+
+bool ambiguous_verdict(const fg_model* m, const double* lo, const double* hi, int C, int t, double margin) {
+  if (!(m->kappa > 0.0)) return false;
+  for (int j = 0; j < C; ++j) {
+    if (j == t) continue;
+    const double mg = lo[t] - hi[j] - margin;
     const double w = (hi[t] - lo[t]) + (hi[j] - lo[j]);
     const double floor64 = 1e-11 * std::max({1.0, std::fabs(lo[t]), std::fabs(hi[j])});
-    if (!(m > 0.125 * kappa * w + floor64) && !(m < -kappa * w - floor64))
+    if (!(mg > m->band_hi * w + floor64) && !(mg < m->band_lo * w - floor64))
       return true;  // NaN-safe: a non-finite margin is ambiguous
   }
   return false;
 }
 
-// First exact re-decision of a model: upload the f64 weights and map the stream-ordered pool up
-// to the exact pass's working set (about eight FFN-sized f64 tensors, capped at 4 GiB), so the
-// first ambiguous probe of a search does not pay for mapping fresh memory.
+// One re-decided probe's error sample (m_f32 - m_exact) / W.  After kCalibSamples samples the
+// model's band becomes twice the observed extremes (plus 1e-7), where a verdict can flip --
+// m_f32 in [min(err, 0), max(err, 0)] * W -- never wider than the default [-kappa, kappa / 8];
+// later samples keep widening it if they fall outside.
+constexpr int kCalibSamples = 16;
+void calibrate_band(fg_model* m, const double* lo32, const double* hi32, const double* lo64, const double* hi64,
+                    int C, int t) {
+  double m32 = 0.0, w = 0.0;
+  const int j = closest_class(lo32, hi32, C, t, 0.0, &m32, &w);
+  if (j < 0 || !(w > 0.0) || !std::isfinite(m32)) return;
+  const double m64 = lo64[t] - hi64[j];
+  if (!std::isfinite(m64)) return;
+  const double err = (m32 - m64) / w;
+  m->err_min = m->err_samples ? std::min(m->err_min, err) : err;
+  m->err_max = m->err_samples ? std::max(m->err_max, err) : err;
+  ++m->err_samples;
+  if (m->err_samples >= kCalibSamples) {
+    m->band_lo = std::max(-m->kappa, 2.0 * std::min(m->err_min, 0.0) - 1e-7);
+    m->band_hi = std::min(m->kappa / 8, 2.0 * std::max(m->err_max, 0.0) + 1e-7);
+  }
+}
+
 fg_status upload_params64(fg_model* m) {
   fg_ctx* ctx = m->ctx;
   if (m->params64.p) return FG_OK;
@@ -1437,7 +1476,7 @@ fg_status decide_probe(fg_model* m, const double* x_s, const int* pos_s, int wor
   ok = 0;
   if (ps != FG_OK) return FG_OK;
   fg_check_robust((size_t)C, lo, hi, (size_t)pred, margin, &ok);
-  if (!ambiguous_verdict(lo, hi, C, pred, margin, m->kappa)) return FG_OK;
+  if (!ambiguous_verdict(m, lo, hi, C, pred, margin)) return FG_OK;
   fg_ctx* ctx = m->ctx;
   if (fg_status st = upload_params64(m)) return st;
   std::vector<double> elo(C), ehi(C);
@@ -1459,7 +1498,10 @@ fg_status decide_probe(fg_model* m, const double* x_s, const int* pos_s, int wor
   m->exact_ms += ms;
   ps = (fg_status)est;
   ok = 0;
-  if (ps == FG_OK) fg_check_robust((size_t)C, elo.data(), ehi.data(), (size_t)pred, margin, &ok);
+  if (ps == FG_OK) {
+    fg_check_robust((size_t)C, elo.data(), ehi.data(), (size_t)pred, margin, &ok);
+    if (margin == 0.0) calibrate_band(m, lo, hi, elo.data(), ehi.data(), C, pred);
+  }
   return FG_OK;
 }
 
@@ -1485,6 +1527,8 @@ fgh::ExactJob* start_exact_job(fg_model* m, const double* x_s, const int* pos_s,
   if (!job) {
     auto j = std::make_unique<fgh::ExactJob>();
     const int C = m->cfg.classes, nsites = 3 * m->cfg.layers;
+    j->lo32.resize(C);
+    j->hi32.resize(C);
     if (cudaMallocHost(&j->host, sizeof(double) * 2 * C) != cudaSuccess ||
         cudaMallocHost(&j->hstat, sizeof(int) * (nsites + 1)) != cudaSuccess ||
         cudaEventCreate(&j->start) != cudaSuccess || cudaEventCreate(&j->done) != cudaSuccess) {
@@ -1524,7 +1568,10 @@ int finish_exact_job(fg_model* m, fgh::ExactJob* job, int pred, fg_status& ps) {
     if (job->hstat[i] != kStatusClear) ps = (job->hstat[i] & 15) == kCodeInval ? FG_EINVAL : FG_EDOMAIN;
   if (ps == FG_OK && job->hstat[job->nsites]) ps = FG_EDOMAIN;
   int ok = 0;
-  if (ps == FG_OK) fg_check_robust((size_t)job->classes, job->host, job->host + job->classes, (size_t)pred, 0.0, &ok);
+  if (ps == FG_OK) {
+    fg_check_robust((size_t)job->classes, job->host, job->host + job->classes, (size_t)pred, 0.0, &ok);
+    calibrate_band(m, job->lo32.data(), job->hi32.data(), job->host, job->host + job->classes, job->classes, pred);
+  }
   return ok;
 }
 
@@ -1706,7 +1753,7 @@ fg_status fg_bound_pass(fg_model* m, int S, const double* x, const int* position
   }
   cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(t0); cudaEventDestroy(t1);
   m->stats = fg_run_stats{total_ms, passes ? total_ms / passes : 0.0, passes, slots,
-                          ctx->launches - launches0, (double)S, 0, 0.0};
+                          ctx->launches - launches0, (double)S, 0, 0.0, m->band_lo, m->band_hi, m->err_samples};
   return st;
 }
 
@@ -1766,6 +1813,9 @@ fg_status fg_certify(fg_model* m, int S, const double* x, const int* positions, 
   }
   stats.exact_probes = m->exact_probes;
   stats.exact_ms = m->exact_ms;
+  stats.band_lo = m->band_lo;
+  stats.band_hi = m->band_hi;
+  stats.band_samples = m->err_samples;
   stats.device_ms += m->exact_ms;
   m->stats = stats;
   return FG_OK;
@@ -1957,9 +2007,11 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
       const double* plo = w.h_logits + (size_t)i * C;
       const double* phi = w.h_logits + (size_t)slots * C + (size_t)i * C;
       int ok = 0;
-      if (async_exact && t.phase != P_ZERO && ps == FG_OK && ambiguous_verdict(plo, phi, C, pred[s], 0.0, m->kappa)) {
+      if (async_exact && t.phase != P_ZERO && ps == FG_OK && ambiguous_verdict(m, plo, phi, C, pred[s], 0.0)) {
         fgh::ExactJob* job = start_exact_job(m, x + s * LE, positions + (size_t)s * words, words, norm, t.eps, s, st);
         if (st) break;
+        std::copy(plo, plo + C, job->lo32.begin());
+        std::copy(phi, phi + C, job->hi32.begin());
         pending.push_back(job);
         slot[i] = -1;  // waits out of its slot
         continue;
@@ -1986,7 +2038,8 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
   cudaEventElapsedTime(&total, c0, c1);
   cudaEventDestroy(c0); cudaEventDestroy(c1); cudaEventDestroy(e0); cudaEventDestroy(e1);
   m->stats = fg_run_stats{(double)total, passes ? pass_ms_sum / passes : 0.0, passes, slots,
-                          ctx->launches - launches0, sentence_passes, m->exact_probes, m->exact_ms};
+                          ctx->launches - launches0, sentence_passes, m->exact_probes, m->exact_ms,
+                          m->band_lo, m->band_hi, m->err_samples};
   return st;
 }
 
@@ -2178,7 +2231,8 @@ fg_status fg_maxeps_spec(fg_model* m, int S, const double* x, const int* positio
   for (int s = 0; s < S; ++s) predicted_out[s] = pred[s];
   *rounds_out = rounds;
   m->stats = fg_run_stats{(double)total, passes ? pass_ms_sum / passes : 0.0, passes, slots,
-                          ctx->launches - launches0, sentence_passes, m->exact_probes, m->exact_ms};
+                          ctx->launches - launches0, sentence_passes, m->exact_probes, m->exact_ms,
+                          m->band_lo, m->band_hi, m->err_samples};
   return st;
 }
 
@@ -2460,6 +2514,9 @@ fg_status fg_bound_pass_exact(fg_model* m, const double* x, const int* positions
 fg_status fg_model_set_exact_resolve(fg_model* m, double kappa) {
   if (!(kappa >= 0.0) || !std::isfinite(kappa)) return fail(m->ctx, FG_EINVAL, "fg_model_set_exact_resolve: kappa");
   m->kappa = kappa;
+  m->band_lo = -kappa;  // recalibrated from this model's next re-decisions
+  m->band_hi = kappa / 8;
+  m->err_samples = 0;
   return FG_OK;
 }
 

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "../../include/faith_gpu.h"
 
@@ -137,6 +138,7 @@ struct ExactJob {
   int sentence = -1;
   double eps = 0.0;
   bool busy = false;
+  std::vector<double> lo32, hi32;  // the fused pass's logits bounds of the probe (calibration)
 };
 
 // The word-level pass of one sentence in the exact precision mode (fg_exact_pass.cu).  With

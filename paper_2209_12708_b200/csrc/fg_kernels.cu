@@ -34,7 +34,7 @@ __host__ __device__ __forceinline__ int dual_norm(int p) {
   return p == NORM_L1 ? NORM_LINF : (p == NORM_L2 ? NORM_L2 : NORM_L1);
 }
 
-constexpr double kNormPad = 1.0 + 0x1p-20;
+constexpr double kNormPad = 1.0 + 0x1p-22;
 
 // Accumulates the q-norm partials of the upper (u = c + r) and lower (l = c - r) rows.
 template <int Q>
@@ -69,9 +69,9 @@ struct NormAcc {
       l = warp_sum(l);
     }
   }
-  // The finished norm carries an outward pad of 2^-20 (about one f32 GEMM's worth of rounding,
-  // DESIGN.md §6), so every concretization widens [lo, hi] by 2^-20 * eps * ||Λ|| beyond what the
-  // f32 Λ planes give: rounding in the f32 planes cannot pull a bound inside the exact one.
+  // The finished norm carries an outward pad of 2^-22 (four f32 ulps), so every
+  // concretization widens [lo, hi] by 2^-22 * eps * ||Λ|| beyond what the f32 Λ planes give: the
+  // f32 storage rounding of the planes cannot pull a bound inside the exact one.
   __device__ __forceinline__ double fin(double v) const { return (Q == NORM_L2 ? sqrt(v) : v) * kNormPad; }
 };
 

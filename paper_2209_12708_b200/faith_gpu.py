@@ -75,7 +75,8 @@ class Relaxation(NamedTuple):
 class RunStats(C.Structure):
     _fields_ = [("device_ms", C.c_double), ("pass_ms", C.c_double), ("passes", C.c_int), ("slots", C.c_int),
                 ("launches", C.c_uint64), ("sentence_passes", C.c_double), ("exact_probes", C.c_int),
-                ("exact_ms", C.c_double)]
+                ("exact_ms", C.c_double), ("band_lo", C.c_double), ("band_hi", C.c_double),
+                ("band_samples", C.c_int)]
 
 
 class FgConfig(C.Structure):
