@@ -739,7 +739,9 @@ struct fg_model {
   int exact_probes = 0;   // per call: probes re-decided by the exact pass, and their time
   double exact_ms = 0.0;
   // asynchronous re-decisions (fg_maxeps): a low-priority side stream and reusable jobs
-  cudaStream_t exact_stream = nullptr;
+  static constexpr int kExactStreams = 4;  // concurrent re-decisions (one exact pass fills ~half the FP64 pipe)
+  cudaStream_t exact_stream[kExactStreams] = {};
+  int exact_rr = 0;
   std::vector<std::unique_ptr<fgh::ExactJob>> jobs;
   ~fg_model() {
     for (auto& j : jobs) {
@@ -748,7 +750,8 @@ struct fg_model {
       if (j->start) cudaEventDestroy(j->start);
       if (j->done) cudaEventDestroy(j->done);
     }
-    if (exact_stream) cudaStreamDestroy(exact_stream);
+    for (cudaStream_t st : exact_stream)
+      if (st) cudaStreamDestroy(st);
   }
   // offsets of the layers in params (gen_synthetic order)
   size_t layer_off(int l) const {
@@ -1513,13 +1516,14 @@ fgh::ExactJob* start_exact_job(fg_model* m, const double* x_s, const int* pos_s,
   fg_ctx* ctx = m->ctx;
   st = upload_params64(m);
   if (st) return nullptr;
-  if (!m->exact_stream) {
+  if (!m->exact_stream[0]) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&m->exact_stream, cudaStreamNonBlocking, lo) != cudaSuccess) {
-      st = fail(ctx, FG_ECUDA, "exact side stream");
-      return nullptr;
-    }
+    for (cudaStream_t& es : m->exact_stream)
+      if (cudaStreamCreateWithPriority(&es, cudaStreamNonBlocking, lo) != cudaSuccess) {
+        st = fail(ctx, FG_ECUDA, "exact side stream");
+        return nullptr;
+      }
   }
   fgh::ExactJob* job = nullptr;
   for (auto& j : m->jobs)
@@ -1539,7 +1543,7 @@ fgh::ExactJob* start_exact_job(fg_model* m, const double* x_s, const int* pos_s,
     m->jobs.push_back(std::move(j));
   }
   fg_ctx side = *ctx;  // the same device, launches counted on the side stream
-  side.stream = m->exact_stream;
+  side.stream = m->exact_stream[m->exact_rr++ % fg_model::kExactStreams];
   side.launches = 0;
   cudaEventRecord(job->start, side.stream);
   st = fgh::exact_pass(&side, m->cfg, m->params64.as<double>(), x_s, pos_s, words, norm, eps, nullptr, nullptr,
@@ -2029,7 +2033,8 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
     if (!st) poll(false);
   }
   while (!pending.empty() && !st) poll(true);  // (an error left jobs in flight)
-  if (m->exact_stream) cudaStreamSynchronize(m->exact_stream);
+  for (cudaStream_t es : m->exact_stream)
+    if (es) cudaStreamSynchronize(es);
   if (!have_pred) pred = fut.get();
   for (int s = 0; s < S; ++s) predicted_out[s] = pred[s];
   CK(cudaEventRecord(c1, ctx->stream));
