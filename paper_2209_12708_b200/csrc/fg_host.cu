@@ -675,7 +675,8 @@ struct Workspace {
   bool dots2_ok = false;
   int bn_sim = 0, bn_simx = 0, bn_wvx = 0;
   bool dots_ok = false;
-  bool wv_fold = false;  // D = 64: only the P.V product on tcgen05, its query / feature rows folded in pairs
+  bool fold64 = false;  // D = 64: the McCormick GEMMs fold pairs of query tokens / keys / head features
+  int kp = 0;            // head dimension rounded up to the GEMM engine's 32-deep K steps
   long long crX = 0, crQKV = 0, crF = 0, crSC = 0;
   DBuf X_b, R1_b, QKV_b, SC_b, CTX_b, F_b;  // f64 lb/ub(/lo/hi) blocks
   DBuf pooled, pooled_b, coef;
@@ -835,35 +836,35 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot, Workspace* wsp =
   w.bn_simx = umma_pick_bn((int)(2 * L)); // Q.K^T x-side: both output planes in N = 2L
   w.bn_wvx = umma_pick_bn((int)(2 * hd)); // P.V x-side: N = 2hd
   w.dots_ok = false;
-  w.wv_fold = false;
-  // D = 64 (c1): the similarity product's folded coordinate (the query token) is gathered in layer
-  // 1 and its y-side contracts over hd (16 at c1, < one 32-deep K step), so it stays FP32 SIMT;
-  // the P.V product folds pairs of query tokens (x-side) / head features (y-side)
-  const bool wv_only = w.tm_ok && D == 64 && w.bn_sim > 0 && w.bn_wvx > 0 && L % 32 == 0 && (2 * hd) % 32 == 0 &&
-                       hd % 2 == 0 && L % 2 == 0;
-  if (wv_only || (w.tm_ok && D % 128 == 0 && w.bn_sim > 0 && w.bn_simx > 0 && w.bn_wvx > 0 && hd % 32 == 0 &&
-                  L % 32 == 0)) {
+  w.fold64 = false;
+  // head dimension padded to whole K steps (zero coefficients: c1's hd = 16 contracts over 32)
+  w.kp = (int)((hd + 31) / 32 * 32);
+  // D = 64 (c1) folds pairs of a batch coordinate into the 128 TMEM lanes, which a gathered
+  // coordinate cannot provide (one perturbed word), so the layer-1 products run dense there
+  const bool fold = D == 64;
+  if (w.tm_ok && (D % 128 == 0 || fold) && w.bn_sim > 0 && w.bn_simx > 0 && w.bn_wvx > 0 && L % 32 == 0 &&
+      (!fold || (L % 2 == 0 && hd % 2 == 0))) {
     const long long SH = (long long)S * H;
     bool ok = lam_map(w.tm_QKVk, w.QF.as<float>(), w.crQKV, D, (int)(3 * E), rows, 1) &&
               lam_map(w.tm_QKVrow, w.QF.as<float>(), w.crQKV, D, (int)(3 * E), rows, 2) &&
               lam_map(w.tm_SC, w.SC.as<float>(), w.crSC, D, (int)L, SH * L, 1);
     for (int part = 0; part < 2 && ok; ++part) {
-      CK(w.cf_sim_x[part].alloc(sizeof(float) * SH * 2 * L * 2 * hd));
-      CK(w.cf_sim_y[part].alloc(sizeof(float) * SH * 2 * L * hd));
+      CK(w.cf_sim_x[part].alloc(sizeof(float) * SH * 2 * L * 2 * w.kp));
+      CK(w.cf_sim_y[part].alloc(sizeof(float) * SH * 2 * L * w.kp));
       CK(w.cf_wv_x[part].alloc(sizeof(float) * SH * 2 * hd * 2 * L));
       CK(w.cf_wv_y[part].alloc(sizeof(float) * SH * 2 * L * L));
       // x-side coefficient arrays [SH][2 planes][rows][K] are read as [SH][2*rows][K]
-      ok = ok && (wv_only || (umma_tmap_wop(w.tm_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), (int)(2 * hd), (int)(2 * L), 1, (int)SH, w.bn_simx) &&
-                              umma_tmap_wop(w.tm_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), (int)hd, (int)L, 2, (int)SH, w.bn_sim))) &&
+      ok = ok && umma_tmap_wop(w.tm_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), 2 * w.kp, (int)(2 * L), 1, (int)SH, w.bn_simx) &&
+           umma_tmap_wop(w.tm_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), w.kp, (int)L, 2, (int)SH, w.bn_sim) &&
            umma_tmap_wop(w.tm_wv_x[part].bytes, w.cf_wv_x[part].as<float>(), (int)(2 * L), (int)(2 * hd), 1, (int)SH, w.bn_wvx) &&
            umma_tmap_wop(w.tm_wv_y[part].bytes, w.cf_wv_y[part].as<float>(), (int)L, (int)L, 2, (int)SH, w.bn_sim);
     }
-    w.dots_ok = ok && !wv_only;
-    w.wv_fold = ok && wv_only;
-    bool ok2 = w.dots_ok && w.bn_sim >= 64 && w.bn_simx >= 64 && w.bn_wvx >= 64;
+    w.dots_ok = ok;
+    w.fold64 = ok && fold;
+    bool ok2 = w.dots_ok && !fold && w.bn_sim >= 64 && w.bn_simx >= 64 && w.bn_wvx >= 64;
     for (int part = 0; part < 2 && ok2; ++part)
-      ok2 = umma_tmap_wop(w.tm2_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), (int)(2 * hd), (int)(2 * L), 1, (int)SH, w.bn_simx / 2) &&
-            umma_tmap_wop(w.tm2_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), (int)hd, (int)L, 2, (int)SH, w.bn_sim / 2) &&
+      ok2 = umma_tmap_wop(w.tm2_sim_x[part].bytes, w.cf_sim_x[part].as<float>(), 2 * w.kp, (int)(2 * L), 1, (int)SH, w.bn_simx / 2) &&
+            umma_tmap_wop(w.tm2_sim_y[part].bytes, w.cf_sim_y[part].as<float>(), w.kp, (int)L, 2, (int)SH, w.bn_sim / 2) &&
             umma_tmap_wop(w.tm2_wv_x[part].bytes, w.cf_wv_x[part].as<float>(), (int)(2 * L), (int)(2 * hd), 1, (int)SH, w.bn_wvx / 2) &&
             umma_tmap_wop(w.tm2_wv_y[part].bytes, w.cf_wv_y[part].as<float>(), (int)L, (int)L, 2, (int)SH, w.bn_sim / 2);
     w.dots2_ok = ok2;
@@ -984,7 +985,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     g_tag = "affine_gemm";
     if (l == 0 && onehot) {
       // Q/K rows at unperturbed tokens are never read in layer 1 on the gathered tcgen05 path
-      const bool gathered = !sharded && w.dots_ok && umma_dots_enabled() && !no_qk_skip();
+      const bool gathered = !sharded && w.dots_ok && !w.fold64 && umma_dots_enabled() && !no_qk_skip();
       LAUNCH(launch_onehot_affine(QKV, w.crQKV, lw.qkv.w32.as<float>(), w.pos_all.as<int>(), w.slot_map.as<int>(), S,
                                   L, E, 3 * E, w.W, D, w.col0, st, gathered ? 2 * E : 0));
     } else {
@@ -1017,13 +1018,13 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     const double scale = 1.0 / std::sqrt((double)hd);
     g_tag = "dot_similarity";
     if (w.dots_ok && umma_dots_enabled()) {
-      LAUNCH(launch_sim_coef_split(q, k, S, H, L, hd, w.cf_sim_x[0].as<float>(), w.cf_sim_x[1].as<float>(),
+      LAUNCH(launch_sim_coef_split(q, k, S, H, L, hd, w.kp, w.cf_sim_x[0].as<float>(), w.cf_sim_x[1].as<float>(),
                                    w.cf_sim_y[0].as<float>(), w.cf_sim_y[1].as<float>(), st));
       LAUNCH(launch_sim_bias(q, k, sc, S, H, L, hd, scale, st));
       // x-side: scores[s,h,i,j,:] = sum_k2 Cx[j,k2] (Qc|Qr)[i, h*hd + k2]   (K0 = hd: c|r concat)
       // (both output planes in one N = 2L range: n -> plane n / L, key j = n % L)
       LamGemm gx{};
-      gx.M = D; gx.N = 2 * L; gx.K = 2 * hd; gx.K0 = hd;
+      gx.M = D; gx.N = 2 * L; gx.K = 2 * w.kp; gx.K0 = w.kp;
       gx.nb[0] = S; gx.nb[1] = H; gx.nb[2] = L; gx.nb[3] = 1;
       gx.kdim = 1;
       gx.lam_c[0][1] = hd;                    // neuron h*hd (+k)
@@ -1034,7 +1035,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gx.ldn_out = D;
       gx.n_split = L; gx.split_stride = w.crSC;
       gx.alpha = (float)scale;
-      if (l == 0 && onehot) {
+      if (w.fold64) gx.fold1 = 3;  // pairs of query tokens i
+      if (l == 0 && onehot && !w.fold64) {
         // Q/K Λ rows vanish off the perturbed tokens: scores Λ[i, j] != 0 only for i or j
         // perturbed -> zero the scores, x-side terms for perturbed queries i, y-side terms for
         // perturbed keys j (gathered batch coordinate)
@@ -1048,7 +1050,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
                              w.dots2_ok ? w.tm2_sim_x[0].bytes : nullptr, w.dots2_ok ? w.tm2_sim_x[1].bytes : nullptr));
       // y-side: scores[s,h,i,j,:] += sum_k lx[i,k] K_p[j, E + h*hd + k]   (per plane p)
       LamGemm gy{};
-      gy.M = D; gy.N = L; gy.K = hd; gy.K0 = hd;
+      gy.M = D; gy.N = L; gy.K = w.kp; gy.K0 = w.kp;
       gy.nb[0] = S; gy.nb[1] = H; gy.nb[2] = L; gy.nb[3] = 2;
       gy.kdim = 1;
       gy.lam_c[0][1] = hd; gy.lam_c[0][4] = E;
@@ -1061,7 +1063,8 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gy.out_c[3] = w.crSC; gy.ldn_out = (long long)L * D;
       gy.alpha = (float)scale;
       gy.accumulate = 1;
-      if (l == 0 && onehot) {
+      if (w.fold64) gy.fold1 = 3;  // pairs of keys j
+      if (l == 0 && onehot && !w.fold64) {
         gy.nb[2] = w.W;
         gy.gather = w.pos_all.as<int>();
         gy.gather_slot = w.slot_map.as<int>();
@@ -1100,7 +1103,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     // ctx = DotProduct(probs, v)
     NView cx{CTX, w.crX, CTX_lb, CTX_ub, nullptr, nullptr, (long long)L * E, E, 0};
     g_tag = "dot_weighted";
-    if ((w.dots_ok || w.wv_fold) && umma_dots_enabled()) {
+    if (w.dots_ok && umma_dots_enabled()) {
       LAUNCH(launch_wv_coef_split(sc, v, S, H, L, hd, w.cf_wv_x[0].as<float>(), w.cf_wv_x[1].as<float>(),
                                   w.cf_wv_y[0].as<float>(), w.cf_wv_y[1].as<float>(), st));
       LAUNCH(launch_wv_bias(sc, v, cx, S, H, L, hd, st));
@@ -1117,7 +1120,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gx.ldn_out = D;
       gx.n_split = hd; gx.split_stride = w.crX;
       gx.alpha = 1.0f;
-      if (w.wv_fold) gx.fold1 = 3;  // pairs of query tokens i
+      if (w.fold64) gx.fold1 = 3;  // pairs of query tokens i
       LAUNCH(launch_lam_gemm(w.tm_SC.bytes, w.tm_wv_x[0].bytes, w.tm_wv_x[1].bytes, gx, w.bn_wvx, st,
                              w.dots2_ok ? w.tm2_wv_x[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_x[1].bytes : nullptr));
       // y-side: ctx[s,i,h*hd+k,:] += sum_j lx[i,j] V_p[j, 2E + h*hd + k]   (K along token rows)
@@ -1135,7 +1138,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gy.out_c[3] = w.crX; gy.ldn_out = (long long)E * D;
       gy.alpha = 1.0f;
       gy.accumulate = 1;
-      if (w.wv_fold) gy.fold1 = 3;  // pairs of head features k
+      if (w.fold64) gy.fold1 = 3;  // pairs of head features k
       LAUNCH(launch_lam_gemm(w.tm_QKVrow.bytes, w.tm_wv_y[0].bytes, w.tm_wv_y[1].bytes, gy, w.bn_sim, st,
                              w.dots2_ok ? w.tm2_wv_y[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_y[1].bytes : nullptr));
     } else {

@@ -210,7 +210,7 @@ int launch_ref_affine_f64(const float* W, const float* X, long long x_cr, double
 //   sim_y [S*H][2][L][hd]    y-side (lx, |lx| of Q rows i)
 //   wv_x  [S*H][2][hd][2L]   x-side of P.V (rows k, K = (c | r) of the P rows)
 //   wv_y  [S*H][2][L][L]     y-side (lx, |lx| of P, rows i, K = j)
-int launch_sim_coef_split(const NView& q, const NView& k, int S, int H, int L, int hd, float* x_hi,
+int launch_sim_coef_split(const NView& q, const NView& k, int S, int H, int L, int hd, int kp, float* x_hi,
                           float* x_lo, float* y_hi, float* y_lo, cudaStream_t st);
 int launch_wv_coef_split(const NView& p, const NView& v, int S, int H, int L, int hd, float* x_hi,
                          float* x_lo, float* y_hi, float* y_lo, cudaStream_t st);

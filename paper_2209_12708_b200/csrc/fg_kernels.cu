@@ -2757,22 +2757,35 @@ __device__ __forceinline__ void split_store(float* hi, float* lo, long long i, d
 }
 
 // McCormick coefficients of Q.K^T for the tcgen05 engine (K-major, see fg_internal.cuh).
-__global__ void sim_coef_split_kernel(NView q, NView k, int H, int L, int hd, float* xh, float* xl,
+// The contraction index k runs over kp >= hd (hd rounded up to the engine's 32-deep K steps);
+// coefficients of the padding k in [hd, kp) are zero, so the Λ rows the padded K reads past the
+// head (the next head's, finite) contribute exactly nothing.
+__global__ void sim_coef_split_kernel(NView q, NView k, int H, int L, int hd, int kp, float* xh, float* xl,
                                       float* yh, float* yl) {
   const int sh = blockIdx.x;
   const int s = sh / H, h = sh % H;
-  for (int t = threadIdx.x; t < L * hd; t += blockDim.x) {
-    const int j = t / hd, kk = t % hd;
+  for (int t = threadIdx.x; t < L * kp; t += blockDim.x) {
+    const int j = t / kp, kk = t % kp;
+    const long long x0 = ((long long)(sh * 2 + 0) * L + j) * 2 * kp, x1 = ((long long)(sh * 2 + 1) * L + j) * 2 * kp;
+    const long long y0 = ((long long)(sh * 2 + 0) * L + j) * kp + kk, y1 = ((long long)(sh * 2 + 1) * L + j) * kp + kk;
+    if (kk >= hd) {  // padding: zero coefficients
+      xh[x0 + kk] = xl[x0 + kk] = 0.f;
+      xh[x0 + kp + kk] = xl[x0 + kp + kk] = 0.f;
+      xh[x1 + kk] = xl[x1 + kk] = 0.f;
+      xh[x1 + kp + kk] = xl[x1 + kp + kk] = 0.f;
+      yh[y0] = yl[y0] = 0.f;
+      yh[y1] = yl[y1] = 0.f;
+      continue;
+    }
     const long long yi = nidx(k, s, j, h * hd + kk);
     const double ly = k.lo[yi], uy = k.hi[yi];
-    const long long x0 = ((long long)(sh * 2 + 0) * L + j) * 2 * hd, x1 = ((long long)(sh * 2 + 1) * L + j) * 2 * hd;
     split_store(xh, xl, x0 + kk, 0.5 * (ly + uy));
-    split_store(xh, xl, x0 + hd + kk, 0.5 * (fabs(uy) - fabs(ly)));
+    split_store(xh, xl, x0 + kp + kk, 0.5 * (fabs(uy) - fabs(ly)));
     split_store(xh, xl, x1 + kk, 0.5 * (uy - ly));
-    split_store(xh, xl, x1 + hd + kk, 0.5 * (fabs(uy) + fabs(ly)));
+    split_store(xh, xl, x1 + kp + kk, 0.5 * (fabs(uy) + fabs(ly)));
     const double lx = q.lo[nidx(q, s, j, h * hd + kk)];  // row i = j of Q
-    split_store(yh, yl, ((long long)(sh * 2 + 0) * L + j) * hd + kk, lx);
-    split_store(yh, yl, ((long long)(sh * 2 + 1) * L + j) * hd + kk, fabs(lx));
+    split_store(yh, yl, y0, lx);
+    split_store(yh, yl, y1, fabs(lx));
   }
 }
 
@@ -3253,9 +3266,9 @@ int launch_scale(const float* x, long long xcr, const double* xlb, const double*
   return 1;
 }
 
-int launch_sim_coef_split(const NView& q, const NView& k, int S, int H, int L, int hd, float* x_hi,
+int launch_sim_coef_split(const NView& q, const NView& k, int S, int H, int L, int hd, int kp, float* x_hi,
                           float* x_lo, float* y_hi, float* y_lo, cudaStream_t st) {
-  sim_coef_split_kernel<<<S * H, 256, 0, st>>>(q, k, H, L, hd, x_hi, x_lo, y_hi, y_lo);
+  sim_coef_split_kernel<<<S * H, 256, 0, st>>>(q, k, H, L, hd, kp, x_hi, x_lo, y_hi, y_lo);
   return 1;
 }
 
