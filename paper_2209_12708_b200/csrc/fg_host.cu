@@ -296,12 +296,17 @@ LamGemm affine_lam(const DevAffine& a, float* out, long long out_cr, const float
   return g;
 }
 
+// `skip_status` (per sentence slot, rows_per_slot token rows each): tiles of slots whose pass has
+// already failed are skipped (early exit, LamGemm::skip_status).
 int launch_affine_lambda(const DevAffine& a, const TensorMap* tm_in, const float* in, long long in_cr,
                          float* out, long long out_cr, const float* res, long long res_cr, long long rows,
-                         int D, cudaStream_t st) {
+                         int D, cudaStream_t st, const int* skip_status = nullptr, int rows_per_slot = 1) {
   if (a.umma && tm_in && umma_affine_enabled() && (D % 128 == 0 || (D == 64 && rows % 2 == 0))) {
-    return launch_lam_gemm(tm_in->bytes, a.tm_hi.bytes, a.tm_lo.bytes,
-                           affine_lam(a, out, out_cr, res, res_cr, rows, D), a.bn, st,
+    LamGemm g = affine_lam(a, out, out_cr, res, res_cr, rows, D);
+    g.skip_status = skip_status;
+    g.skip_div = rows_per_slot;
+    g.skip_slots = (int)(rows / rows_per_slot);
+    return launch_lam_gemm(tm_in->bytes, a.tm_hi.bytes, a.tm_lo.bytes, g, a.bn, st,
                            a.umma2 ? a.tm2_hi.bytes : nullptr, a.umma2 ? a.tm2_lo.bytes : nullptr);
   }
   return launch_gemm(affine_gemm(a, in, in_cr, out, out_cr, res, res_cr, rows, D), st);
@@ -689,13 +694,16 @@ struct Workspace {
   int* h_slot = nullptr;
   double* h_logits = nullptr;
   int* h_status = nullptr;
-  cudaGraphExec_t graph = nullptr;
-  int graph_norm = -1;
-  uint64_t graph_launches = 0;
+  // captured passes: [0] plain, [1] with early exit (the GEMMs skip slots that already failed)
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  int graph_norm[2] = {-1, -1};
+  uint64_t graph_launches[2] = {0, 0};
   ~Workspace() { release_host(); }
   void release_host() {
-    if (graph) cudaGraphExecDestroy(graph);
-    graph = nullptr;
+    for (auto& g : graph) {
+      if (g) cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
     if (h_eps) cudaFreeHost(h_eps);
     if (h_slot) cudaFreeHost(h_slot);
     if (h_logits) cudaFreeHost(h_logits);
@@ -942,7 +950,7 @@ fg_status concretize_site(fg_model* m, const float* lam, long long cr, const dou
 
 // One batched bound pass over the resident slots (graph.cpp:531-673 node order).
 // Reads ws.eps / ws.slot_map; writes ws.logits / ws.status.
-fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nullptr) {
+fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nullptr, bool early_exit = false) {
   fg_ctx* ctx = m->ctx;
   Workspace& w = wsp ? *wsp : m->ws;
   const fg_config& c = m->cfg;
@@ -966,6 +974,9 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
   double *S_lb = w.SC_b.as<double>(), *S_ub = S_lb + nSC, *S_lo = S_ub + nSC, *S_hi = S_lo + nSC;
   double* eps = w.eps.as<double>();
   int* status = w.status.as<int>();
+  // early exit: the GEMMs skip the tiles of slots whose pass already failed (a per-tile test
+  // that costs ~5 % of the GEMMs, so it is only on when a pass is expected to carry failures)
+  const int* skip = early_exit ? status : nullptr;
   double* dlo = w.dump_lo.as<double>();
   double* dhi = w.dump_hi.as<double>();
   const size_t per_layer = 8ull * L * E + 4ull * H * L * L + 2ull * H * L + 2ull * L * F;
@@ -990,7 +1001,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
                                   L, E, 3 * E, w.W, D, w.col0, st, gathered ? 2 * E : 0));
     } else {
       LAUNCH(launch_affine_lambda(lw.qkv, w.tm_ok ? &w.tm_X : nullptr, X, w.crX, QKV, w.crQKV, nullptr, 0,
-                                  (long long)S * L, D, st));
+                                  (long long)S * L, D, st, skip, L));
     }
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(X_lb, X_ub, lw.qkv.w64.as<double>(), lw.qkv.b64.as<double>(), nullptr,
@@ -1035,6 +1046,9 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gx.ldn_out = D;
       gx.n_split = L; gx.split_stride = w.crSC;
       gx.alpha = (float)scale;
+      gx.skip_status = sharded ? nullptr : skip;  // b[0] = sentence slot
+      gx.skip_div = 1;
+      gx.skip_slots = S;
       if (w.fold64) gx.fold1 = 3;  // pairs of query tokens i
       if (l == 0 && onehot && !w.fold64) {
         // Q/K Λ rows vanish off the perturbed tokens: scores Λ[i, j] != 0 only for i or j
@@ -1063,6 +1077,9 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gy.out_c[3] = w.crSC; gy.ldn_out = (long long)L * D;
       gy.alpha = (float)scale;
       gy.accumulate = 1;
+      gy.skip_status = sharded ? nullptr : skip;
+      gy.skip_div = 1;
+      gy.skip_slots = S;
       if (w.fold64) gy.fold1 = 3;  // pairs of keys j
       if (l == 0 && onehot && !w.fold64) {
         gy.nb[2] = w.W;
@@ -1120,6 +1137,9 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gx.ldn_out = D;
       gx.n_split = hd; gx.split_stride = w.crX;
       gx.alpha = 1.0f;
+      gx.skip_status = sharded ? nullptr : skip;
+      gx.skip_div = 1;
+      gx.skip_slots = S;
       if (w.fold64) gx.fold1 = 3;  // pairs of query tokens i
       LAUNCH(launch_lam_gemm(w.tm_SC.bytes, w.tm_wv_x[0].bytes, w.tm_wv_x[1].bytes, gx, w.bn_wvx, st,
                              w.dots2_ok ? w.tm2_wv_x[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_x[1].bytes : nullptr));
@@ -1138,6 +1158,9 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gy.out_c[3] = w.crX; gy.ldn_out = (long long)E * D;
       gy.alpha = 1.0f;
       gy.accumulate = 1;
+      gy.skip_status = sharded ? nullptr : skip;
+      gy.skip_div = 1;
+      gy.skip_slots = S;
       if (w.fold64) gy.fold1 = 3;  // pairs of head features k
       LAUNCH(launch_lam_gemm(w.tm_QKVrow.bytes, w.tm_wv_y[0].bytes, w.tm_wv_y[1].bytes, gy, w.bn_sim, st,
                              w.dots2_ok ? w.tm2_wv_y[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_y[1].bytes : nullptr));
@@ -1153,7 +1176,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     g_tag = "affine_gemm";
     const bool res0 = l == 0 && onehot;  // the Λ0 residual is a +1 scatter instead of a read
     LAUNCH(launch_affine_lambda(lw.wo, w.tm_ok ? &w.tm_CTX : nullptr, CTX, w.crX, R1, w.crX, res0 ? nullptr : X,
-                                res0 ? 0 : w.crX, (long long)S * L, D, st));
+                                res0 ? 0 : w.crX, (long long)S * L, D, st, skip, L));
     if (res0) LAUNCH(launch_add_onehot(R1, w.pos_all.as<int>(), w.slot_map.as<int>(), S, L, E, w.W, D, w.col0, st));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(CTX_lb, CTX_ub, lw.wo.w64.as<double>(), lw.wo.b64.as<double>(), X_lb, X_ub,
@@ -1165,7 +1188,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     // f1 = affine(res1, W1); act = ReluVerify/TanhVerify/SiluVerify(f1)
     g_tag = "affine_gemm";
     LAUNCH(launch_affine_lambda(lw.w1, w.tm_ok ? &w.tm_R1 : nullptr, R1, w.crX, Fl, w.crF, nullptr, 0,
-                                (long long)S * L, D, st));
+                                (long long)S * L, D, st, skip, L));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(R1_lb, R1_ub, lw.w1.w64.as<double>(), lw.w1.b64.as<double>(), nullptr,
                               nullptr, F_lb, F_ub, S, L, E, F, st));
@@ -1189,7 +1212,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     // cur = res1 + affine(act, W2)
     g_tag = "affine_gemm";
     LAUNCH(launch_affine_lambda(lw.w2, w.tm_ok ? &w.tm_F : nullptr, Fl, w.crF, X, w.crX, R1, w.crX,
-                                (long long)S * L, D, st));
+                                (long long)S * L, D, st, skip, L));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(F_lb, F_ub, lw.w2.w64.as<double>(), lw.w2.b64.as<double>(), R1_lb, R1_ub,
                               X_lb, X_ub, S, L, F, E, st));
@@ -1235,7 +1258,8 @@ bool use_graphs() {
 
 // Runs one pass over all slots; eps/slot_map must be staged in the pinned host
 // buffers.  Results land in w.h_logits / w.h_status after the call returns.
-fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, float* ms, Workspace* wsp = nullptr) {
+fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, float* ms, Workspace* wsp = nullptr,
+                   bool early_exit = false) {
   fg_ctx* ctx = m->ctx;
   Workspace& w = wsp ? *wsp : m->ws;
   cudaStream_t st = ctx->stream;
@@ -1244,26 +1268,27 @@ fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, floa
   CK(cudaMemcpyAsync(w.slot_map.p, w.h_slot, sizeof(int) * S, cudaMemcpyHostToDevice, st));
   if (ev0) CK(cudaEventRecord(ev0, st));
   if (use_graphs() && m->shard.capturable) {
-    if (!w.graph || w.graph_norm != norm) {
-      if (w.graph) cudaGraphExecDestroy(w.graph);
-      w.graph = nullptr;
+    const int gi = early_exit ? 1 : 0;
+    if (!w.graph[gi] || w.graph_norm[gi] != norm) {
+      if (w.graph[gi]) cudaGraphExecDestroy(w.graph[gi]);
+      w.graph[gi] = nullptr;
       cudaGraph_t g;
       uint64_t before = ctx->launches;
       CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      fg_status s = enqueue_pass(m, norm, nullptr, &w);
+      fg_status s = enqueue_pass(m, norm, nullptr, &w, early_exit);
       cudaError_t ce = cudaStreamEndCapture(st, &g);
       if (s) return s;
       if (ce != cudaSuccess) return fail(ctx, FG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-      CK(cudaGraphInstantiate(&w.graph, g, 0));
+      CK(cudaGraphInstantiate(&w.graph[gi], g, 0));
       cudaGraphDestroy(g);
-      w.graph_norm = norm;
-      w.graph_launches = ctx->launches - before;
+      w.graph_norm[gi] = norm;
+      w.graph_launches[gi] = ctx->launches - before;
       ctx->launches = before;
     }
-    CK(cudaGraphLaunch(w.graph, st));
-    ctx->launches += w.graph_launches;
+    CK(cudaGraphLaunch(w.graph[gi], st));
+    ctx->launches += w.graph_launches[gi];
   } else {
-    fg_status s = enqueue_pass(m, norm, nullptr, &w);
+    fg_status s = enqueue_pass(m, norm, nullptr, &w, early_exit);
     if (s) return s;
   }
   if (ev1) CK(cudaEventRecord(ev1, st));
@@ -1977,6 +2002,10 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
       block = false;
     }
   };
+  // early exit is switched on for a pass when at least a quarter of the previous pass's probes
+  // failed (domain / validation errors): deep random-init models (c4, c5) fail almost every probe
+  // above eps ~ 1e-7 part-way through the pass, c1-c3 almost none
+  bool early_exit = false;
   while (done < S && !st) {
     bool any = false;
     for (int i = 0; i < slots; ++i) {
@@ -1993,9 +2022,18 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
       continue;
     }
     float ms = 0.f;
-    if ((st = run_pass(m, norm, e0, e1, &ms))) break;
+    if ((st = run_pass(m, norm, e0, e1, &ms, nullptr, early_exit))) break;
     pass_ms_sum += ms;
     ++passes;
+    {
+      int active = 0, failed = 0;
+      for (int i = 0; i < slots; ++i)
+        if (slot[i] >= 0) {
+          ++active;
+          failed += decode_status(w.h_status[i]) != FG_OK;
+        }
+      early_exit = active > 0 && 4 * failed >= active;
+    }
     if (!have_pred) {
       pred = fut.get();
       have_pred = true;

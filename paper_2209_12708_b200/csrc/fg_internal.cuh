@@ -190,6 +190,12 @@ struct LamGemm {
   // batch coordinate b[fold1 - 1] (e.g. two token rows) fill the upper / lower 64 lanes of one
   // 128-row tile; the Λ tensor map then has a 64-wide box (umma_tmap_lam with dims[0] = 64)
   int fold1;
+  // early exit: tiles of a sentence slot whose status word is already set (a relaxation raised
+  // a domain / validation error earlier in the pass) are skipped; slot = b[0] / skip_div, for
+  // skip_slots <= 1024 slots (the kernel keeps a bitmask of them in shared memory)
+  const int* skip_status;
+  int skip_div, skip_slots;
+  int skip_tiles_per_b0, skip_b0_scale;  // set by launch_lam_gemm
 };
 bool umma_available();
 int umma_pick_bn(int N);  // 256 / 128 / 64, or 0 when N is not a multiple of 64

@@ -157,7 +157,8 @@ struct Ring {
   static constexpr int kOp = 2 * kWT + 2 * kL;
   static constexpr int kRawOff = S * kOp;
   static constexpr int kBarOff = kRawOff + R * kL;
-  static constexpr int kBytes = kBarOff + 256 + 1024;  // + barriers / TMEM slot + alignment slack
+  static constexpr int kMaskOff = kBarOff + 256;        // early-exit slot bitmask (32 words)
+  static constexpr int kBytes = kMaskOff + 128 + 1024;  // + barriers / TMEM slot, mask, alignment slack
   static_assert(kBytes <= 227 * 1024, "rings exceed shared memory");
   static_assert(3 * S + 2 * R + 4 <= 31, "barrier area");
 };
@@ -188,6 +189,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = p.K / kBK;
+  // slots whose pass already failed (early exit), one bit each; everything the per-tile test
+  // needs is re-read from the kernel parameters / shared memory (no registers held across the
+  // role loops: this kernel runs at its 128-register limit)
+  if (p.skip_tiles_per_b0)
+    for (int base = warp * 32; base < p.skip_slots; base += kThreads) {
+      const int slot = base + lane;
+      const uint32_t bits = __ballot_sync(0xffffffffu, slot < p.skip_slots && p.skip_status[slot] != kStatusClear);
+      if (lane == 0) reinterpret_cast<uint32_t*>(smem + RL::kMaskOff)[base >> 5] = bits;
+    }
   uint32_t rank = 0;
   if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -250,12 +260,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     m0 = mt * (PAIR ? 2 : 1) * kBM + (int)rank * kBM;  // this CTA's first d-row
     n0 = nt * BN;
   };
+  // every role skips the same tiles (the status words are not written during this kernel), so
+  // the stage / accumulator counters stay in step
+  // b[0] is the slowest tile coordinate: one division per tile, no full decode
+  auto skipped = [&](int t) -> bool {
+    if (!p.skip_tiles_per_b0) return false;
+    const int slot = (t / p.skip_tiles_per_b0) * p.skip_b0_scale / p.skip_div;
+    return (reinterpret_cast<const uint32_t*>(smem + RL::kMaskOff)[slot >> 5] >> (slot & 31)) & 1u;
+  };
 
   if (warp == 0) {
     // ---------------- W producer ----------------
     if (lane == 0) {
       int g = 0;
       for (int t = unit; t < num_tiles; t += nunits) {
+        if (skipped(t)) continue;
         int b[4], m0, n0;
         decode(t, b, m0, n0);
         const int wc2 = lin5(p.w_c[0], b), wc3 = lin5(p.w_c[1], b);
@@ -275,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int g = 0;
       for (int t = unit; t < num_tiles; t += nunits) {
+        if (skipped(t)) continue;
         int b[4], m0, n0;
         decode(t, b, m0, n0);
         const int lc1 = lin5(p.lam_c[0], b), lc2 = lin5(p.lam_c[1], b), lc3 = lin5(p.lam_c[2], b);
@@ -308,8 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // D f32, A/B tf32, both K-major, N = BN, M = 128 (256 for a pair)
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)((PAIR ? 2 : 1) * kBM >> 4) << 24);
-      int g = 0, it = 0;
-      for (int t = unit; t < num_tiles; t += nunits, ++it) {
+      int g = 0, it = -1;
+      for (int t = unit; t < num_tiles; t += nunits) {
+        if (skipped(t)) continue;
+        ++it;
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -355,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int d = threadIdx.x - 128;
     int g = 0;
     for (int t = unit; t < num_tiles; t += nunits) {
+      if (skipped(t)) continue;
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % S, r = g % R;
         mbar_wait(&rawfull[r], (g / R) & 1);
@@ -405,8 +428,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grp = (warp - 8) >> 2;
     const bool has_x = p.accumulate || p.res;
     const long long xld = p.accumulate ? p.ldn_out : p.ldn_res;
-    int it = 0;
-    for (int t = unit; t < num_tiles; t += nunits, ++it) {
+    int it = -1;
+    for (int t = unit; t < num_tiles; t += nunits) {
+      if (skipped(t)) continue;
+      ++it;
       if (p.epi_groups == 2 ? ((it & 1) != grp) : (grp != 0)) continue;
       int b[4], m0, n0;
       decode(t, b, m0, n0);
@@ -647,6 +672,11 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
   long long tiles = (long long)p.tiles_m * p.tiles_n * p.nb[0] * p.nb[1] * p.nb[2] * p.nb[3];
   if (tiles <= 0 || tiles > 0x7fffffff) return -1;
   p.num_tiles = (int)tiles;
+  p.skip_tiles_per_b0 = 0;  // early exit (see LamGemm::skip_status)
+  if (p.skip_status && p.skip_slots > 0 && p.skip_slots <= 1024 && p.skip_div > 0) {
+    p.skip_tiles_per_b0 = p.tiles_m * p.tiles_n * p.nb[1] * p.nb[2] * p.nb[3];
+    p.skip_b0_scale = p.fold1 == 1 ? 2 : 1;
+  }
   const int grid = (int)std::min<long long>(tiles, g_num_sms);
   switch (bn) {
     case 256: return launch_ring<256, 2, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
