@@ -934,11 +934,11 @@ fg_status shard_allreduce(fg_model* m, double* buf, size_t count, int norm) {
 // all-reduce -> finish when the perturbation columns are sharded.
 fg_status concretize_site(fg_model* m, const float* lam, long long cr, const double* lb, const double* ub,
                           long long rows_per_s, long long nrows, int D, int norm, const double* eps, double* lo,
-                          double* hi) {
+                          double* hi, const int* skip = nullptr) {
   fg_ctx* ctx = m->ctx;
   cudaStream_t st = ctx->stream;
   if (!m->shard.active()) {
-    LAUNCH(launch_concretize(lam, cr, lb, ub, rows_per_s, nrows, D, norm, eps, lo, hi, st));
+    LAUNCH(launch_concretize(lam, cr, lb, ub, rows_per_s, nrows, D, norm, eps, lo, hi, st, skip));
     return FG_OK;
   }
   double* part = m->ws.part.as<double>();
@@ -1005,7 +1005,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     }
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(X_lb, X_ub, lw.qkv.w64.as<double>(), lw.qkv.b64.as<double>(), nullptr,
-                              nullptr, Q_lb, Q_ub, S, L, E, 3 * E, st));
+                              nullptr, Q_lb, Q_ub, S, L, E, 3 * E, st, skip));
     g_tag = "concretize";
     // first layer under the one-hot binding: Q/K/V Λ rows are zero outside the perturbed tokens
     const bool sparse0 = l == 0 && onehot && !sharded;
@@ -1013,7 +1013,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       LAUNCH(launch_concretize_tokens(QKV, w.crQKV, Q_lb, Q_ub, (long long)L * 3 * E, nQKV, D, norm, eps, Q_lo, Q_hi,
                                       w.pos_all.as<int>(), w.slot_map.as<int>(), w.W, 3 * E, st));
     } else if (fg_status s = concretize_site(m, QKV, w.crQKV, Q_lb, Q_ub, (long long)L * 3 * E, nQKV, D, norm,
-                                             eps, Q_lo, Q_hi)) {
+                                             eps, Q_lo, Q_hi, skip)) {
       return s;
     }
     if (dump) {
@@ -1180,7 +1180,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     if (res0) LAUNCH(launch_add_onehot(R1, w.pos_all.as<int>(), w.slot_map.as<int>(), S, L, E, w.W, D, w.col0, st));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(CTX_lb, CTX_ub, lw.wo.w64.as<double>(), lw.wo.b64.as<double>(), X_lb, X_ub,
-                              R1_lb, R1_ub, S, L, E, E, st));
+                              R1_lb, R1_ub, S, L, E, E, st, skip));
     if (dump) {
       LAUNCH(launch_concretize(R1, w.crX, R1_lb, R1_ub, (long long)L * E, nX, D, norm, eps, dlo, dhi, st));
       if (fg_status s = dump->copy(base + off_ctx + 2ull * L * E, dlo, dhi, (size_t)L * E)) return s;
@@ -1191,12 +1191,12 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
                                 (long long)S * L, D, st, skip, L));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(R1_lb, R1_ub, lw.w1.w64.as<double>(), lw.w1.b64.as<double>(), nullptr,
-                              nullptr, F_lb, F_ub, S, L, E, F, st));
+                              nullptr, F_lb, F_ub, S, L, E, F, st, skip));
     g_tag = "act_verify";
     if (!sharded) {
       LAUNCH(launch_elementwise_verify(c.activation, Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm,
                                        eps, status, site(l, 2), dump ? F_lo : nullptr,
-                                       dump ? F_hi : nullptr, st));
+                                       dump ? F_hi : nullptr, st, nullptr, nullptr, skip));
     } else {
       if (fg_status s = concretize_site(m, Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm, eps, F_lo, F_hi))
         return s;
@@ -1215,7 +1215,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
                                 (long long)S * L, D, st, skip, L));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(F_lb, F_ub, lw.w2.w64.as<double>(), lw.w2.b64.as<double>(), R1_lb, R1_ub,
-                              X_lb, X_ub, S, L, F, E, st));
+                              X_lb, X_ub, S, L, F, E, st, skip));
     if (dump) {
       LAUNCH(launch_concretize(X, w.crX, X_lb, X_ub, (long long)L * E, nX, D, norm, eps, dlo, dhi, st));
       if (fg_status s = dump->copy(base + off_f1 + 2ull * L * F + (size_t)L * E, dlo, dhi, (size_t)L * E)) return s;

@@ -70,7 +70,7 @@ int launch_gemm(const GemmArgs& g, cudaStream_t st);
 
 int launch_concretize(const float* lam, long long cr, const double* lb, const double* ub,
                       long long rows_per_s, long long nrows, int D, int norm, const double* eps,
-                      double* lo, double* hi, cudaStream_t st);
+                      double* lo, double* hi, cudaStream_t st, const int* skip = nullptr);
 
 // concretize of token rows whose Λ is zero outside the perturbed tokens (first-layer Q/K/V)
 int launch_concretize_tokens(const float* lam, long long cr, const double* lb, const double* ub,
@@ -82,7 +82,7 @@ int launch_elementwise_verify(int kind, float* lam, long long cr, double* lb, do
                               long long rows_per_s, long long nrows, int D, int norm,
                               const double* eps, int* status, int site, double* lo_out,
                               double* hi_out, cudaStream_t st, const double* lo_in = nullptr,
-                              const double* hi_in = nullptr);
+                              const double* hi_in = nullptr, const int* skip = nullptr);
 
 // Standalone envelope / compose (operator-level API).
 int launch_relax(int kind, const double* lo, const double* hi, long long n, double* a_low,
@@ -97,7 +97,7 @@ int launch_compose(float* lam_in, long long cr_in, const double* lb_in, const do
 int launch_affine_bias(const double* lb_in, const double* ub_in, const double* w64,
                        const double* bias, const double* res_lb, const double* res_ub,
                        double* lb_out, double* ub_out, int S, int rows, int C, int O,
-                       cudaStream_t st);
+                       cudaStream_t st, const int* skip = nullptr);
 
 // Pairwise-similarity McCormick dot product Q.K^T (relax.cpp:573-617) scaled by `scale`
 // (the following Scale node, model.cpp:416-418).  out: [S, H, L, L] neurons.

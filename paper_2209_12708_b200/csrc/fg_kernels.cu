@@ -84,6 +84,11 @@ __device__ __forceinline__ void set_status(int* status, int s, int site, int cod
   atomicMin(status + s, (site << 4) | code);
 }
 
+// Early exit (enqueue_pass' `skip`): this slot's pass already failed, its later results are unused.
+__device__ __forceinline__ bool slot_failed(const int* skip, long long s) {
+  return skip != nullptr && skip[s] != kStatusClear;
+}
+
 // ---------------------------------------------------------------------------
 // Envelope lines in f64 (relax.cpp:12-108, 313-468).  Return 0, kCodeInval or
 // kCodeDomain exactly where the reference throws.
@@ -335,10 +340,10 @@ __global__ void __launch_bounds__(256) concretize_kernel(const float* __restrict
                                                          long long rows_per_s, long long nrows, int D,
                                                          const double* __restrict__ eps,
                                                          double* __restrict__ lo,
-                                                         double* __restrict__ hi) {
+                                                         double* __restrict__ hi, const int* __restrict__ skip) {
   long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
   int lane = threadIdx.x & (kWarp - 1);
-  if (row >= nrows) return;
+  if (row >= nrows || slot_failed(skip, row / rows_per_s)) return;
   const float* c = lam + row * D;
   const float* r = c + cr;
   NormAcc<Q> acc;
@@ -444,10 +449,10 @@ __global__ void __launch_bounds__(256) elementwise_verify_kernel(
     int kind, float* __restrict__ lam, long long cr, double* __restrict__ lb, double* __restrict__ ub,
     long long rows_per_s, long long nrows, int D, const double* __restrict__ eps,
     int* __restrict__ status, int site, double* __restrict__ lo_out, double* __restrict__ hi_out,
-    const double* __restrict__ lo_in, const double* __restrict__ hi_in) {
+    const double* __restrict__ lo_in, const double* __restrict__ hi_in, const int* __restrict__ skip) {
   long long row = (long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp;
   int lane = threadIdx.x & (kWarp - 1);
-  if (row >= nrows) return;
+  if (row >= nrows || slot_failed(skip, row / rows_per_s)) return;
   float* c = lam + row * D;
   float* r = c + cr;
   long long s = row / rows_per_s;
@@ -498,11 +503,13 @@ __global__ void __launch_bounds__(256) concretize_rows2_kernel(const float* __re
                                                                const double* __restrict__ lb,
                                                                const double* __restrict__ ub, long long rows_per_s,
                                                                long long nrows, int D, const double* __restrict__ eps,
-                                                               double* __restrict__ lo, double* __restrict__ hi) {
+                                                               double* __restrict__ lo, double* __restrict__ hi,
+                                                               const int* __restrict__ skip) {
   const long long row0 = 2 * ((long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp);
   const int lane = threadIdx.x & (kWarp - 1);
   if (row0 >= nrows) return;
   const bool two = row0 + 1 < nrows;
+  if (slot_failed(skip, row0 / rows_per_s) && (!two || slot_failed(skip, (row0 + 1) / rows_per_s))) return;
   NormAcc<Q> acc[2];
   for (int d = lane * 4; d < D; d += 4 * kWarp) {
     const float* c0 = lam + row0 * D + d;
@@ -533,11 +540,12 @@ template <int Q>
 __global__ void __launch_bounds__(256) elementwise_verify_rows2_kernel(
     int kind, float* __restrict__ lam, long long cr, double* __restrict__ lb, double* __restrict__ ub,
     long long rows_per_s, long long nrows, int D, const double* __restrict__ eps, int* __restrict__ status, int site,
-    double* __restrict__ lo_out, double* __restrict__ hi_out) {
+    double* __restrict__ lo_out, double* __restrict__ hi_out, const int* __restrict__ skip) {
   const long long row0 = 2 * ((long long)blockIdx.x * (blockDim.x / kWarp) + threadIdx.x / kWarp);
   const int lane = threadIdx.x & (kWarp - 1);
   if (row0 >= nrows) return;
   const int nr = row0 + 1 < nrows ? 2 : 1;
+  if (slot_failed(skip, row0 / rows_per_s) && (nr == 1 || slot_failed(skip, (row0 + 1) / rows_per_s))) return;
   NormAcc<Q> acc[2];
   for (int d = lane * 4; d < D; d += 4 * kWarp) {
     const float* c0 = lam + row0 * D + d;
@@ -629,10 +637,15 @@ constexpr int kBiasChunk = 256;  // input neurons staged in SMEM per step
 __global__ void __launch_bounds__(kBiasCols) affine_bias_kernel(
     const double* __restrict__ lb_in, const double* __restrict__ ub_in, const double* __restrict__ w,
     const double* __restrict__ bias, const double* __restrict__ res_lb, const double* __restrict__ res_ub,
-    double* __restrict__ lb_out, double* __restrict__ ub_out, long long nrows, int C, int O) {
+    double* __restrict__ lb_out, double* __restrict__ ub_out, long long nrows, int C, int O,
+    const int* __restrict__ skip, int rows_per_slot) {
   __shared__ double2 xs[kBiasRows][kBiasChunk];  // (lb, ub) of the CTA's rows
   const int j = blockIdx.x * kBiasCols + threadIdx.x;
   const long long r0 = (long long)blockIdx.y * kBiasRows;
+  // every row of the CTA in failed slots (block-uniform test)
+  if (skip && slot_failed(skip, r0 / rows_per_slot) &&
+      slot_failed(skip, (min(r0 + kBiasRows, nrows) - 1) / rows_per_slot))
+    return;
   double ub_acc[kBiasRows], lb_acc[kBiasRows];
 #pragma unroll
   for (int r = 0; r < kBiasRows; ++r) ub_acc[r] = lb_acc[r] = 0.0;
@@ -2835,16 +2848,17 @@ bool rows2_enabled() {  // comparison runs: FG_NO_ROWS2=1 keeps one row per warp
 
 int launch_concretize(const float* lam, long long cr, const double* lb, const double* ub,
                       long long rows_per_s, long long nrows, int D, int norm, const double* eps,
-                      double* lo, double* hi, cudaStream_t st) {
+                      double* lo, double* hi, cudaStream_t st, const int* skip) {
   if (nrows <= 0) return 0;
   if (rows2_enabled() && D % 4 == 0 && D <= 256) {
     DISPATCH_Q(dual_norm(norm), concretize_rows2_kernel,
-               <<<blocks_for((nrows + 1) / 2, 8), 256, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi));
+               <<<blocks_for((nrows + 1) / 2, 8), 256, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi,
+                                                                 skip));
     return 1;
   }
   dim3 grid(blocks_for(nrows, 8)), block(256);
   DISPATCH_Q(dual_norm(norm), concretize_kernel,
-             <<<grid, block, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi));
+             <<<grid, block, 0, st>>>(lam, cr, lb, ub, rows_per_s, nrows, D, eps, lo, hi, skip));
   return 1;
 }
 
@@ -2871,18 +2885,19 @@ int launch_concretize_tokens(const float* lam, long long cr, const double* lb, c
 int launch_elementwise_verify(int kind, float* lam, long long cr, double* lb, double* ub,
                               long long rows_per_s, long long nrows, int D, int norm,
                               const double* eps, int* status, int site, double* lo_out,
-                              double* hi_out, cudaStream_t st, const double* lo_in, const double* hi_in) {
+                              double* hi_out, cudaStream_t st, const double* lo_in, const double* hi_in,
+                              const int* skip) {
   if (nrows <= 0) return 0;
   if (rows2_enabled() && !lo_in && D % 4 == 0 && D <= 256) {
     DISPATCH_Q(dual_norm(norm), elementwise_verify_rows2_kernel,
                <<<blocks_for((nrows + 1) / 2, 8), 256, 0, st>>>(kind, lam, cr, lb, ub, rows_per_s, nrows, D, eps,
-                                                                 status, site, lo_out, hi_out));
+                                                                 status, site, lo_out, hi_out, skip));
     return 1;
   }
   dim3 grid(blocks_for(nrows, 8)), block(256);
   DISPATCH_Q(dual_norm(norm), elementwise_verify_kernel,
              <<<grid, block, 0, st>>>(kind, lam, cr, lb, ub, rows_per_s, nrows, D, eps, status,
-                                      site, lo_out, hi_out, lo_in, hi_in));
+                                      site, lo_out, hi_out, lo_in, hi_in, skip));
   return 1;
 }
 
@@ -2907,13 +2922,13 @@ int launch_compose(float* lam_in, long long cr_in, const double* lb_in, const do
 int launch_affine_bias(const double* lb_in, const double* ub_in, const double* w64,
                        const double* bias, const double* res_lb, const double* res_ub,
                        double* lb_out, double* ub_out, int S, int rows, int C, int O,
-                       cudaStream_t st) {
+                       cudaStream_t st, const int* skip) {
   long long nrows = (long long)S * rows;
   long long total = nrows * O;
   if (total <= 0) return 0;
   dim3 grid(blocks_for(O, kBiasCols), blocks_for(nrows, kBiasRows));
   affine_bias_kernel<<<grid, kBiasCols, 0, st>>>(lb_in, ub_in, w64, bias, res_lb, res_ub, lb_out, ub_out, nrows,
-                                                 C, O);
+                                                 C, O, skip, rows);
   return 1;
 }
 
