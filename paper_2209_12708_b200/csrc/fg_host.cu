@@ -686,12 +686,14 @@ struct Workspace {
   DBuf X_b, R1_b, QKV_b, SC_b, CTX_b, F_b;  // f64 lb/ub(/lo/hi) blocks
   DBuf pooled, pooled_b, coef;
   DBuf eps, status, logits, slot_map, x_all, pos_all;
+  DBuf active;  // per slot: 1 = holds a probe this pass, 0 = idle (status kStatusIdle, skipped)
   DBuf dump_lo, dump_hi;
   // column-sharded pass: concretization partials and the softmax chain's phase buffers
   int col0 = 0;
   DBuf part, sm_ex, sm_sig, sm_rows, head_part;
   double* h_eps = nullptr;  // pinned
   int* h_slot = nullptr;
+  int* h_active = nullptr;  // all 1 outside fg_maxeps
   double* h_logits = nullptr;
   int* h_status = nullptr;
   // captured passes: [0] plain, [1] with early exit (the GEMMs skip slots that already failed)
@@ -706,10 +708,12 @@ struct Workspace {
     }
     if (h_eps) cudaFreeHost(h_eps);
     if (h_slot) cudaFreeHost(h_slot);
+    if (h_active) cudaFreeHost(h_active);
     if (h_logits) cudaFreeHost(h_logits);
     if (h_status) cudaFreeHost(h_status);
     h_eps = nullptr;
     h_slot = nullptr;
+    h_active = nullptr;
     h_logits = nullptr;
     h_status = nullptr;
   }
@@ -809,6 +813,7 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot, Workspace* wsp =
   CK(w.status.alloc(sizeof(int) * S));
   CK(w.logits.alloc(sizeof(double) * 2 * S * c.classes));
   CK(w.slot_map.alloc(sizeof(int) * S));
+  CK(w.active.alloc(sizeof(int) * S));
   CK(w.x_all.alloc(sizeof(double) * (size_t)std::max(Ntot, 1) * L * E));
   CK(w.pos_all.alloc(sizeof(int) * (size_t)std::max(Ntot, 1) * W));
   size_t dmax = std::max({(size_t)nQKV, (size_t)nF, (size_t)nSC});
@@ -824,6 +829,9 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot, Workspace* wsp =
   }
   CK(cudaMallocHost(&w.h_eps, sizeof(double) * S));
   CK(cudaMallocHost(&w.h_slot, sizeof(int) * S));
+  CK(cudaMallocHost(&w.h_active, sizeof(int) * S));
+  std::fill(w.h_active, w.h_active + S, 1);
+  CK(cudaMemcpy(w.active.p, w.h_active, sizeof(int) * S, cudaMemcpyHostToDevice));
   CK(cudaMallocHost(&w.h_logits, sizeof(double) * 2 * S * c.classes));
   CK(cudaMallocHost(&w.h_status, sizeof(int) * S));
   w.S = S;
@@ -983,7 +991,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
   auto site = [](int l, int k) { return l * 8 + k; };
 
   g_tag = "init";
-  LAUNCH(launch_fill_int(status, kStatusClear, S, st));
+  LAUNCH(launch_init_status(status, w.active.as<int>(), S, st));
   // Λ0 is one-hot: the first layer consumes it analytically (no Λ0 in HBM) unless dumping
   const bool onehot = !dump && onehot_first_layer();
   LAUNCH(launch_init_input(onehot ? nullptr : X, w.crX, X_lb, X_ub, w.x_all.as<double>(), w.pos_all.as<int>(),
@@ -1266,6 +1274,7 @@ fg_status run_pass(fg_model* m, int norm, cudaEvent_t ev0, cudaEvent_t ev1, floa
   const int S = w.S, C = m->cfg.classes;
   CK(cudaMemcpyAsync(w.eps.p, w.h_eps, sizeof(double) * S, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(w.slot_map.p, w.h_slot, sizeof(int) * S, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(w.active.p, w.h_active, sizeof(int) * S, cudaMemcpyHostToDevice, st));
   if (ev0) CK(cudaEventRecord(ev0, st));
   if (use_graphs() && m->shard.capturable) {
     const int gi = early_exit ? 1 : 0;
@@ -1806,6 +1815,8 @@ fg_status fg_bound_pass_dump(fg_model* m, const double* x, const int* positions,
   w.h_slot[0] = 0;
   CK(cudaMemcpyAsync(w.eps.p, w.h_eps, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(w.slot_map.p, w.h_slot, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  w.h_active[0] = 1;
+  CK(cudaMemcpyAsync(w.active.p, w.h_active, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   Dumper d{node_lo, node_hi, ctx};
   if ((st = enqueue_pass(m, norm, &d))) return st;
   const int C = m->cfg.classes;
@@ -2008,21 +2019,26 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
   bool early_exit = false;
   while (done < S && !st) {
     bool any = false;
+    int idle = 0;
     for (int i = 0; i < slots; ++i) {
       if (slot[i] < 0 && ready_head < ready.size()) slot[i] = ready[ready_head++];
       while (slot[i] < 0 && next < S && sent[next].phase == P_DONE) ++next;
       if (slot[i] < 0 && next < S) slot[i] = next++;
       int s = slot[i];
       any = any || s >= 0;
+      idle += s < 0;
       w.h_slot[i] = s >= 0 ? s : 0;
       w.h_eps[i] = s >= 0 ? sent[s].eps : 0.0;
+      w.h_active[i] = s >= 0;
     }
     if (!any) {  // every remaining sentence waits for its exact verdict
       poll(true);
       continue;
     }
     float ms = 0.f;
-    if ((st = run_pass(m, norm, e0, e1, &ms, nullptr, early_exit))) break;
+    // idle slots (finished sentences, or ones waiting for an exact verdict) are skipped like
+    // failed ones: the tail of a batch, when few sentences remain, costs only their tiles
+    if ((st = run_pass(m, norm, e0, e1, &ms, nullptr, early_exit || 4 * idle >= slots))) break;
     pass_ms_sum += ms;
     ++passes;
     {
@@ -2074,6 +2090,8 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
     if (!st) poll(false);
   }
   while (!pending.empty() && !st) poll(true);  // (an error left jobs in flight)
+  std::fill(w.h_active, w.h_active + slots, 1);  // every other entry point runs all slots
+  cudaMemcpyAsync(w.active.p, w.h_active, sizeof(int) * slots, cudaMemcpyHostToDevice, ctx->stream);
   for (cudaStream_t es : m->exact_stream)
     if (es) cudaStreamSynchronize(es);
   if (!have_pred) pred = fut.get();
@@ -2183,9 +2201,10 @@ fg_status fg_maxeps_spec(fg_model* m, int S, const double* x, const int* positio
         const SpecProbe& pr = probes[mine[b0 + std::min((size_t)i, nb - 1)]];
         w.h_slot[i] = pr.sent;
         w.h_eps[i] = pr.eps;
+        w.h_active[i] = (size_t)i < nb;  // padding slots of a short batch: skipped
       }
       float ms = 0.f;
-      if ((st = run_pass(m, norm, e0, e1, &ms))) break;
+      if ((st = run_pass(m, norm, e0, e1, &ms, nullptr, 4 * (slots - (int)nb) >= slots))) break;
       pass_ms_sum += ms;
       ++passes;
       sentence_passes += (double)nb;
@@ -2266,6 +2285,8 @@ fg_status fg_maxeps_spec(fg_model* m, int S, const double* x, const int* positio
       }
     }
   }
+  std::fill(w.h_active, w.h_active + slots, 1);
+  cudaMemcpyAsync(w.active.p, w.h_active, sizeof(int) * slots, cudaMemcpyHostToDevice, ctx->stream);
   cudaEventRecord(c1, ctx->stream);
   cudaEventSynchronize(c1);
   float total = 0.f;  // the whole call, host-side forward / exchanges / exact passes included

@@ -20,6 +20,9 @@ namespace fg {
 // EINVAL (1) beats EDOMAIN (2) because ConcreteBounds::validate runs over all
 // neurons before any domain check (relax.cpp:314-335, 364-392, 397-410).
 constexpr int kStatusClear = 0x7fffffff;
+// status of a slot that holds no probe in this pass (fg_maxeps: its sentence finished or waits
+// for an exact re-decision): not clear, so every early-exit kernel skips it
+constexpr int kStatusIdle = 0x7ffffffe;
 constexpr int kCodeInval = 1;
 constexpr int kCodeDomain = 2;
 
@@ -148,6 +151,8 @@ int launch_scale(const float* x, long long xcr, const double* xlb, const double*
                  float* y, long long ycr, double* ylb, double* yub, long long n, int D,
                  cudaStream_t st);
 int launch_fill_int(int* p, int v, long long n, cudaStream_t st);
+// status[i] = active[i] ? kStatusClear : kStatusIdle (start of a pass)
+int launch_init_status(int* status, const int* active, int n, cudaStream_t st);
 
 // ---- tcgen05 3xTF32 engine for Λ contractions (fg_umma.cu) ---------------------------
 // Out_b[n, d] (+)= alpha * sum_k Wop_b[n, k] * Λ_b[k, d] (+ R_b[n, d]), computed as

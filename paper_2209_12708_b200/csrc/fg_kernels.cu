@@ -3310,6 +3310,16 @@ int launch_fill_int(int* p, int v, long long n, cudaStream_t st) {
   return 1;
 }
 
+__global__ void init_status_kernel(int* status, const int* active, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) status[i] = active[i] ? kStatusClear : kStatusIdle;
+}
+
+int launch_init_status(int* status, const int* active, int n, cudaStream_t st) {
+  init_status_kernel<<<(n + 255) / 256, 256, 0, st>>>(status, active, n);
+  return 1;
+}
+
 // ===========================================================================
 // Column-sharded pass: rank r owns perturbation columns [col0, col0 + D)
 // of every Λ.  Every column-separable op is unchanged; each concretization becomes

@@ -204,7 +204,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int tiles_m = PAIR ? p.tiles_m / 2 : p.tiles_m;
   const int num_tiles = PAIR ? p.num_tiles / 2 : p.num_tiles;
-  constexpr int kGather = PAIR ? 256 : 128;  // split / epilogue threads reporting to the (leader) CTA
+  // arrivals on the leader's split / tempty barriers: every split / epilogue thread of a single
+  // CTA; one elected thread per CTA of a pair (after a named barrier of its 128 threads: remote
+  // mbarrier arrivals cross the cluster's DSMEM path, 128 of them per stage serialise)
+  constexpr int kGather = PAIR ? 2 : 128;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -412,9 +415,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<float4*>(st + RL::kLlo + off) = make_float4(l[0], l[1], l[2], l[3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_wait(&wfull[s], (g / S) & 1);  // this CTA's W tile landed too
-        if (PAIR) mbar_arrive_cta0(&split[s]);
-        else mbar_arrive(&split[s]);
+        if (PAIR) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (d == 0) {
+            mbar_wait(&wfull[s], (g / S) & 1);  // this CTA's W tile landed too
+            mbar_arrive_cta0(&split[s]);
+          }
+        } else {
+          mbar_wait(&wfull[s], (g / S) & 1);  // this CTA's W tile landed too
+          mbar_arrive(&split[s]);
+        }
       }
     }
   } else if (warp >= 8) {
@@ -515,8 +525,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      if (PAIR) mbar_arrive_cta0(&tempty[acc]);
-      else mbar_arrive(&tempty[acc]);
+      if (PAIR) {
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + grp) : "memory");
+        if ((threadIdx.x & 127) == 0) mbar_arrive_cta0(&tempty[acc]);
+      } else {
+        mbar_arrive(&tempty[acc]);
+      }
     }
   }
 
@@ -655,6 +669,11 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
     long long tiles = (long long)p.tiles_m * p.tiles_n * p.nb[0] * p.nb[1] * p.nb[2] * p.nb[3];
     if (tiles <= 0 || tiles > 0x7fffffff) return -1;
     p.num_tiles = (int)tiles;  // single-CTA tiles; the pair kernel walks tiles / 2 pair tiles
+    p.skip_tiles_per_b0 = 0;
+    if (p.skip_status && p.skip_slots > 0 && p.skip_slots <= 1024 && p.skip_div > 0) {
+      p.skip_tiles_per_b0 = p.tiles_m / 2 * p.tiles_n * p.nb[1] * p.nb[2] * p.nb[3];
+      p.skip_b0_scale = 1;
+    }
     const int grid = 2 * (int)std::min<long long>(tiles / 2, g_num_sms / 2);
     switch (bn) {
       case 256: return launch_ring<256, 3, 2, true>(tm_lam, tm2_whi, tm2_wlo, p, grid, st);
