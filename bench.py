@@ -429,6 +429,7 @@ def main():
         search(*inputs[s])
     barrier()
     dev_ms, calls, launches, passes, pass_ms, exact_probes, exact_ms = 0.0, [], 0, 0, [], 0, 0.0
+    rollbacks = 0
     h2d = d2h = 0
     # fg_maxeps runs the eps = 0 probes up front on a narrow workspace (one pass for B <= 256
     # sentences) when words*embed > 128 and the pass is not column-sharded: its eps/slot staging
@@ -446,6 +447,7 @@ def main():
             pass_ms.append(st["pass_ms"])
             exact_probes += st["exact_probes"]
             exact_ms += st["exact_ms"]
+            rollbacks += st["spec_rollbacks"]
             calls.extend(r["calls"].tolist())
             # every step copies its batch's inputs in (x f64, positions i32) and the results out
             # (eps f64, calls / predicted / status i32), plus per pass the eps/slot staging and
@@ -488,6 +490,10 @@ def main():
         "passes_per_sentence": statistics.mean(calls),
         "exact_probes_per_sentence": exact_probes / (B * args.steps),
         "exact_ms_share": exact_ms / dev_ms if dev_ms else 0.0,
+        "speculation": {"rollbacks_per_step": rollbacks / args.steps, "batched_passes_per_step": passes / args.steps,
+                        "_note": "sentences bisect on with a guessed verdict while their ambiguous probe is "
+                                 "re-decided; a wrong guess rolls the sentence back (include/faith_gpu.h "
+                                 "fg_model_set_speculation)"},
         "ambiguity_band": {"lo": st["band_lo"], "hi": st["band_hi"], "calibration_samples": st["band_samples"],
                            "unit": "fraction of the two logits bounds' widths"},
         "e2e": {"value": e2e, "unit": "sentences/s", "h2d_bytes_per_step": h2d // args.steps,

@@ -233,6 +233,20 @@ fg_status fg_bound_pass_exact(fg_model* model, const double* x, const int* posit
 #define FG_DEFAULT_KAPPA 6e-6
 fg_status fg_model_set_exact_resolve(fg_model* model, double kappa);
 
+/* What fg_maxeps does with a sentence while its ambiguous probe is re-decided (asynchronously,
+ * on side streams).  PREDICTED (default): the sentence keeps its slot and bisects on with the
+ * verdict its f32 margins predict after correcting them by the model's mean measured error;
+ * when the exact verdict differs, the sentence is rolled back to that probe and advanced with
+ * the exact verdict, and re-decisions started on the abandoned path are dropped.  VERIFIED /
+ * FAILED: always guess that verdict (tests of the roll-back path).  OFF: the sentence leaves its
+ * slot until the exact verdict is in.  Every mode returns the same eps / calls: only verdicts
+ * confirmed by the exact pass stay on a sentence's bisection path. */
+#define FG_SPECULATE_OFF 0
+#define FG_SPECULATE_PREDICTED 1
+#define FG_SPECULATE_VERIFIED 2
+#define FG_SPECULATE_FAILED 3
+fg_status fg_model_set_speculation(fg_model* model, int mode);
+
 /* certify(sentence, p, eps) -- cmd_verify (cli.cpp:64-133) for S sentences:
  * predicted = argmax(forward); verified = check_robust(concretize(pass), predicted, margin).
  * bounded[s] = 0 when the pass raised a domain error (cli.cpp:92-94). */
@@ -338,6 +352,8 @@ typedef struct {
   double exact_ms;       /* time spent in those exact passes (included in device_ms) */
   double band_lo, band_hi; /* the model's ambiguity band after the call (units of W) */
   int band_samples;      /* re-decided probes it was calibrated on so far */
+  int spec_rollbacks;    /* fg_maxeps: speculative bisection steps whose guessed verdict the
+                            exact re-decision overturned (the sentence was rolled back) */
 } fg_run_stats;
 fg_status fg_last_run_stats(const fg_model* model, fg_run_stats* out);
 

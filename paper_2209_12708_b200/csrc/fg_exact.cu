@@ -64,6 +64,10 @@ __global__ void __launch_bounds__(kXThreads) x_affine_lam_tiled_kernel(
     const double* __restrict__ xlw, const double* __restrict__ xuw, const double* __restrict__ w,
     double* __restrict__ ylw, double* __restrict__ yuw, long long rows, int c, int o, int d) {
   __shared__ double su[kIC][kXThreads], sl[kIC][kXThreads], sw[kIC][JT];
+  // per staged input row: bit t = (w_t > 0), bit 8 + t = (w_t < 0), so the inner loop branches on
+  // integer bits instead of two f64 compares per weight on the FP64 pipe (NaN / ±0: neither bit)
+  __shared__ uint32_t sgn[kIC];
+  static_assert(JT <= 8, "sign mask holds 8 weights per row");
   const int kb = (d + kXThreads - 1) / kXThreads;
   const int jtiles = o / JT;
   const long long blk = blockIdx.x;
@@ -94,17 +98,29 @@ __global__ void __launch_bounds__(kXThreads) x_affine_lam_tiled_kernel(
       sw[ii][t] = ii < ni ? w[(long long)(i0 + ii) * o + j0 + t] : 0.0;
     }
     __syncthreads();
+    if (threadIdx.x < kIC) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int t = 0; t < JT; ++t) {
+        const double v = sw[threadIdx.x][t];
+        m |= (v > 0.0 ? 1u : 0u) << t;
+        m |= (v < 0.0 ? 1u : 0u) << (8 + t);
+      }
+      sgn[threadIdx.x] = m;
+    }
+    __syncthreads();
     for (int ii = 0; ii < ni; ++ii) {
       const double xu = su[ii][threadIdx.x], xl = sl[ii][threadIdx.x];
+      const uint32_t m = sgn[ii];
       double wv[JT];
 #pragma unroll
       for (int t = 0; t < JT; ++t) wv[t] = sw[ii][t];
 #pragma unroll
       for (int t = 0; t < JT; ++t) {
-        if (wv[t] > 0.0) {  // wp = w, wn = 0
+        if ((m >> t) & 1u) {  // w > 0: wp = w, wn = 0
           yu[t] += wv[t] * xu;
           yl[t] += wv[t] * xl;
-        } else if (wv[t] < 0.0) {  // wp = 0, wn = w
+        } else if ((m >> (8 + t)) & 1u) {  // w < 0: wp = 0, wn = w
           un[t] += wv[t] * xl;
           ln[t] += wv[t] * xu;
         }

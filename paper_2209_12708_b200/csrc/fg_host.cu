@@ -749,6 +749,7 @@ struct fg_model {
   double band_lo = -FG_DEFAULT_KAPPA, band_hi = FG_DEFAULT_KAPPA / 8;
   double err_min = 0.0, err_max = 0.0;
   int err_samples = 0;
+  int speculate = FG_SPECULATE_PREDICTED;  // fg_maxeps while a re-decision runs (fg_model_set_speculation)
   int exact_probes = 0;   // per call: probes re-decided by the exact pass, and their time
   double exact_ms = 0.0;
   // asynchronous re-decisions (fg_maxeps): a low-priority side stream and reusable jobs
@@ -1458,6 +1459,19 @@ int closest_class(const double* lo, const double* hi, int C, int t, double margi
   return jb;
 }
 
+// The exact verdict an ambiguous probe most likely gets (fg_maxeps speculates on it): every
+// f32 margin corrected by the model's mean measured error (m_f32 - m_exact) / W, or before any
+// calibration sample by -1e-6 (the fused pass's margins run below the exact ones).
+int guess_verdict(const fg_model* m, const double* lo, const double* hi, int C, int t) {
+  const double mid = m->err_samples ? 0.5 * (m->err_min + m->err_max) : -1e-6;
+  for (int j = 0; j < C; ++j) {
+    if (j == t) continue;
+    const double w = (hi[t] - lo[t]) + (hi[j] - lo[j]);
+    if (!(lo[t] - hi[j] - mid * w > 0.0)) return 0;
+  }
+  return 1;
+}
+
 bool ambiguous_verdict(const fg_model* m, const double* lo, const double* hi, int C, int t, double margin) {
   if (!(m->kappa > 0.0)) return false;
   for (int j = 0; j < C; ++j) {
@@ -1955,13 +1969,28 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
     return FG_OK;
   };
   // A probe after ε = 0 (P_MAX / P_BISECT) whose f32 verdict is ambiguous is re-decided
-  // asynchronously (start_exact_job): the sentence leaves its slot until the exact verdict is in,
-  // then resumes from `ready` ahead of new sentences.  Column-sharded models decide synchronously
-  // (every rank must run the same sentences in the same slots).
+  // asynchronously (start_exact_job) while its sentence keeps its slot and bisects on
+  // speculatively with the verdict the f32 margin predicts (guess_verdict).  When the exact
+  // verdict lands it either confirms the guess, or the sentence rolls back to its state at that
+  // probe, is advanced with the exact verdict -- the reference's bisection step -- and every
+  // re-decision started on the abandoned path is cancelled (per-sentence sequence numbers).
+  // The call returns only when every re-decision has landed, so each verdict on the final path
+  // is the exact one.  Column-sharded models decide synchronously (every rank must run the same
+  // sentences in the same slots).
   const bool async_exact = !m->shard.active();
-  std::vector<fgh::ExactJob*> pending;
-  std::vector<int> ready;  // resumed sentences, FIFO
+  struct Pend {
+    fgh::ExactJob* job;
+    int s;
+    Sent snap;  // the sentence before this probe's (guessed) bisection step
+    int guess, seq;
+    bool cancelled;
+  };
+  std::vector<Pend> pending;
+  std::vector<int> next_seq(S, 0);
+  std::vector<char> queued(S, 0);
+  std::vector<int> ready;  // rolled-back sentences waiting for a slot, FIFO
   size_t ready_head = 0;
+  int rollbacks = 0;
   // one bisection step of sentence s with verdict ok (cli.cpp:163-177); true when finished
   auto advance = [&](int s, int ok) -> bool {
     Sent& t = sent[s];
@@ -1995,8 +2024,8 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
   // applies finished jobs (block: wait for the oldest one)
   auto poll = [&](bool block) {
     for (size_t k = 0; k < pending.size();) {
-      fgh::ExactJob* job = pending[k];
-      cudaError_t q = block && k == 0 ? cudaEventSynchronize(job->done) : cudaEventQuery(job->done);
+      Pend& pj = pending[k];
+      cudaError_t q = block && k == 0 ? cudaEventSynchronize(pj.job->done) : cudaEventQuery(pj.job->done);
       if (q == cudaErrorNotReady) {
         ++k;
         continue;
@@ -2005,10 +2034,31 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
         st = fail(ctx, FG_ECUDA, std::string("exact re-decision: ") + cudaGetErrorString(q));
         return;
       }
-      const int s = job->sentence;
+      const int s = pj.s;
       fg_status ps = FG_OK;
-      const int ok = finish_exact_job(m, job, pred[s], ps);
-      if (!advance(s, ps == FG_OK && ok)) ready.push_back(s);
+      const int verdict = finish_exact_job(m, pj.job, pred[s], ps) && ps == FG_OK;
+      if (pj.cancelled) {
+      } else if (pj.guess < 0) {  // no speculation: the sentence waited out of its slot
+        if (!advance(s, verdict)) {
+          queued[s] = 1;
+          ready.push_back(s);
+        }
+      } else if (verdict != pj.guess) {  // wrong guess: back to the probe
+        ++rollbacks;
+        for (Pend& o : pending)
+          if (o.s == s && o.seq > pj.seq) o.cancelled = true;
+        if (sent[s].phase == P_DONE) --done;
+        sent[s] = pj.snap;
+        int in_slot = -1;
+        for (int i = 0; i < slots; ++i)
+          if (slot[i] == s) in_slot = i;
+        if (advance(s, verdict)) {
+          if (in_slot >= 0) slot[in_slot] = -1;
+        } else if (in_slot < 0 && !queued[s]) {
+          queued[s] = 1;
+          ready.push_back(s);
+        }
+      }
       pending.erase(pending.begin() + (long)k);
       block = false;
     }
@@ -2017,11 +2067,15 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
   // failed (domain / validation errors): deep random-init models (c4, c5) fail almost every probe
   // above eps ~ 1e-7 part-way through the pass, c1-c3 almost none
   bool early_exit = false;
-  while (done < S && !st) {
+  while ((done < S || !pending.empty()) && !st) {
     bool any = false;
     int idle = 0;
     for (int i = 0; i < slots; ++i) {
-      if (slot[i] < 0 && ready_head < ready.size()) slot[i] = ready[ready_head++];
+      while (slot[i] < 0 && ready_head < ready.size()) {
+        const int r = ready[ready_head++];
+        queued[r] = 0;
+        if (sent[r].phase != P_DONE) slot[i] = r;
+      }
       while (slot[i] < 0 && next < S && sent[next].phase == P_DONE) ++next;
       if (slot[i] < 0 && next < S) slot[i] = next++;
       int s = slot[i];
@@ -2031,7 +2085,7 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
       w.h_eps[i] = s >= 0 ? sent[s].eps : 0.0;
       w.h_active[i] = s >= 0;
     }
-    if (!any) {  // every remaining sentence waits for its exact verdict
+    if (!any) {  // every sentence is done, some speculatively: wait for their exact verdicts
       poll(true);
       continue;
     }
@@ -2073,8 +2127,12 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
         if (st) break;
         std::copy(plo, plo + C, job->lo32.begin());
         std::copy(phi, phi + C, job->hi32.begin());
-        pending.push_back(job);
-        slot[i] = -1;  // waits out of its slot
+        const int guess = m->speculate == FG_SPECULATE_OFF       ? -1
+                          : m->speculate == FG_SPECULATE_VERIFIED  ? 1
+                          : m->speculate == FG_SPECULATE_FAILED    ? 0
+                                                                   : guess_verdict(m, plo, phi, C, pred[s]);
+        pending.push_back(Pend{job, s, t, guess, next_seq[s]++, false});
+        if (guess < 0 || advance(s, guess)) slot[i] = -1;
         continue;
       }
       if ((st = decide_probe(m, x + s * LE, positions + (size_t)s * words, words, norm, t.eps, plo, phi, pred[s],
@@ -2103,7 +2161,7 @@ fg_status fg_maxeps(fg_model* m, int S, const double* x, const int* positions, i
   cudaEventDestroy(c0); cudaEventDestroy(c1); cudaEventDestroy(e0); cudaEventDestroy(e1);
   m->stats = fg_run_stats{(double)total, passes ? pass_ms_sum / passes : 0.0, passes, slots,
                           ctx->launches - launches0, sentence_passes, m->exact_probes, m->exact_ms,
-                          m->band_lo, m->band_hi, m->err_samples};
+                          m->band_lo, m->band_hi, m->err_samples, rollbacks};
   return st;
 }
 
@@ -2576,6 +2634,14 @@ fg_status fg_bound_pass_exact(fg_model* m, const double* x, const int* positions
   if (fg_status st = upload_params64(m)) return st;
   return fgh::exact_pass(ctx, m->cfg, m->params64.as<double>(), x, positions, words, norm, eps, logits_lo,
                          logits_hi, node_lo, node_hi, status);
+}
+
+fg_status fg_model_set_speculation(fg_model* m, int mode) {
+  if (!m) return FG_EINVAL;
+  if (mode < FG_SPECULATE_OFF || mode > FG_SPECULATE_FAILED)
+    return fail(m->ctx, FG_EINVAL, "fg_model_set_speculation: unknown mode");
+  m->speculate = mode;
+  return FG_OK;
 }
 
 fg_status fg_model_set_exact_resolve(fg_model* m, double kappa) {

@@ -28,6 +28,7 @@ RELAX = {"relu": 0, "tanh": 1, "silu": 2, "exp": 3, "recip": 4,
          "sqrt": 5, "square": 6}  # extension: LayerNorm bound chain (no reference counterpart)
 DOT = {"similarity": 0, "weighted_values": 1}
 # ambiguity band of the decision-exact verdicts (FG_DEFAULT_KAPPA, include/faith_gpu.h)
+SPECULATE = {"off": 0, "predicted": 1, "verified": 2, "failed": 3}  # FG_SPECULATE_*
 DEFAULT_KAPPA = 6e-6
 STATUS_NAME = {0: "ok", 1: "invalid_argument", 2: "domain_error", 3: "out_of_range", 4: "runtime_error",
                5: "cuda_error", 6: "out_of_memory"}
@@ -76,7 +77,7 @@ class RunStats(C.Structure):
     _fields_ = [("device_ms", C.c_double), ("pass_ms", C.c_double), ("passes", C.c_int), ("slots", C.c_int),
                 ("launches", C.c_uint64), ("sentence_passes", C.c_double), ("exact_probes", C.c_int),
                 ("exact_ms", C.c_double), ("band_lo", C.c_double), ("band_hi", C.c_double),
-                ("band_samples", C.c_int)]
+                ("band_samples", C.c_int), ("spec_rollbacks", C.c_int)]
 
 
 class FgConfig(C.Structure):
@@ -133,6 +134,7 @@ def load_library():
     L.fg_bound_pass_dump.argtypes = [vp, _dp, _ip, C.c_int, C.c_int, C.c_double, _dp, _dp, _dp, _dp, _ip]
     L.fg_bound_pass_exact.argtypes = [vp, _dp, _ip, C.c_int, C.c_int, C.c_double, _dp, _dp, _dp, _dp, _ip]
     L.fg_model_set_exact_resolve.argtypes = [vp, C.c_double]
+    L.fg_model_set_speculation.argtypes = [vp, C.c_int]
     L.fg_certify.argtypes = [vp, C.c_int, _dp, _ip, C.c_int, C.c_int, _dp, C.c_double, _ip, _ip, _ip, _dp, _dp, _ip]
     L.fg_maxeps.argtypes = [vp, C.c_int, _dp, _ip, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, _dp, _ip,
                             _ip, _ip]
@@ -652,6 +654,12 @@ class Model:
     def set_exact_resolve(self, kappa: float):
         """Ambiguity band of the decision-exact verdicts (include/faith_gpu.h); 0 = raw f32 verdicts."""
         self.ctx._check(self.lib.fg_model_set_exact_resolve(self.handle, float(kappa)), "fg_model_set_exact_resolve")
+
+    def set_speculation(self, mode: str):
+        """fg_maxeps while a re-decision runs: "predicted" (default), "verified", "failed", "off"
+        (include/faith_gpu.h fg_model_set_speculation)."""
+        code = SPECULATE[mode]
+        self.ctx._check(self.lib.fg_model_set_speculation(self.handle, code), "fg_model_set_speculation")
 
     def certify(self, x, positions, norm: str, eps, margin: float = 0.0):
         """cmd_verify semantics per sentence -> dict of arrays."""

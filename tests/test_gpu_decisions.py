@@ -160,3 +160,40 @@ def test_maxeps_exact_probe_accounting(models, port):
         m.set_exact_resolve(F.DEFAULT_KAPPA)
     with pytest.raises(F.InvalidArgument):
         m.set_exact_resolve(-1.0)
+
+
+@pytest.mark.parametrize("mode", ["off", "predicted", "verified", "failed"])
+def test_maxeps_speculation_modes_match_golden(models, port, mode):
+    """While a re-decision runs, fg_maxeps bisects on with a guessed verdict and rolls the
+    sentence back when the exact verdict differs.  Whatever the guesses -- predicted, always
+    verified, always failed (forcing roll-backs), or no speculation -- the ε and calls are the
+    reference's.  A wide band (kappa 1e-4 until 16 calibration samples) sends many probes to the
+    exact pass, so the roll-back path runs."""
+    recs = [json.load(open(p)) for p in sorted(glob.glob(os.path.join(GOLDEN, "c3_maxeps_s*.json")))]
+    w, cfg, params, m = models("c3")
+    xs, ps = zip(*[sentence(port, w, cfg, rec["sentence"]) for rec in recs])
+    try:
+        m.set_exact_resolve(1e-4)
+        m.set_speculation(mode)
+        r = m.maxeps(np.stack(xs), np.stack(ps), recs[0]["norm"], recs[0]["eps_max"], recs[0]["tol"])
+        st = m.last_stats()
+    finally:
+        m.set_speculation("predicted")
+        m.set_exact_resolve(F.DEFAULT_KAPPA)
+    for k, rec in enumerate(recs):
+        assert (int(r["status"][k]), int(r["calls"][k])) == (rec["status"], rec["calls"]), rec["sentence"]
+        assert r["eps"][k] == rec["max_epsilon"], rec["sentence"]
+    print(f"{mode}: {st['exact_probes']} exact probes, {st['spec_rollbacks']} roll-backs")
+    assert st["exact_probes"] >= 8
+    if mode == "off":
+        assert st["spec_rollbacks"] == 0
+    if mode in ("verified", "failed"):
+        assert st["spec_rollbacks"] >= 1
+
+
+def test_speculation_mode_validation(models):
+    w, cfg, params, m = models("c1")
+    with pytest.raises(F.InvalidArgument):
+        m.ctx._check(m.lib.fg_model_set_speculation(m.handle, 7), "fg_model_set_speculation")
+    with pytest.raises(KeyError):
+        m.set_speculation("sometimes")
