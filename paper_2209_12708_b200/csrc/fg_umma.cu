@@ -94,6 +94,41 @@ __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint6
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// One K chunk (32 deep = 4 K-steps of 8) of the 3xTF32 product, issued by one elected lane of a
+// converged warp: D (+)= A_hi B_hi + A_lo B_hi + A_hi B_lo per K-step.  The descriptors of the
+// four operand tiles are passed once; the K-step advances by +32 B (+2 in the descriptor's
+// address field).  A single asm block keeps the twelve tcgen05.mma on uniform operands
+// (no per-instruction elect / R2UR sequences around each MMA).
+template <bool PAIR>
+__device__ __forceinline__ void umma3_kchunk(uint32_t d_tmem, uint64_t ahi, uint64_t alo, uint64_t bhi, uint64_t blo,
+                                             uint32_t idesc, uint32_t acc_first) {
+#define FG_MMA(CG)                                                                          \
+  asm volatile(                                                                             \
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a0, a1, b0, b1;\n\t"                           \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                     \
+      "setp.ne.b32 p, %5, 0;\n\t"                                                           \
+      "setp.eq.b32 t, 0, 0;\n\t"                                                            \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], %1, %3, %6, p;\n\t"               \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], %2, %3, %6, t;\n\t"               \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], %1, %4, %6, t;\n\t"               \
+      "add.s64 a0, %1, 2;\n\tadd.s64 a1, %2, 2;\n\tadd.s64 b0, %3, 2;\n\tadd.s64 b1, %4, 2;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], a0, b0, %6, t;\n\t"               \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], a1, b0, %6, t;\n\t"               \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], a0, b1, %6, t;\n\t"               \
+      "add.s64 a0, %1, 4;\n\tadd.s64 a1, %2, 4;\n\tadd.s64 b0, %3, 4;\n\tadd.s64 b1, %4, 4;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], a0, b0, %6, t;\n\t"               \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], a1, b0, %6, t;\n\t"               \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], a0, b1, %6, t;\n\t"               \
+      "add.s64 a0, %1, 6;\n\tadd.s64 a1, %2, 6;\n\tadd.s64 b0, %3, 6;\n\tadd.s64 b1, %4, 6;\n\t" \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], a0, b0, %6, t;\n\t"               \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], a1, b0, %6, t;\n\t"               \
+      "@e tcgen05.mma.cta_group::" CG ".kind::tf32 [%0], a0, b1, %6, t;\n}"                 \
+      ::"r"(d_tmem), "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(acc_first), "r"(idesc))
+  if (PAIR) FG_MMA("2");
+  else FG_MMA("1");
+#undef FG_MMA
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -343,24 +378,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = g % S;
           mbar_wait(&split[s], (g / S) & 1);
           tc_fence_after();
+          {
+            // +32 B per 8 tf32 of K inside the 128 B rows (umma3_kchunk)
+            const uint32_t st = smem_u32(smem) + s * RL::kOp;
+            umma3_kchunk<PAIR>(d_tmem, kmajor_sw128_desc(st + RL::kLhi), kmajor_sw128_desc(st + RL::kLlo),
+                               kmajor_sw128_desc(st), kmajor_sw128_desc(st + RL::kWlo), idesc, kb != 0);
+          }
           if (lane == 0) {
-            uint8_t* st = smem + s * RL::kOp;
-            const uint32_t w_hi = smem_u32(st), w_lo = smem_u32(st + RL::kWlo);
-            const uint32_t l_hi = smem_u32(st + RL::kLhi), l_lo = smem_u32(st + RL::kLlo);
-#pragma unroll
-            for (int ks = 0; ks < kBK / 8; ++ks) {  // +32 B per 8 tf32 of K inside the 128 B rows
-              const uint64_t ahi = kmajor_sw128_desc(l_hi + ks * 32), alo = kmajor_sw128_desc(l_lo + ks * 32);
-              const uint64_t bhi = kmajor_sw128_desc(w_hi + ks * 32), blo = kmajor_sw128_desc(w_lo + ks * 32);
-              if (PAIR) {
-                umma2_tf32(d_tmem, ahi, bhi, idesc, (kb | ks) != 0);
-                umma2_tf32(d_tmem, alo, bhi, idesc, 1);
-                umma2_tf32(d_tmem, ahi, blo, idesc, 1);
-              } else {
-                umma_tf32(d_tmem, ahi, bhi, idesc, (kb | ks) != 0);
-                umma_tf32(d_tmem, alo, bhi, idesc, 1);
-                umma_tf32(d_tmem, ahi, blo, idesc, 1);
-              }
-            }
             if (PAIR) {
               umma2_commit_both(&opempty[s]);
               if (kb == nkb - 1) umma2_commit_both(&tfull[acc]);
