@@ -311,12 +311,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- W producer ----------------
     if (lane == 0) {
       int g = 0;
-      for (int t = unit; t < num_tiles; t += nunits) {
+#pragma unroll 1
+    for (int t = unit; t < num_tiles; t += nunits) {
         if (skipped(t)) continue;
         int b[4], m0, n0;
         decode(t, b, m0, n0);
         const int wc2 = lin5(p.w_c[0], b), wc3 = lin5(p.w_c[1], b);
         const int nw0 = n0 + (PAIR ? (int)rank * (BN / 2) : 0);
+#pragma unroll 1
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = g % S;
           mbar_wait(&opempty[s], ((g / S) & 1) ^ 1);
@@ -331,11 +333,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- Λ producer (raw ring) ----------------
     if (lane == 0) {
       int g = 0;
-      for (int t = unit; t < num_tiles; t += nunits) {
+#pragma unroll 1
+    for (int t = unit; t < num_tiles; t += nunits) {
         if (skipped(t)) continue;
         int b[4], m0, n0;
         decode(t, b, m0, n0);
         const int lc1 = lin5(p.lam_c[0], b), lc2 = lin5(p.lam_c[1], b), lc3 = lin5(p.lam_c[2], b);
+#pragma unroll 1
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int r = g % R;
           mbar_wait(&rawfree[r], ((g / R) & 1) ^ 1);
@@ -367,13 +371,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)((PAIR ? 2 : 1) * kBM >> 4) << 24);
       int g = 0, it = -1;
-      for (int t = unit; t < num_tiles; t += nunits) {
+#pragma unroll 1
+    for (int t = unit; t < num_tiles; t += nunits) {
         if (skipped(t)) continue;
         ++it;
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+#pragma unroll 1
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = g % S;
           mbar_wait(&split[s], (g / S) & 1);
@@ -403,8 +409,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // (the 128 B swizzle spreads a warp's rows over all banks).
     const int d = threadIdx.x - 128;
     int g = 0;
+#pragma unroll 1
     for (int t = unit; t < num_tiles; t += nunits) {
       if (skipped(t)) continue;
+#pragma unroll 1
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % S, r = g % R;
         mbar_wait(&rawfull[r], (g / R) & 1);
@@ -463,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool has_x = p.accumulate || p.res;
     const long long xld = p.accumulate ? p.ldn_out : p.ldn_res;
     int it = -1;
+#pragma unroll 1
     for (int t = unit; t < num_tiles; t += nunits) {
       if (skipped(t)) continue;
       ++it;
@@ -491,13 +500,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       // rolling refill two chunks ahead (register double buffer pa / pb)
       constexpr int NCH = BN / 32;
       float pa[32], pb[32];
-      auto load_x = [&](int c, float (&dst)[32]) {
-        if (p.accumulate && (p.n_split & 31)) {  // plane boundary inside the chunk (see finish)
+      // a plane boundary inside a 32-column chunk (n_split < 32, e.g. hd = 16): per-element
+      // addresses, stepped incrementally (two divisions per chunk)
+      auto split_off = [&](int c, int j, int& pl, int& nn) -> long long {
+        if (j == 0) {
           const int nb0 = n0 + c * 32;
+          pl = nb0 / p.n_split;
+          nn = nb0 - pl * p.n_split;
+        } else if (++nn == p.n_split) {
+          nn = 0;
+          ++pl;
+        }
+        return (long long)pl * p.split_stride + (long long)nn * p.ldn_out;
+      };
+      auto load_x = [&](int c, float (&dst)[32]) {
+        if (p.accumulate && (p.n_split & 31)) {
+          int pl = 0, nn = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            dst[j] = out_b[(long long)((nb0 + j) / p.n_split) * p.split_stride +
-                           (long long)((nb0 + j) % p.n_split) * p.ldn_out];
+          for (int j = 0; j < 32; ++j) dst[j] = out_b[split_off(c, j, pl, nn)];
           return;
         }
         const float* xs = chunk_x(c);
@@ -521,13 +541,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) o[j] += rc[j * p.ldn_res];
         }
-        if (p.n_split & 31) {  // a plane boundary inside the chunk (n_split < 32, e.g. hd = 16)
-          const int nb0 = n0 + c * 32;
+        if (p.n_split & 31) {  // a plane boundary inside the chunk (split_off)
+          int pl = 0, nn = 0;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            __stcs(out_b + (long long)((nb0 + j) / p.n_split) * p.split_stride +
-                       (long long)((nb0 + j) % p.n_split) * p.ldn_out,
-                   o[j]);
+          for (int j = 0; j < 32; ++j) __stcs(out_b + split_off(c, j, pl, nn), o[j]);
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) __stcs(oc + j * p.ldn_out, o[j]);
