@@ -164,6 +164,21 @@ int launch_init_status(int* status, const int* active, int n, cudaStream_t st);
 //   Batch b = ((b0*nb1 + b1)*nb2 + b2)*nb3 + b3; every coordinate / offset is
 //   co[0]*b0 + co[1]*b1 + co[2]*b2 + co[3]*b3 + co[4].
 // Tensor maps are opaque 128-byte CUtensorMap objects (64-byte aligned storage).
+// Division by a runtime divisor d >= 1 as a multiply-high (x < 2^31): q = (umulhi(x, m) + x) >> s
+// with s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1 (set on the host by make_fastdiv).
+struct FastDiv {
+  uint32_t m = 0, s = 0;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  while ((1ull << f.s) < d) ++f.s;
+  f.m = (uint32_t)((((1ull << 32) * ((1ull << f.s) - d)) / d) + 1);
+  return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, FastDiv f) { return (__umulhi(x, f.m) + x) >> f.s; }
+#endif
+
 struct LamGemm {
   int M, N, K, K0;
   int nb[4];
@@ -201,6 +216,8 @@ struct LamGemm {
   const int* skip_status;
   int skip_div, skip_slots;
   int skip_tiles_per_b0, skip_b0_scale;  // set by launch_lam_gemm
+  // divisors of the tile decode, set by launch_lam_gemm
+  FastDiv f_tn, f_tm, f_nb1, f_nb2, f_nb3, f_skip_t, f_skip_div, f_nsplit;
 };
 bool umma_available();
 int umma_pick_bn(int N);  // 256 / 128 / 64, or 0 when N is not a multiple of 64

@@ -166,6 +166,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// b[i] of a 4-entry batch coordinate held in registers (runtime i without a local-memory array)
+__device__ __forceinline__ int get_at(const int (&b)[4], int i) {
+  return i == 0 ? b[0] : (i == 1 ? b[1] : (i == 2 ? b[2] : b[3]));
+}
+__device__ __forceinline__ void add_at(int (&b)[4], int i, int v) {
+  b[0] += i == 0 ? v : 0;
+  b[1] += i == 1 ? v : 0;
+  b[2] += i == 2 ? v : 0;
+  b[3] += i == 3 ? v : 0;
+}
+
 __device__ __forceinline__ int lin5(const int* co, const int* b) {
   return co[0] * b[0] + co[1] * b[1] + co[2] * b[2] + co[3] * b[3] + co[4];
 }
@@ -282,19 +293,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // tile t -> (batch b0..b3, m-tile over d, n-tile over output neurons); n fastest so that
   // units running concurrently share the (HBM-resident) Λ tiles through L2.
-  auto decode = [&](int t, int* b, int& m0, int& n0) {
-    int nt = t % p.tiles_n;
-    int rest = t / p.tiles_n;
-    int mt = rest % tiles_m;
-    int batch = rest / tiles_m;
-    b[3] = batch % p.nb[3];
-    batch /= p.nb[3];
-    b[2] = batch % p.nb[2];
-    batch /= p.nb[2];
-    b[1] = batch % p.nb[1];
-    b[0] = batch / p.nb[1];
+  auto decode = [&](int t, int (&b)[4], int& m0, int& n0) {
+    const int rest = (int)fdiv((uint32_t)t, p.f_tn);
+    const int nt = t - rest * p.tiles_n;
+    int batch = (int)fdiv((uint32_t)rest, p.f_tm);
+    const int mt = rest - batch * tiles_m;
+    int q = (int)fdiv((uint32_t)batch, p.f_nb3);
+    b[3] = batch - q * p.nb[3];
+    batch = q;
+    q = (int)fdiv((uint32_t)batch, p.f_nb2);
+    b[2] = batch - q * p.nb[2];
+    batch = q;
+    q = (int)fdiv((uint32_t)batch, p.f_nb1);
+    b[1] = batch - q * p.nb[1];
+    b[0] = q;
     if (p.gather) b[2] = p.gather[p.gather_slot[b[0]] * p.gather_ld + b[2]];
-    if (p.fold1) b[p.fold1 - 1] *= 2;  // the pair (b, b + 1) of the folded coordinate
+    if (p.fold1) add_at(b, p.fold1 - 1, get_at(b, p.fold1 - 1));  // the pair (2b, 2b + 1) of the folded coordinate
     m0 = mt * (PAIR ? 2 : 1) * kBM + (int)rank * kBM;  // this CTA's first d-row
     n0 = nt * BN;
   };
@@ -303,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // b[0] is the slowest tile coordinate: one division per tile, no full decode
   auto skipped = [&](int t) -> bool {
     if (!p.skip_tiles_per_b0) return false;
-    const int slot = (t / p.skip_tiles_per_b0) * p.skip_b0_scale / p.skip_div;
+    const int slot = (int)fdiv(fdiv((uint32_t)t, p.f_skip_t) * p.skip_b0_scale, p.f_skip_div);
     return (reinterpret_cast<const uint32_t*>(smem + RL::kMaskOff)[slot >> 5] >> (slot & 31)) & 1u;
   };
 
@@ -481,15 +495,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = it & 1;
       int dd = m0 + q * 32 + lane;
       if (p.fold1) {  // lanes 64..127 hold the second of the folded pair (warp-uniform: q >> 1)
-        b[p.fold1 - 1] += q >> 1;
+        add_at(b, p.fold1 - 1, q >> 1);
         dd &= 63;
       }
       float* out_b = p.out + lin5l(p.out_c, b) + dd;
       const float* res = p.res ? p.res + lin5l(p.res_c, b) + (long long)n0 * p.ldn_res + dd : nullptr;
       auto chunk_out = [&](int c) -> float* {
         const int n = n0 + c * 32;
-        float* out = p.n_split ? out_b + (long long)(n / p.n_split) * p.split_stride +
-                                     (long long)(n % p.n_split) * p.ldn_out - (long long)c * 32 * p.ldn_out
+        const int pl = p.n_split ? (int)fdiv((uint32_t)n, p.f_nsplit) : 0;
+        float* out = p.n_split ? out_b + (long long)pl * p.split_stride +
+                                     (long long)(n - pl * p.n_split) * p.ldn_out - (long long)c * 32 * p.ldn_out
                                : out_b + (long long)n0 * p.ldn_out;
         return out + (long long)c * 32 * p.ldn_out;
       };
@@ -505,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto split_off = [&](int c, int j, int& pl, int& nn) -> long long {
         if (j == 0) {
           const int nb0 = n0 + c * 32;
-          pl = nb0 / p.n_split;
+          pl = (int)fdiv((uint32_t)nb0, p.f_nsplit);
           nn = nb0 - pl * p.n_split;
         } else if (++nn == p.n_split) {
           nn = 0;
@@ -529,17 +544,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
         float* oc = chunk_out(c);
         float o[32];
-        const float al = (p.alpha_r_dim1 > 0 && b[p.alpha_r_dim1 - 1] == 1) ? p.alpha_r : p.alpha;
+        const float al = (p.alpha_r_dim1 > 0 && get_at(b, p.alpha_r_dim1 - 1) == 1) ? p.alpha_r : p.alpha;
 #pragma unroll
         for (int j = 0; j < 32; ++j) o[j] = al * __uint_as_float(v[j]);
         if (has_x) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) o[j] += xv[j];
-        }
-        if (p.accumulate && res) {  // both (unused by the pass): residual loaded directly
-          const float* rc = res + (long long)c * 32 * p.ldn_res;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] += rc[j * p.ldn_res];
         }
         if (p.n_split & 31) {  // a plane boundary inside the chunk (split_off)
           int pl = 0, nn = 0;
@@ -699,6 +709,17 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
     tm2_whi = tm2_wlo = nullptr;
   }
   if (p.M % kBM || p.K % kBK || p.K0 % kBK || bn <= 0 || p.N % bn) return -1;
+  if (p.accumulate && p.res) return -1;  // one added operand: the previous output or a residual
+  auto set_divisors = [&](int tiles_m_walk) {
+    p.f_tn = make_fastdiv((uint32_t)p.tiles_n);
+    p.f_tm = make_fastdiv((uint32_t)tiles_m_walk);
+    p.f_nb1 = make_fastdiv((uint32_t)p.nb[1]);
+    p.f_nb2 = make_fastdiv((uint32_t)p.nb[2]);
+    p.f_nb3 = make_fastdiv((uint32_t)p.nb[3]);
+    p.f_skip_t = make_fastdiv((uint32_t)std::max(p.skip_tiles_per_b0, 1));
+    p.f_skip_div = make_fastdiv((uint32_t)std::max(p.skip_div, 1));
+    p.f_nsplit = make_fastdiv((uint32_t)std::max(p.n_split, 1));
+  };
   if (tm2_whi && tm2_wlo && p.M % (2 * kBM) == 0 && bn >= 64 && umma_pair_enabled()) {
     if (!g_num_sms) {
       int dev = 0;
@@ -715,6 +736,7 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
       p.skip_tiles_per_b0 = p.tiles_m / 2 * p.tiles_n * p.nb[1] * p.nb[2] * p.nb[3];
       p.skip_b0_scale = 1;
     }
+    set_divisors(p.tiles_m / 2);
     const int grid = 2 * (int)std::min<long long>(tiles / 2, g_num_sms / 2);
     switch (bn) {
       case 256: return launch_ring<256, 3, 2, true>(tm_lam, tm2_whi, tm2_wlo, p, grid, st);
@@ -737,6 +759,7 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
     p.skip_tiles_per_b0 = p.tiles_m * p.tiles_n * p.nb[1] * p.nb[2] * p.nb[3];
     p.skip_b0_scale = p.fold1 == 1 ? 2 : 1;
   }
+  set_divisors(p.tiles_m);
   const int grid = (int)std::min<long long>(tiles, g_num_sms);
   switch (bn) {
     case 256: return launch_ring<256, 2, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
