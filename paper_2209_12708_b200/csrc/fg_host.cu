@@ -296,13 +296,22 @@ LamGemm affine_lam(const DevAffine& a, float* out, long long out_cr, const float
   return g;
 }
 
+// whether launch_affine_lambda runs this affine on the tcgen05 engine (which honours
+// LamGemm::kmask; the FP32 SIMT fallback does not)
+bool affine_on_umma(const DevAffine& a, const TensorMap* tm_in, long long rows, int D) {
+  return a.umma && tm_in && umma_affine_enabled() && (D % 128 == 0 || (D == 64 && rows % 2 == 0));
+}
+
 // `skip_status` (per sentence slot, rows_per_slot token rows each): tiles of slots whose pass has
-// already failed are skipped (early exit, LamGemm::skip_status).
+// already failed are skipped (early exit, LamGemm::skip_status).  `kmask`: zero input rows
+// (LamGemm::kmask; tcgen05 engine only, see affine_on_umma).
 int launch_affine_lambda(const DevAffine& a, const TensorMap* tm_in, const float* in, long long in_cr,
                          float* out, long long out_cr, const float* res, long long res_cr, long long rows,
-                         int D, cudaStream_t st, const int* skip_status = nullptr, int rows_per_slot = 1) {
-  if (a.umma && tm_in && umma_affine_enabled() && (D % 128 == 0 || (D == 64 && rows % 2 == 0))) {
+                         int D, cudaStream_t st, const int* skip_status = nullptr, int rows_per_slot = 1,
+                         const unsigned char* kmask = nullptr) {
+  if (affine_on_umma(a, tm_in, rows, D)) {
     LamGemm g = affine_lam(a, out, out_cr, res, res_cr, rows, D);
+    g.kmask = kmask;
     g.skip_status = skip_status;
     g.skip_div = rows_per_slot;
     g.skip_slots = (int)(rows / rows_per_slot);
@@ -684,6 +693,7 @@ struct Workspace {
   int kp = 0;            // head dimension rounded up to the GEMM engine's 32-deep K steps
   long long crX = 0, crQKV = 0, crF = 0, crSC = 0;
   DBuf X_b, R1_b, QKV_b, SC_b, CTX_b, F_b;  // f64 lb/ub(/lo/hi) blocks
+  DBuf keepF;  // per FFN row (s, t, f): 0 = Λ row zero after the activation (LamGemm::kmask of W2)
   DBuf pooled, pooled_b, coef;
   DBuf eps, status, logits, slot_map, x_all, pos_all;
   DBuf active;  // per slot: 1 = holds a probe this pass, 0 = idle (status kStatusIdle, skipped)
@@ -806,6 +816,7 @@ fg_status ensure_workspace(fg_model* m, int S, int W, int Ntot, Workspace* wsp =
   CK(w.CTX_b.alloc(sizeof(double) * 4 * nX));
   CK(w.QKV_b.alloc(sizeof(double) * 4 * nQKV));
   CK(w.F_b.alloc(sizeof(double) * 4 * nF));
+  CK(w.keepF.alloc((size_t)nF));
   CK(w.SC_b.alloc(sizeof(double) * 4 * nSC));
   CK(w.pooled.alloc(sizeof(double) * 2 * S * E * D));
   CK(w.pooled_b.alloc(sizeof(double) * 4 * S * E));
@@ -1202,10 +1213,15 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     LAUNCH(launch_affine_bias(R1_lb, R1_ub, lw.w1.w64.as<double>(), lw.w1.b64.as<double>(), nullptr,
                               nullptr, F_lb, F_ub, S, L, E, F, st, skip));
     g_tag = "act_verify";
+    // W2 on the tcgen05 engine takes the activation's zero rows as a mask, so the verify kernel
+    // leaves rows that the relaxation keeps or zeroes as they are (the dump re-reads Λ_F: no mask)
+    unsigned char* keepF =
+        (!sharded && !dump && affine_on_umma(lw.w2, w.tm_ok ? &w.tm_F : nullptr, (long long)S * L, D))
+            ? w.keepF.as<unsigned char>() : nullptr;
     if (!sharded) {
       LAUNCH(launch_elementwise_verify(c.activation, Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm,
                                        eps, status, site(l, 2), dump ? F_lo : nullptr,
-                                       dump ? F_hi : nullptr, st, nullptr, nullptr, skip));
+                                       dump ? F_hi : nullptr, st, nullptr, nullptr, skip, keepF));
     } else {
       if (fg_status s = concretize_site(m, Fl, w.crF, F_lb, F_ub, (long long)L * F, nF, D, norm, eps, F_lo, F_hi))
         return s;
@@ -1221,7 +1237,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
     // cur = res1 + affine(act, W2)
     g_tag = "affine_gemm";
     LAUNCH(launch_affine_lambda(lw.w2, w.tm_ok ? &w.tm_F : nullptr, Fl, w.crF, X, w.crX, R1, w.crX,
-                                (long long)S * L, D, st, skip, L));
+                                (long long)S * L, D, st, skip, L, keepF));
     g_tag = "affine_bias";
     LAUNCH(launch_affine_bias(F_lb, F_ub, lw.w2.w64.as<double>(), lw.w2.b64.as<double>(), R1_lb, R1_ub,
                               X_lb, X_ub, S, L, F, E, st, skip));

@@ -85,7 +85,8 @@ int launch_elementwise_verify(int kind, float* lam, long long cr, double* lb, do
                               long long rows_per_s, long long nrows, int D, int norm,
                               const double* eps, int* status, int site, double* lo_out,
                               double* hi_out, cudaStream_t st, const double* lo_in = nullptr,
-                              const double* hi_in = nullptr, const int* skip = nullptr);
+                              const double* hi_in = nullptr, const int* skip = nullptr,
+                              unsigned char* keep = nullptr);
 
 // Standalone envelope / compose (operator-level API).
 int launch_relax(int kind, const double* lo, const double* hi, long long n, double* a_low,
@@ -201,6 +202,9 @@ struct LamGemm {
   int accumulate;
   int tiles_m, tiles_n, num_tiles;  // set by launch_lam_gemm
   int epi_groups;                   // epilogue warp groups draining tiles (1 or 2; launch_lam_gemm)
+  // optional K-row mask (keep[b0 * K + k] == 0: Λ row k of batch row b0 is zero, whatever the
+  // buffer holds; written by elementwise_verify's `keep`): the split warps zero those rows
+  const unsigned char* kmask;
   // optional gather of batch coordinate b2 (sparse first-layer McCormick terms): when set,
   // b2 <- gather[slot_map[b0] * gather_ld + b2] (the perturbed token of word b2 of sentence b0)
   const int* gather;

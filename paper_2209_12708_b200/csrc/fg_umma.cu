@@ -418,9 +418,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
     for (int t = unit; t < num_tiles; t += nunits) {
       if (skipped(t)) continue;
+      const unsigned char* mrow = nullptr;  // K-row mask of this thread's batch row (LamGemm::kmask)
+      if (p.kmask) {
+        int b[4], m0, n0;
+        decode(t, b, m0, n0);
+        mrow = p.kmask + (long long)(b[0] + (p.fold1 == 1 ? (d >> 6) : 0)) * p.K;
+      }
 #pragma unroll 1
       for (int kb = 0; kb < nkb; ++kb, ++g) {
         const int s = g % S, r = g % R;
+        uint4 mk0 = make_uint4(0, 0, 0, 0), mk1 = mk0;
+        if (mrow) {  // issued before the waits: its latency overlaps them
+          mk0 = __ldg(reinterpret_cast<const uint4*>(mrow + kb * kBK));
+          mk1 = __ldg(reinterpret_cast<const uint4*>(mrow + kb * kBK) + 1);
+        }
         mbar_wait(&rawfull[r], (g / R) & 1);
         mbar_wait(&opempty[s], ((g / S) & 1) ^ 1);  // the MMAs of this stage's previous use are done
         uint8_t* st = smem + s * RL::kOp;
@@ -438,6 +449,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (async-proxy) write into the same buffer, then release it
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&rawfree[r]);
+        if (mrow) {
+          const uint32_t mw[8] = {mk0.x, mk0.y, mk0.z, mk0.w, mk1.x, mk1.y, mk1.z, mk1.w};
+#pragma unroll
+          for (int k = 0; k < kBK; ++k)
+            if (((mw[k >> 2] >> (8 * (k & 3))) & 0xffu) == 0) v[k] = 0.f;
+        }
 #pragma unroll
         for (int j = 0; j < kBK / 4; ++j) {
           float h[4], l[4];
