@@ -195,7 +195,8 @@ struct DevAffine {
   DBuf a_hi, a_lo;        // [2][O][C] f32: (W^T, |W|^T) split for 3xTF32 (tcgen05 path)
   TensorMap tm_hi, tm_lo;
   TensorMap tm2_hi, tm2_lo;  // box height bn/2: one CTA's half of a W tile (CTA-pair kernel)
-  bool umma = false, umma2 = false;
+  TensorMap tmA_hi, tmA_lo;  // box height 128: the N tile of the TMEM-operand engine
+  bool umma = false, umma2 = false, ummaA = false;
   int bn = 0;
   int C = 0, O = 0;
 };
@@ -244,6 +245,8 @@ fg_status upload_affine(fg_ctx* ctx, DevAffine& a, int C, int O, const std::vect
              umma_tmap_wop(a.tm_lo.bytes, a.a_lo.as<float>(), C, O, 2, 1, a.bn);
     a.umma2 = a.umma && a.bn >= 64 && umma_tmap_wop(a.tm2_hi.bytes, a.a_hi.as<float>(), C, O, 2, 1, a.bn / 2) &&
               umma_tmap_wop(a.tm2_lo.bytes, a.a_lo.as<float>(), C, O, 2, 1, a.bn / 2);
+    a.ummaA = a.umma && O % 128 == 0 && umma_tmap_wop(a.tmA_hi.bytes, a.a_hi.as<float>(), C, O, 2, 1, 128) &&
+              umma_tmap_wop(a.tmA_lo.bytes, a.a_lo.as<float>(), C, O, 2, 1, 128);
   }
   return FG_OK;
 }
@@ -262,6 +265,18 @@ bool umma_dots_enabled() {
 bool umma_affine_enabled() {
   const char* e = std::getenv("FG_NO_UMMA_AFFINE");
   return umma_enabled() && !(e && e[0] == '1');
+}
+// affine GEMMs with the split Λ operand in tensor memory (LamGemm::tmem_a, N tile 128):
+// FG_AFFINE_TMEM_A=1.  Off by default: measured 8 % slower than the shared-memory engine at N tile
+// 256, whose two 256-column accumulators leave no tensor memory for operand stages.
+bool affine_tmem_a_enabled() {
+  const char* e = std::getenv("FG_AFFINE_TMEM_A");
+  return e && e[0] == '1';
+}
+// McCormick GEMMs with the split Λ operand in tensor memory (FG_DOTS_TMEM_A=0: shared memory)
+bool dots_tmem_a_enabled() {
+  const char* e = std::getenv("FG_DOTS_TMEM_A");
+  return !(e && e[0] == '0');
 }
 
 // Λ bound GEMM of one affine over `rows` token rows: tcgen05 3xTF32 when the shape and
@@ -315,6 +330,10 @@ int launch_affine_lambda(const DevAffine& a, const TensorMap* tm_in, const float
     g.skip_status = skip_status;
     g.skip_div = rows_per_slot;
     g.skip_slots = (int)(rows / rows_per_slot);
+    if (a.ummaA && D % 128 == 0 && affine_tmem_a_enabled()) {
+      g.tmem_a = 1;
+      return launch_lam_gemm(tm_in->bytes, a.tmA_hi.bytes, a.tmA_lo.bytes, g, 128, st);
+    }
     return launch_lam_gemm(tm_in->bytes, a.tm_hi.bytes, a.tm_lo.bytes, g, a.bn, st,
                            a.umma2 ? a.tm2_hi.bytes : nullptr, a.umma2 ? a.tm2_lo.bytes : nullptr);
   }
@@ -1080,6 +1099,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
         gx.gather_slot = w.slot_map.as<int>();
         gx.gather_ld = w.W;
       }
+      gx.tmem_a = dots_tmem_a_enabled();
       LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_x[0].bytes, w.tm_sim_x[1].bytes, gx, w.bn_simx, st,
                              w.dots2_ok ? w.tm2_sim_x[0].bytes : nullptr, w.dots2_ok ? w.tm2_sim_x[1].bytes : nullptr));
       // y-side: scores[s,h,i,j,:] += sum_k lx[i,k] K_p[j, E + h*hd + k]   (per plane p)
@@ -1107,6 +1127,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
         gy.gather_slot = w.slot_map.as<int>();
         gy.gather_ld = w.W;
       }
+      gy.tmem_a = dots_tmem_a_enabled();
       LAUNCH(launch_lam_gemm(w.tm_QKVk.bytes, w.tm_sim_y[0].bytes, w.tm_sim_y[1].bytes, gy, w.bn_sim, st,
                              w.dots2_ok ? w.tm2_sim_y[0].bytes : nullptr, w.dots2_ok ? w.tm2_sim_y[1].bytes : nullptr));
     } else {
@@ -1161,6 +1182,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gx.skip_div = 1;
       gx.skip_slots = S;
       if (w.fold64) gx.fold1 = 3;  // pairs of query tokens i
+      gx.tmem_a = dots_tmem_a_enabled();
       LAUNCH(launch_lam_gemm(w.tm_SC.bytes, w.tm_wv_x[0].bytes, w.tm_wv_x[1].bytes, gx, w.bn_wvx, st,
                              w.dots2_ok ? w.tm2_wv_x[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_x[1].bytes : nullptr));
       // y-side: ctx[s,i,h*hd+k,:] += sum_j lx[i,j] V_p[j, 2E + h*hd + k]   (K along token rows)
@@ -1182,6 +1204,7 @@ fg_status enqueue_pass(fg_model* m, int norm, Dumper* dump, Workspace* wsp = nul
       gy.skip_div = 1;
       gy.skip_slots = S;
       if (w.fold64) gy.fold1 = 3;  // pairs of head features k
+      gy.tmem_a = dots_tmem_a_enabled();
       LAUNCH(launch_lam_gemm(w.tm_QKVrow.bytes, w.tm_wv_y[0].bytes, w.tm_wv_y[1].bytes, gy, w.bn_sim, st,
                              w.dots2_ok ? w.tm2_wv_y[0].bytes : nullptr, w.dots2_ok ? w.tm2_wv_y[1].bytes : nullptr));
     } else {
@@ -2528,9 +2551,15 @@ fg_status fg_selftest_affine(fg_ctx* ctx, int rows, int C, int O, int D, uint64_
   bool umma = a.umma && have_tm;
   if (umma) {
     CK(cudaEventRecord(e0, ctx->stream));
-    LAUNCH(launch_lam_gemm(tm.bytes, a.tm_hi.bytes, a.tm_lo.bytes, affine_lam(a, Y2.as<float>(), nout, nullptr, 0, rows, D),
-                           a.bn, ctx->stream, a.umma2 ? a.tm2_hi.bytes : nullptr,
-                           a.umma2 ? a.tm2_lo.bytes : nullptr));
+    if (a.ummaA && D % 128 == 0 && affine_tmem_a_enabled()) {
+      LamGemm g = affine_lam(a, Y2.as<float>(), nout, nullptr, 0, rows, D);
+      g.tmem_a = 1;
+      LAUNCH(launch_lam_gemm(tm.bytes, a.tmA_hi.bytes, a.tmA_lo.bytes, g, 128, ctx->stream));
+    } else {
+      LAUNCH(launch_lam_gemm(tm.bytes, a.tm_hi.bytes, a.tm_lo.bytes, affine_lam(a, Y2.as<float>(), nout, nullptr, 0, rows, D),
+                             a.bn, ctx->stream, a.umma2 ? a.tm2_hi.bytes : nullptr,
+                             a.umma2 ? a.tm2_lo.bytes : nullptr));
+    }
     CK(cudaEventRecord(e1, ctx->stream));
     CK(cudaEventSynchronize(e1));
     cudaEventElapsedTime(&t, e0, e1);

@@ -205,6 +205,10 @@ struct LamGemm {
   // optional K-row mask (keep[b0 * K + k] == 0: Λ row k of batch row b0 is zero, whatever the
   // buffer holds; written by elementwise_verify's `keep`): the split warps zero those rows
   const unsigned char* kmask;
+  // 1: the split Λ operand is staged in tensor memory instead of shared memory (tcgen05.mma
+  // with A from TMEM; N tile 128, single CTA): shared memory then carries only the W operand
+  // stages, the raw Λ ring and the tensor core's W reads
+  int tmem_a;
   // optional gather of batch coordinate b2 (sparse first-layer McCormick terms): when set,
   // b2 <- gather[slot_map[b0] * gather_ld + b2] (the perturbed token of word b2 of sentence b0)
   const int* gather;

@@ -129,6 +129,47 @@ __device__ __forceinline__ void umma3_kchunk(uint32_t d_tmem, uint64_t ahi, uint
 #undef FG_MMA
 }
 
+// The same K chunk with the Λ operand (A) read from tensor memory: a_hi / a_lo are the TMEM
+// addresses of the chunk's 32 hi / 32 lo columns (one tf32 per 32-bit column, row d = lane d),
+// advanced by 8 columns per K-step.  Only the W operand (B) is read from shared memory.
+__device__ __forceinline__ void umma3_kchunk_ts(uint32_t d_tmem, uint32_t ahi, uint32_t alo, uint64_t bhi,
+                                                uint64_t blo, uint32_t idesc, uint32_t acc_first) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b32 a0, a1;\n\t.reg .b64 b0, b1;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %6, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %6, t;\n\t"
+      "add.u32 a0, %1, 8;\n\tadd.u32 a1, %2, 8;\n\tadd.s64 b0, %3, 2;\n\tadd.s64 b1, %4, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a0], b0, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], b0, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a0], b1, %6, t;\n\t"
+      "add.u32 a0, %1, 16;\n\tadd.u32 a1, %2, 16;\n\tadd.s64 b0, %3, 4;\n\tadd.s64 b1, %4, 4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a0], b0, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], b0, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a0], b1, %6, t;\n\t"
+      "add.u32 a0, %1, 24;\n\tadd.u32 a1, %2, 24;\n\tadd.s64 b0, %3, 6;\n\tadd.s64 b1, %4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a0], b0, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], b0, %6, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a0], b1, %6, t;\n}"
+      ::"r"(d_tmem), "r"(ahi), "r"(alo), "l"(bhi), "l"(blo), "r"(acc_first), "r"(idesc));
+}
+
+// 32 consecutive 32-bit TMEM columns of this thread's lane (warp w accesses lanes 32(w%4)..+31)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -185,14 +226,18 @@ __device__ __forceinline__ void mbar_arrive_cta0(uint64_t* local_bar) {
 
 // SMEM plan: an operand ring of S stages {W_hi, W_lo, L_hi, L_lo} feeding the MMA and a raw
 // ring of R Λ tiles feeding the split warps, so Λ loads run ahead of the operand stages.
-template <int BN, int S, int R, bool PAIR>
+// TA: the split Λ operand lives in tensor memory (S stages of 64 columns after the two
+// accumulators), so a shared-memory operand stage holds only {W_hi, W_lo}.
+template <int BN, int S, int R, bool PAIR, bool TA = false>
 struct Ring {
   static constexpr int kWT = (PAIR ? BN / 2 : BN) * kBK * 4;  // this CTA's W tile, hi or lo
   static constexpr int kL = kBK * kBM * 4;                    // Λ tile: 16 KB
   static constexpr int kWlo = kWT;
   static constexpr int kLhi = 2 * kWT;
   static constexpr int kLlo = 2 * kWT + kL;
-  static constexpr int kOp = 2 * kWT + 2 * kL;
+  static constexpr int kOp = TA ? 2 * kWT : 2 * kWT + 2 * kL;
+  static constexpr int kTmemCols = TA ? 512 : (2 * BN < 32 ? 32 : 2 * BN);  // allocation: a power of 2
+  static_assert(!TA || (2 * BN + S * 2 * kBK <= 512 && !PAIR), "TMEM plan of the TA engine: 2 accumulators + S A stages");
   static constexpr int kRawOff = S * kOp;
   static constexpr int kBarOff = kRawOff + R * kL;
   static constexpr int kMaskOff = kBarOff + 256;        // early-exit slot bitmask (32 words)
@@ -209,11 +254,11 @@ struct Ring {
 // leader's `tempty`.
 //   warp 0: W producer    warp 1: TMEM alloc + MMA issuer    warp 2: Λ producer
 //   warps 4-7: split/transpose Λ -> L_hi/L_lo    warps 8-15: epilogue (2 groups)
-template <int BN, int S, int R, bool PAIR>
+template <int BN, int S, int R, bool PAIR, bool TA = false>
 __global__ void __launch_bounds__(kThreads, 1)
     lam_gemm_kernel(const __grid_constant__ CUtensorMap tm_lam, const __grid_constant__ CUtensorMap tm_whi,
                     const __grid_constant__ CUtensorMap tm_wlo, const LamGemm p) {
-  using RL = Ring<BN, S, R, PAIR>;
+  using RL = Ring<BN, S, R, PAIR, TA>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + RL::kBarOff);
@@ -273,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     } else {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                   "r"(2 * BN < 32 ? 32 : 2 * BN));
+                   "r"(RL::kTmemCols));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
   }
@@ -393,8 +438,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           {
             // +32 B per 8 tf32 of K inside the 128 B rows (umma3_kchunk)
             const uint32_t st = smem_u32(smem) + s * RL::kOp;
-            umma3_kchunk<PAIR>(d_tmem, kmajor_sw128_desc(st + RL::kLhi), kmajor_sw128_desc(st + RL::kLlo),
-                               kmajor_sw128_desc(st), kmajor_sw128_desc(st + RL::kWlo), idesc, kb != 0);
+            if (TA) {
+              const uint32_t a = tmem_base + 2 * BN + s * 2 * kBK;
+              umma3_kchunk_ts(d_tmem, a, a + kBK, kmajor_sw128_desc(st), kmajor_sw128_desc(st + RL::kWlo), idesc,
+                              kb != 0);
+            } else {
+              umma3_kchunk<PAIR>(d_tmem, kmajor_sw128_desc(st + RL::kLhi), kmajor_sw128_desc(st + RL::kLlo),
+                                 kmajor_sw128_desc(st), kmajor_sw128_desc(st + RL::kWlo), idesc, kb != 0);
+            }
           }
           if (lane == 0) {
             if (PAIR) {
@@ -454,6 +505,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK; ++k)
             if (((mw[k >> 2] >> (8 * (k & 3))) & 0xffu) == 0) v[k] = 0.f;
+        }
+        if (TA) {
+          // hi / lo parts into this stage's tensor-memory columns (lane d = this thread's row)
+          tc_fence_after();  // after the opempty wait: the stage's previous MMAs are done
+          uint32_t hl[kBK], lo[kBK];
+#pragma unroll
+          for (int k = 0; k < kBK; ++k) {
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hl[k]) : "f"(v[k]));
+            lo[k] = __float_as_uint(v[k] - __uint_as_float(hl[k]));
+          }
+          const uint32_t ta = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + 2 * BN + s * 2 * kBK;
+          tmem_st32(ta, hl);
+          tmem_st32(ta + kBK, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          mbar_wait(&wfull[s], (g / S) & 1);  // this CTA's W tile landed too
+          mbar_arrive(&split[s]);
+          continue;
         }
 #pragma unroll
         for (int j = 0; j < kBK / 4; ++j) {
@@ -604,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    "r"(2 * BN < 32 ? 32 : 2 * BN));
     else
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                   "r"(2 * BN < 32 ? 32 : 2 * BN));
+                   "r"(RL::kTmemCols));
   }
 }
 
@@ -629,11 +698,11 @@ EncodeTiledFn encode_fn() {
 
 int g_num_sms = 0;
 
-template <int BN, int S, int R, bool PAIR>
+template <int BN, int S, int R, bool PAIR, bool TA = false>
 int launch_ring(const void* tm_lam, const void* tm_whi, const void* tm_wlo, const LamGemm& p, int grid,
                 cudaStream_t st) {
-  using RL = Ring<BN, S, R, PAIR>;
-  auto kern = lam_gemm_kernel<BN, S, R, PAIR>;
+  using RL = Ring<BN, S, R, PAIR, TA>;
+  auto kern = lam_gemm_kernel<BN, S, R, PAIR, TA>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RL::kBytes);
@@ -729,7 +798,7 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
     p.f_skip_div = make_fastdiv((uint32_t)std::max(p.skip_div, 1));
     p.f_nsplit = make_fastdiv((uint32_t)std::max(p.n_split, 1));
   };
-  if (tm2_whi && tm2_wlo && p.M % (2 * kBM) == 0 && bn >= 64 && umma_pair_enabled()) {
+  if (!p.tmem_a && tm2_whi && tm2_wlo && p.M % (2 * kBM) == 0 && bn >= 64 && umma_pair_enabled()) {
     if (!g_num_sms) {
       int dev = 0;
       cudaGetDevice(&dev);
@@ -770,6 +839,10 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
   }
   set_divisors(p.tiles_m);
   const int grid = (int)std::min<long long>(tiles, g_num_sms);
+  if (p.tmem_a) {  // Λ operand from tensor memory: two accumulators + 4 operand stages of 64 columns
+    if (bn == 128) return launch_ring<128, 4, 6, false, true>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+    if (bn == 64) return launch_ring<64, 4, 6, false, true>(tm_lam, tm_whi, tm_wlo, p, grid, st);
+  }
   switch (bn) {
     case 256: return launch_ring<256, 2, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
     case 128: return launch_ring<128, 3, 2, false>(tm_lam, tm_whi, tm_wlo, p, grid, st);
