@@ -655,68 +655,110 @@ __global__ void compose_kernel(const float* __restrict__ lin, long long crin, co
 // Affine bias path (relax.cpp:273-299) in f64: one thread per output neuron,
 // i accumulated in the reference's order; optional residual propagate_add(res, y).
 // ---------------------------------------------------------------------------
-constexpr int kBiasRows = 8;     // token rows per CTA (one weight load feeds all of them)
-constexpr int kBiasCols = 128;   // output neurons per CTA (one per thread)
-constexpr int kBiasChunk = 256;  // input neurons staged in SMEM per step
+// ---------------------------------------------------------------------------
+// Affine bias in f64 (relax.cpp:280-303 on the O(N) part): per token row r and output j
+//   ub' = sum_i (W > 0 ? W ub : W lb) + b,   lb' = sum_i (W > 0 ? W lb : W ub) + b  (+ residual)
+// as the two FP64 products  m = W . mid,  q = |W| . rad  (mid = (lb + ub) / 2, rad = (ub - lb) / 2,
+// ub' = m + q + b, lb' = m - q + b): the same sums without a per-term sign select, so the kernel
+// is a register-tiled DFMA GEMM (rows x outputs, K = inputs).  CTA tile 64 rows x 64 outputs,
+// 16-deep K chunks staged in shared memory (W and |W|, mid and rad), thread tile 4 x 4 with rows
+// {2ty, 2ty + 1, 32 + 2ty, 33 + 2ty} and outputs likewise in tx (double2 loads, conflict-free).
+// Rounding differs from the reference's four sign-half sums by f64 ulps, far inside the fused
+// pass's f32 error band (the exact mode keeps the reference's order, fg_exact.cu).
+// ---------------------------------------------------------------------------
+constexpr int kBgR = 64, kBgJ = 64, kBgK = 16;
+constexpr int kBgPad = 2;  // row padding (doubles): conflict-free K-fastest staging stores, 16 B aligned
 
-__global__ void __launch_bounds__(kBiasCols) affine_bias_kernel(
+__global__ void __launch_bounds__(256, 1) affine_bias_kernel(
     const double* __restrict__ lb_in, const double* __restrict__ ub_in, const double* __restrict__ w,
     const double* __restrict__ bias, const double* __restrict__ res_lb, const double* __restrict__ res_ub,
     double* __restrict__ lb_out, double* __restrict__ ub_out, long long nrows, int C, int O,
     const int* __restrict__ skip, int rows_per_slot) {
-  __shared__ double2 xs[kBiasRows][kBiasChunk];  // (lb, ub) of the CTA's rows
-  const int j = blockIdx.x * kBiasCols + threadIdx.x;
-  const long long r0 = (long long)blockIdx.y * kBiasRows;
+  __shared__ __align__(16) double sM[kBgK][kBgR + kBgPad];
+  __shared__ __align__(16) double sR[kBgK][kBgR + kBgPad];
+  __shared__ __align__(16) double sW[kBgK][kBgJ];
+  __shared__ __align__(16) double sA[kBgK][kBgJ];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long long r0 = (long long)blockIdx.y * kBgR;
+  const int j0 = blockIdx.x * kBgJ;
   // every row of the CTA in failed slots (block-uniform test)
   if (skip && slot_failed(skip, r0 / rows_per_slot) &&
-      slot_failed(skip, (min(r0 + kBiasRows, nrows) - 1) / rows_per_slot))
+      slot_failed(skip, (min(r0 + kBgR, nrows) - 1) / rows_per_slot))
     return;
-  double ub_acc[kBiasRows], lb_acc[kBiasRows];
+  double am[4][4], aq[4][4];
 #pragma unroll
-  for (int r = 0; r < kBiasRows; ++r) ub_acc[r] = lb_acc[r] = 0.0;
-  for (int i0 = 0; i0 < C; i0 += kBiasChunk) {
-    const int n = min(kBiasChunk, C - i0);
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) am[q][c] = aq[q][c] = 0.0;
+  // staging: element e = threadIdx.x + 256 p (p < 4) of the chunk; (lb, ub) with K fastest
+  // (k = e % 16, row = e / 16: coalesced 128 B row segments), W with outputs fastest.  The next
+  // chunk's values are loaded into registers while the current chunk is multiplied.
+  double pl[4], pu[4], pw[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int e = threadIdx.x + 256 * p;
+      const int k = e % kBgK, r = e / kBgK;
+      const bool ok = r0 + r < nrows && k0 + k < C;
+      pl[p] = ok ? lb_in[(r0 + r) * C + k0 + k] : 0.0;
+      pu[p] = ok ? ub_in[(r0 + r) * C + k0 + k] : 0.0;
+      const int j = e % kBgJ, kw = e / kBgJ;
+      pw[p] = (k0 + kw < C && j0 + j < O) ? w[(long long)(k0 + kw) * O + j0 + j] : 0.0;
+    }
+  };
+  load(0);
+  for (int k0 = 0; k0 < C; k0 += kBgK) {
     __syncthreads();
-    for (int t = threadIdx.x; t < kBiasRows * kBiasChunk; t += kBiasCols) {
-      const int r = t / kBiasChunk, i = t % kBiasChunk;
-      double2 v = make_double2(0.0, 0.0);
-      if (i < n && r0 + r < nrows) v = make_double2(lb_in[(r0 + r) * C + i0 + i], ub_in[(r0 + r) * C + i0 + i]);
-      xs[r][i] = v;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int e = threadIdx.x + 256 * p;
+      sM[e % kBgK][e / kBgK] = 0.5 * (pl[p] + pu[p]);
+      sR[e % kBgK][e / kBgK] = 0.5 * (pu[p] - pl[p]);
+      sW[e / kBgJ][e % kBgJ] = pw[p];
+      sA[e / kBgJ][e % kBgJ] = fabs(pw[p]);
     }
     __syncthreads();
-    if (j < O) {
-      // sign-selected operand, one f64 FMA per bound: y_ub += w * (w > 0 ? ub : lb),
-      // y_lb += w * (w > 0 ? lb : ub) -- the sum of relax.cpp:280-287 (whose four separate
-      // sign-half sums the exact mode, fg_exact.cu, keeps bit for bit) at a quarter of the FP64
-      // instructions; unrolled so several weight loads are in flight per thread
-#pragma unroll 8
-      for (int i = 0; i < n; ++i) {
-        const double wv = w[(long long)(i0 + i) * O + j];
-        const bool pos = wv > 0.0;
+    if (k0 + kBgK < C) load(k0 + kBgK);
 #pragma unroll
-        for (int r = 0; r < kBiasRows; ++r) {
-          const double2 x = xs[r][i];
-          ub_acc[r] = __fma_rn(wv, pos ? x.y : x.x, ub_acc[r]);
-          lb_acc[r] = __fma_rn(wv, pos ? x.x : x.y, lb_acc[r]);
+    for (int k = 0; k < kBgK; ++k) {
+      const double2 m0 = *reinterpret_cast<const double2*>(&sM[k][2 * ty]);
+      const double2 m1 = *reinterpret_cast<const double2*>(&sM[k][32 + 2 * ty]);
+      const double2 q0 = *reinterpret_cast<const double2*>(&sR[k][2 * ty]);
+      const double2 q1 = *reinterpret_cast<const double2*>(&sR[k][32 + 2 * ty]);
+      const double2 w0 = *reinterpret_cast<const double2*>(&sW[k][2 * tx]);
+      const double2 w1 = *reinterpret_cast<const double2*>(&sW[k][32 + 2 * tx]);
+      const double2 a0 = *reinterpret_cast<const double2*>(&sA[k][2 * tx]);
+      const double2 a1 = *reinterpret_cast<const double2*>(&sA[k][32 + 2 * tx]);
+      const double mv[4] = {m0.x, m0.y, m1.x, m1.y}, qv[4] = {q0.x, q0.y, q1.x, q1.y};
+      const double wv[4] = {w0.x, w0.y, w1.x, w1.y}, av[4] = {a0.x, a0.y, a1.x, a1.y};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          am[q][c] = __fma_rn(wv[c], mv[q], am[q][c]);
+          aq[q][c] = __fma_rn(av[c], qv[q], aq[q][c]);
         }
-      }
     }
   }
-  if (j >= O) return;
-  const double bv = bias ? bias[j] : 0.0;
 #pragma unroll
-  for (int r = 0; r < kBiasRows; ++r) {
-    const long long row = r0 + r;
-    if (row >= nrows) break;
-    const long long t = row * O + j;
-    double yub = ub_acc[r] + bv;
-    double ylb = lb_acc[r] + bv;
-    if (res_lb) {  // propagate_add(res, y) (relax.cpp:666-667)
-      yub = res_ub[t] + yub;
-      ylb = res_lb[t] + ylb;
+  for (int q = 0; q < 4; ++q) {
+    const long long row = r0 + 2 * ty + (q & 1) + 32 * (q >> 1);
+    if (row >= nrows) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = j0 + 2 * tx + (c & 1) + 32 * (c >> 1);
+      if (j >= O) continue;
+      const double bv = bias ? bias[j] : 0.0;
+      const long long t = row * O + j;
+      double yub = (am[q][c] + aq[q][c]) + bv;
+      double ylb = (am[q][c] - aq[q][c]) + bv;
+      if (res_lb) {  // propagate_add(res, y) (relax.cpp:666-667)
+        yub = res_ub[t] + yub;
+        ylb = res_lb[t] + ylb;
+      }
+      ub_out[t] = yub;
+      lb_out[t] = ylb;
     }
-    ub_out[t] = yub;
-    lb_out[t] = ylb;
   }
 }
 
@@ -2951,8 +2993,8 @@ int launch_affine_bias(const double* lb_in, const double* ub_in, const double* w
   long long nrows = (long long)S * rows;
   long long total = nrows * O;
   if (total <= 0) return 0;
-  dim3 grid(blocks_for(O, kBiasCols), blocks_for(nrows, kBiasRows));
-  affine_bias_kernel<<<grid, kBiasCols, 0, st>>>(lb_in, ub_in, w64, bias, res_lb, res_ub, lb_out, ub_out, nrows,
+  dim3 grid(blocks_for(O, kBgJ), blocks_for(nrows, kBgR));
+  affine_bias_kernel<<<grid, 256, 0, st>>>(lb_in, ub_in, w64, bias, res_lb, res_ub, lb_out, ub_out, nrows,
                                                  C, O, skip, rows);
   return 1;
 }
