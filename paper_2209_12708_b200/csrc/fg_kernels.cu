@@ -667,32 +667,43 @@ __global__ void compose_kernel(const float* __restrict__ lin, long long crin, co
 // pass's f32 error band (the exact mode keeps the reference's order, fg_exact.cu).
 // ---------------------------------------------------------------------------
 constexpr int kBgR = 64, kBgJ = 64, kBgK = 16;
-constexpr int kBgPad = 2;  // row padding (doubles): conflict-free K-fastest staging stores, 16 B aligned
+constexpr int kBgS = 68;  // padded SMEM row (doubles): conflict-free DMMA fragment loads (68 = 4 mod 16)
 
-__global__ void __launch_bounds__(256, 1) affine_bias_kernel(
+// f64 tensor-core version (DMMA m8n8k4): CTA tile 64 rows x 64 outputs, 8 warps as 2 x 4, warp
+// tile 32 x 16 = 4 x 2 MMA tiles of 8 x 8 per product; K chunks of 16 staged k-major in shared
+// memory (mid, rad rows; W, |W| columns), the next chunk prefetched into registers.
+// Fragments (PTX mma.m8n8k4 .f64): A[r][k] with r = lane >> 2, k = lane & 3; B[k][n] with
+// k = lane & 3, n = lane >> 2; C[r][2 (lane & 3) + i].
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) affine_bias_kernel(
     const double* __restrict__ lb_in, const double* __restrict__ ub_in, const double* __restrict__ w,
     const double* __restrict__ bias, const double* __restrict__ res_lb, const double* __restrict__ res_ub,
     double* __restrict__ lb_out, double* __restrict__ ub_out, long long nrows, int C, int O,
     const int* __restrict__ skip, int rows_per_slot) {
-  __shared__ __align__(16) double sM[kBgK][kBgR + kBgPad];
-  __shared__ __align__(16) double sR[kBgK][kBgR + kBgPad];
-  __shared__ __align__(16) double sW[kBgK][kBgJ];
-  __shared__ __align__(16) double sA[kBgK][kBgJ];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  __shared__ __align__(16) double sM[kBgK][kBgS];
+  __shared__ __align__(16) double sR[kBgK][kBgS];
+  __shared__ __align__(16) double sW[kBgK][kBgS];
+  __shared__ __align__(16) double sA[kBgK][kBgS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wr = warp >> 2, wc = warp & 3;  // warp tile rows 32 wr.., outputs 16 wc..
   const long long r0 = (long long)blockIdx.y * kBgR;
   const int j0 = blockIdx.x * kBgJ;
   // every row of the CTA in failed slots (block-uniform test)
   if (skip && slot_failed(skip, r0 / rows_per_slot) &&
       slot_failed(skip, (min(r0 + kBgR, nrows) - 1) / rows_per_slot))
     return;
-  double am[4][4], aq[4][4];
+  double am[4][2][2], aq[4][2][2];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) am[q][c] = aq[q][c] = 0.0;
+    for (int b = 0; b < 2; ++b) am[a][b][0] = am[a][b][1] = aq[a][b][0] = aq[a][b][1] = 0.0;
   // staging: element e = threadIdx.x + 256 p (p < 4) of the chunk; (lb, ub) with K fastest
-  // (k = e % 16, row = e / 16: coalesced 128 B row segments), W with outputs fastest.  The next
-  // chunk's values are loaded into registers while the current chunk is multiplied.
+  // (k = e % 16, row = e / 16: coalesced 128 B row segments), W with outputs fastest
   double pl[4], pu[4], pw[4];
   auto load = [&](int k0) {
 #pragma unroll
@@ -707,6 +718,7 @@ __global__ void __launch_bounds__(256, 1) affine_bias_kernel(
     }
   };
   load(0);
+  const int fr = lane >> 2, fk = lane & 3;
   for (int k0 = 0; k0 < C; k0 += kBgK) {
     __syncthreads();
 #pragma unroll
@@ -720,45 +732,48 @@ __global__ void __launch_bounds__(256, 1) affine_bias_kernel(
     __syncthreads();
     if (k0 + kBgK < C) load(k0 + kBgK);
 #pragma unroll
-    for (int k = 0; k < kBgK; ++k) {
-      const double2 m0 = *reinterpret_cast<const double2*>(&sM[k][2 * ty]);
-      const double2 m1 = *reinterpret_cast<const double2*>(&sM[k][32 + 2 * ty]);
-      const double2 q0 = *reinterpret_cast<const double2*>(&sR[k][2 * ty]);
-      const double2 q1 = *reinterpret_cast<const double2*>(&sR[k][32 + 2 * ty]);
-      const double2 w0 = *reinterpret_cast<const double2*>(&sW[k][2 * tx]);
-      const double2 w1 = *reinterpret_cast<const double2*>(&sW[k][32 + 2 * tx]);
-      const double2 a0 = *reinterpret_cast<const double2*>(&sA[k][2 * tx]);
-      const double2 a1 = *reinterpret_cast<const double2*>(&sA[k][32 + 2 * tx]);
-      const double mv[4] = {m0.x, m0.y, m1.x, m1.y}, qv[4] = {q0.x, q0.y, q1.x, q1.y};
-      const double wv[4] = {w0.x, w0.y, w1.x, w1.y}, av[4] = {a0.x, a0.y, a1.x, a1.y};
+    for (int ks = 0; ks < kBgK; ks += 4) {
+      double fm[4], fq[4], fw[2], fa[2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int a = 0; a < 4; ++a) {
+        fm[a] = sM[ks + fk][wr * 32 + a * 8 + fr];
+        fq[a] = sR[ks + fk][wr * 32 + a * 8 + fr];
+      }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          am[q][c] = __fma_rn(wv[c], mv[q], am[q][c]);
-          aq[q][c] = __fma_rn(av[c], qv[q], aq[q][c]);
+      for (int b = 0; b < 2; ++b) {
+        fw[b] = sW[ks + fk][wc * 16 + b * 8 + fr];
+        fa[b] = sA[ks + fk][wc * 16 + b * 8 + fr];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          dmma884(am[a][b], fm[a], fw[b]);
+          dmma884(aq[a][b], fq[a], fa[b]);
         }
     }
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const long long row = r0 + 2 * ty + (q & 1) + 32 * (q >> 1);
+  for (int a = 0; a < 4; ++a) {
+    const long long row = r0 + wr * 32 + a * 8 + fr;
     if (row >= nrows) continue;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = j0 + 2 * tx + (c & 1) + 32 * (c >> 1);
-      if (j >= O) continue;
-      const double bv = bias ? bias[j] : 0.0;
-      const long long t = row * O + j;
-      double yub = (am[q][c] + aq[q][c]) + bv;
-      double ylb = (am[q][c] - aq[q][c]) + bv;
-      if (res_lb) {  // propagate_add(res, y) (relax.cpp:666-667)
-        yub = res_ub[t] + yub;
-        ylb = res_lb[t] + ylb;
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int j = j0 + wc * 16 + b * 8 + 2 * fk + i;
+        if (j >= O) continue;
+        const double bv = bias ? bias[j] : 0.0;
+        const long long t = row * O + j;
+        double yub = (am[a][b][i] + aq[a][b][i]) + bv;
+        double ylb = (am[a][b][i] - aq[a][b][i]) + bv;
+        if (res_lb) {  // propagate_add(res, y) (relax.cpp:666-667)
+          yub = res_ub[t] + yub;
+          ylb = res_lb[t] + ylb;
+        }
+        ub_out[t] = yub;
+        lb_out[t] = ylb;
       }
-      ub_out[t] = yub;
-      lb_out[t] = ylb;
-    }
   }
 }
 
