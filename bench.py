@@ -519,6 +519,12 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
+    if w.name in ("c4", "c5"):
+        # random-init weights at these depths widen the bounds ~10^3x per layer (DESIGN.md §9,
+        # profiles/r1_width_growth_by_depth.txt): the certified radius is ~0 and most probes above
+        # it end in a domain error, so sentences/s here times searches of mostly failing probes
+        line["workload_note"] = ("degenerate on random-init weights: certified eps ~0, probes above it mostly end "
+                                 "in domain errors (early exit)")
 
     prof = None
     prof_clk = None
