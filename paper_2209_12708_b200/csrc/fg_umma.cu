@@ -217,11 +217,26 @@ __device__ __forceinline__ long long lin5l(const long long* co, const int* b) {
   return co[0] * b[0] + co[1] * b[1] + co[2] * b[2] + co[3] * b[3] + co[4];
 }
 
-// Arrive on the pair leader's (CTA rank 0) copy of a barrier.
+// Arrive on the pair leader's (CTA rank 0) copy of a barrier.  The release is restricted to
+// shared memory (fence.release.sync_restrict::shared::cta.cluster + a relaxed cluster arrive:
+// MEMBAR.CTA + FENCE.VIEW.ASYNC instead of the MEMBAR.GPU a .release.cluster arrive costs); the
+// writes it publishes are this CTA's shared-memory operand tiles (already fenced to the async
+// proxy) or, for the accumulator drain, ordered by tcgen05.fence::before_thread_sync.
 __device__ __forceinline__ void mbar_arrive_cta0(uint64_t* local_bar) {
   uint32_t a;
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(a) : "r"(smem_u32(local_bar)));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+  asm volatile("fence.release.sync_restrict::shared::cta.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+// Wait on a local barrier that remote CTAs of the cluster arrive on (cluster-scope acquire).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // SMEM plan: an operand ring of S stages {W_hi, W_lo, L_hi, L_lo} feeding the MMA and a raw
@@ -427,13 +442,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (skipped(t)) continue;
         ++it;
         const int acc = it & 1;
-        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        if (PAIR) mbar_wait_cluster(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        else mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
 #pragma unroll 1
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = g % S;
-          mbar_wait(&split[s], (g / S) & 1);
+          if (PAIR) mbar_wait_cluster(&split[s], (g / S) & 1);
+          else mbar_wait(&split[s], (g / S) & 1);
           tc_fence_after();
           {
             // +32 B per 8 tf32 of K inside the 128 B rows (umma3_kchunk)
@@ -763,8 +780,11 @@ bool umma_tmap_wop(void* tm, const float* base, int K, int N, int P2, int P3, in
 bool umma_pair_enabled() {
   static int v = -1;
   if (v < 0) {
-    const char* e = std::getenv("FG_2CTA");  // CTA-pair kernel: opt-in (slower than one CTA so far)
-    v = (e && e[0] == '1') ? 1 : 0;
+    // CTA-pair kernel (cta_group::2, M = 256) wherever the shape allows it: half the W tile per
+    // CTA and per-pair operand handoffs with a shared-memory-restricted cluster release
+    // (mbar_arrive_cta0); measured 53-55 -> 47-48 ms per c3 pass on the affine GEMMs.  FG_2CTA=0: one CTA
+    const char* e = std::getenv("FG_2CTA");
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }
