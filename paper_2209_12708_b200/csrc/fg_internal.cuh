@@ -209,6 +209,7 @@ struct LamGemm {
   // with A from TMEM; N tile 128, single CTA): shared memory then carries only the W operand
   // stages, the raw Λ ring and the tensor core's W reads
   int tmem_a;
+  int pair_b0;  // CTA pair over batch rows 2b, 2b + 1 instead of d-tiles (M = 128; launch_lam_gemm)
   // optional gather of batch coordinate b2 (sparse first-layer McCormick terms): when set,
   // b2 <- gather[slot_map[b0] * gather_ld + b2] (the perturbed token of word b2 of sentence b0)
   const int* gather;

@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int tiles_m = PAIR ? p.tiles_m / 2 : p.tiles_m;
+  // pair_b0: the pair's two 128-row halves are batch rows 2b and 2b + 1 (M = D = 128), not d-tiles
+  const int tiles_m = (PAIR && !p.pair_b0) ? p.tiles_m / 2 : p.tiles_m;
   const int num_tiles = PAIR ? p.num_tiles / 2 : p.num_tiles;
   // arrivals on the leader's split / tempty barriers: every split / epilogue thread of a single
   // CTA; one elected thread per CTA of a pair (after a named barrier of its 128 threads: remote
@@ -361,7 +362,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     b[0] = q;
     if (p.gather) b[2] = p.gather[p.gather_slot[b[0]] * p.gather_ld + b[2]];
     if (p.fold1) add_at(b, p.fold1 - 1, get_at(b, p.fold1 - 1));  // the pair (2b, 2b + 1) of the folded coordinate
-    m0 = mt * (PAIR ? 2 : 1) * kBM + (int)rank * kBM;  // this CTA's first d-row
+    if (PAIR && p.pair_b0) {  // this CTA's batch row of the pair
+      b[0] = 2 * b[0] + (int)rank;
+      m0 = mt * kBM;
+    } else {
+      m0 = mt * (PAIR ? 2 : 1) * kBM + (int)rank * kBM;  // this CTA's first d-row
+    }
     n0 = nt * BN;
   };
   // every role skips the same tiles (the status words are not written during this kernel), so
@@ -818,23 +824,30 @@ int launch_lam_gemm(const void* tm_lam, const void* tm_whi, const void* tm_wlo, 
     p.f_skip_div = make_fastdiv((uint32_t)std::max(p.skip_div, 1));
     p.f_nsplit = make_fastdiv((uint32_t)std::max(p.n_split, 1));
   };
-  if (!p.tmem_a && tm2_whi && tm2_wlo && p.M % (2 * kBM) == 0 && bn >= 64 && umma_pair_enabled()) {
+  // pairs over batch rows (M = 128): both rows must share the W tile (W independent of b0) and an
+  // early-exit slot
+  const bool skip_on = p.skip_status && p.skip_slots > 0 && p.skip_slots <= 1024 && p.skip_div > 0;
+  const bool pair_rows = p.M == kBM && !p.fold1 && !p.gather && p.nb[0] % 2 == 0 && p.w_c[0][0] == 0 &&
+                         p.w_c[1][0] == 0 && (!skip_on || p.skip_div % 2 == 0);
+  if (!p.tmem_a && tm2_whi && tm2_wlo && (p.M % (2 * kBM) == 0 || pair_rows) && bn >= 64 && umma_pair_enabled()) {
     if (!g_num_sms) {
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    p.pair_b0 = p.M % (2 * kBM) != 0;
     p.tiles_m = p.M / kBM;
     p.tiles_n = p.N / bn;
     long long tiles = (long long)p.tiles_m * p.tiles_n * p.nb[0] * p.nb[1] * p.nb[2] * p.nb[3];
     if (tiles <= 0 || tiles > 0x7fffffff) return -1;
     p.num_tiles = (int)tiles;  // single-CTA tiles; the pair kernel walks tiles / 2 pair tiles
     p.skip_tiles_per_b0 = 0;
-    if (p.skip_status && p.skip_slots > 0 && p.skip_slots <= 1024 && p.skip_div > 0) {
-      p.skip_tiles_per_b0 = p.tiles_m / 2 * p.tiles_n * p.nb[1] * p.nb[2] * p.nb[3];
-      p.skip_b0_scale = 1;
+    if (skip_on) {  // per pair unit of b0 (a b0 pair when pair_b0)
+      p.skip_tiles_per_b0 = (p.pair_b0 ? p.tiles_m : p.tiles_m / 2) * p.tiles_n * p.nb[1] * p.nb[2] * p.nb[3];
+      p.skip_b0_scale = p.pair_b0 ? 2 : 1;
     }
-    set_divisors(p.tiles_m / 2);
+    if (p.pair_b0) p.nb[0] /= 2;  // the kernel walks b0 pairs, b0 = 2 b' + rank
+    set_divisors(p.pair_b0 ? p.tiles_m : p.tiles_m / 2);
     const int grid = 2 * (int)std::min<long long>(tiles / 2, g_num_sms / 2);
     switch (bn) {
       case 256: return launch_ring<256, 3, 2, true>(tm_lam, tm2_whi, tm2_wlo, p, grid, st);
